@@ -1,0 +1,107 @@
+"""ctypes binding of oracle/csrc/oracle.c — TEST INFRASTRUCTURE / CPU
+BASELINE ONLY (never imported by the product package)."""
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "build", "liboracle.so")
+_lib = None
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        L.or_max_threads.restype = ctypes.c_int
+        L.or_spmv_csr.argtypes = [_I64, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.or_spmv_sellp.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.or_spmv_ell.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.or_spmv_coo.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.or_dot.argtypes = [_I64, _P, _P, ctypes.c_int]
+        L.or_dot.restype = ctypes.c_double
+        L.or_cg_sellp.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, ctypes.c_double, _I64, _P, _P,
+                                  ctypes.c_int]
+        L.or_cg_sellp.restype = _I64
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def max_threads():
+    return lib().or_max_threads()
+
+
+class Prepared:
+    """Host arrays of one matrix in the C oracle's layout (int32 columns,
+    int64 offsets), converted once so timed calls only run the fold."""
+
+    def __init__(self, m):
+        self.nrows, self.ncols = int(m.nrows), int(m.ncols)
+        self.col = np.ascontiguousarray(np.asarray(m.col_idx), dtype=np.int32)
+        self.val = np.ascontiguousarray(np.asarray(m.values), dtype=np.float64)
+        if hasattr(m, "slice_sets"):
+            self.kind = "sellp"
+            self.ss = int(m.slice_size)
+            self.sets = np.ascontiguousarray(np.asarray(m.slice_sets), dtype=np.int64)
+            self.lengths = np.ascontiguousarray(np.asarray(m.row_lengths), dtype=np.int64)
+        elif hasattr(m, "stride"):
+            self.kind = "ell"
+            self.stride = int(m.stride)
+            self.lengths = np.ascontiguousarray(np.asarray(m.row_lengths), dtype=np.int64)
+        elif hasattr(m, "row_ptrs"):
+            self.kind = "csr"
+            self.ptrs = np.ascontiguousarray(np.asarray(m.row_ptrs), dtype=np.int64)
+        else:
+            self.kind = "coo"
+            self.row = np.ascontiguousarray(np.asarray(m.row_idx), dtype=np.int32)
+
+    def spmv(self, x, y=None, nthreads=0):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if y is None:
+            y = np.empty(self.nrows, dtype=np.float64)
+        L = lib()
+        if self.kind == "csr":
+            L.or_spmv_csr(self.nrows, _p(self.ptrs), _p(self.col), _p(self.val), _p(x), _p(y), nthreads)
+        elif self.kind == "sellp":
+            L.or_spmv_sellp(self.nrows, self.ss, _p(self.sets), _p(self.col), _p(self.val),
+                            _p(self.lengths), _p(x), _p(y), nthreads)
+        elif self.kind == "ell":
+            L.or_spmv_ell(self.nrows, self.stride, _p(self.col), _p(self.val), _p(self.lengths),
+                          _p(x), _p(y), nthreads)
+        else:
+            L.or_spmv_coo(self.nrows, len(self.val), _p(self.row), _p(self.col), _p(self.val),
+                          _p(x), _p(y), nthreads)
+        return y
+
+    def cg(self, b, tol, max_iters, nthreads=0):
+        assert self.kind == "sellp"
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.nrows, dtype=np.float64)
+        hist = np.empty(max_iters + 1, dtype=np.float64)
+        it = lib().or_cg_sellp(self.nrows, self.ss, _p(self.sets), _p(self.col), _p(self.val),
+                               _p(self.lengths), _p(b), tol, max_iters, _p(x), _p(hist), nthreads)
+        if it < 0:
+            raise RuntimeError("CG breakdown")
+        return x, hist[: it + 1]
+
+
+def dot(a, b, nthreads=0):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return lib().or_dot(len(a), _p(a), _p(b), nthreads)
