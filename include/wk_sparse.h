@@ -1,0 +1,264 @@
+/*
+ * wk_sparse.h — C ABI of the B200-native sparse fp64 hot path
+ * (libwk_sparse.so, built for sm_100a).
+ *
+ * Drop-in boundary. The reference (`warpkit`, arXiv 2006.14290 workbench)
+ * exposes this path as Python operations behind its registry
+ * (`warpkit/dispatch.py:79-125`): `spmv_coo/csr/sellp(m, x, exec)`
+ * (`kernels.py:409-418`), `cg_solve(m, b, tol, max_iters, exec)`
+ * (`kernels.py:283`), plus the format conversions `coo_to_csr` /
+ * `coo_to_sellp` (`sparse.py:212-242`). Its uncompiled CUDA fixtures give the
+ * C shapes a native binding would take: `csr_spmv(nrows, row_ptrs, col_idx,
+ * vals, x, y)` (tests/golden/src/cuda/matrix/csr_kernels.cu:30-31),
+ * `coo_spmv(nnz, ...)` (coo_kernels.cu:34-35), `sellp_spmv(nrows, nslices,
+ * slice_sets, col_idx, ...)` (sellp_kernels.cu:28-30), `cg_update(n, alpha,
+ * beta, ..., stream)` (solver/cg_kernels.cu:35-36), `exec_settings{stream,
+ * device_id}` (base/types.cuh:11-14). Each entry point below cites the
+ * interface it replaces.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (current CUDA device) unless the
+ *     name starts with `h_`. The library never frees caller memory.
+ *   - Values are IEEE binary64; column/row indices are int32; offsets that
+ *     index stored entries (slice_sets) are int64. The reference stores int64
+ *     indices (sparse.py:21-25); int32 halves index traffic and covers every
+ *     configuration (nnz < 2^31).
+ *   - `stream` is a cudaStream_t passed as void*. Every call is asynchronous
+ *     on that stream; only functions documented as "synchronises" block.
+ *   - Return value: 0 on success, a cudaError_t value for CUDA failures, or a
+ *     WK_ERR_* code; `wk_last_error()` gives a message (thread-local).
+ */
+#ifndef WK_SPARSE_H
+#define WK_SPARSE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* wk_stream_t;
+
+enum {
+    WK_OK = 0,
+    WK_ERR_INVALID = 1001,   /* bad argument (ValueError in the reference)             */
+    WK_ERR_DIMENSION = 1002, /* errors.py:47-48 DimensionMismatch                      */
+    WK_ERR_BREAKDOWN = 1003, /* errors.py:55-56 BreakdownError (p.Ap <= 0, rho == 0 …) */
+    WK_ERR_SLICE = 1004      /* errors.py:51-52 InvalidSliceSize                        */
+};
+
+enum { WK_FMT_CSR = 0, WK_FMT_COO = 1, WK_FMT_ELL = 2, WK_FMT_SELLP = 3, WK_FMT_HYBRID = 4 };
+
+/* CSR SpMV strategies: STREAM = nnz-chunked, shared-memory staged,
+ * load-balanced (bitwise for rows <= 1024 entries); SUBWARP = one
+ * power-of-two tile of lanes per row (kernels.py:163-196). */
+enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1 };
+
+const char* wk_last_error(void);
+int wk_version(void);
+/* number of SMs of the current device */
+int wk_device_sm_count(void);
+
+/* ---- SpMV: y = A x ------------------------------------------------------ */
+
+/* replaces spmv_sellp (kernels.py:417-418 -> 116-157); sellp_spmv fixture
+ * (sellp_kernels.cu:28-30). Bitwise equal to dense_spmv_reference.
+ * row_lengths is only read when x[0] is not finite. */
+int wk_spmv_sellp_f64(int64_t nrows, int64_t ncols, int64_t slice_size, const int64_t* slice_sets,
+                      const int32_t* col_idx, const double* values, const int32_t* row_lengths,
+                      const double* x, double* y, wk_stream_t stream);
+
+/* ELL = SELL-P with one slice of stride `stride` >= nrows (no reference). */
+int wk_spmv_ell_f64(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int32_t* col_idx,
+                    const double* values, const int32_t* row_lengths, const double* x, double* y,
+                    wk_stream_t stream);
+
+/* replaces spmv_csr (kernels.py:413-414 -> 163-203); csr_spmv fixture
+ * (csr_kernels.cu:30-31). `plan` (wk_csr_plan_bytes) is required for
+ * WK_CSR_STREAM; subwarp_size <= 0 picks next_pow2(nnz/nrows) <= 32. */
+int wk_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idx,
+                    const double* values, const double* x, double* y, int32_t strategy, int32_t subwarp_size,
+                    void* plan, wk_stream_t stream);
+int64_t wk_csr_plan_chunks(int64_t nnz);
+int64_t wk_csr_plan_bytes(int64_t nnz);
+int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream);
+
+/* replaces spmv_coo (kernels.py:409-410 -> 209-264); coo_spmv fixture
+ * (coo_kernels.cu:34-35). Entries sorted row-major. accumulate = 0 zero-fills y. */
+int wk_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_idx, const int32_t* col_idx,
+                    const double* values, const double* x, double* y, int32_t accumulate, wk_stream_t stream);
+
+/* Hybrid = ELL(width) + sorted COO remainder (no reference; Ginkgo hybrid). */
+int wk_spmv_hybrid_f64(int64_t nrows, int64_t ncols, int64_t ell_width, int64_t ell_stride,
+                       const int32_t* ell_col, const double* ell_val, const int32_t* ell_row_lengths,
+                       int64_t coo_nnz, const int32_t* coo_row, const int32_t* coo_col, const double* coo_val,
+                       const double* x, double* y, wk_stream_t stream);
+
+/* Format-generic operand used by wk_spmv and the solvers. Fields not used by
+ * `format` are ignored. HYBRID uses the ELL fields plus coo_*. */
+typedef struct wk_matrix {
+    int32_t format;
+    int32_t csr_strategy;   /* CSR: WK_CSR_* */
+    int32_t subwarp_size;   /* CSR subwarp: tile size (<= 0: auto) */
+    int32_t reserved;
+    int64_t nrows, ncols, nnz;
+    const int32_t* row_ptrs;  /* CSR */
+    const int32_t* row_idx;   /* COO */
+    const int32_t* col_idx;   /* CSR, COO, ELL, SELLP, HYBRID(ell part) */
+    const double* values;
+    int64_t slice_size;       /* SELLP */
+    const int64_t* slice_sets;
+    int64_t width, stride;    /* ELL, HYBRID */
+    const int32_t* row_lengths; /* ELL, SELLP, HYBRID */
+    int64_t coo_nnz;          /* HYBRID */
+    const int32_t* coo_row;
+    const int32_t* coo_col;
+    const double* coo_val;
+    void* plan;               /* CSR stream plan */
+} wk_matrix;
+
+int wk_spmv(const wk_matrix* A, const double* x, double* y, wk_stream_t stream);
+/* same, but the launch is a no-op while *skip != 0 (device flag) */
+int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t* skip, wk_stream_t stream);
+
+/* ---- BLAS-1 (replaces numpy `@`, `+`, `*` in cg_solve, kernels.py:301-329;
+ *      host_dot/cublasDdot fixture cg_kernels.cu:26-33; residual_norm
+ *      residual_check.cu:17-32; axpy/scale_add cg_kernels.cu:7-21) ------- */
+
+/* bytes of reduction workspace (partials + ticket); zero it once before first use */
+int64_t wk_reduce_workspace_bytes(void);
+/* *result (device) = x . y, deterministic two-level reduction */
+int wk_dot_f64(int64_t n, const double* x, const double* y, double* result, void* workspace, wk_stream_t stream);
+/* *result (device) = ||x||_2 */
+int wk_norm2_f64(int64_t n, const double* x, double* result, void* workspace, wk_stream_t stream);
+/* y = y + alpha * x (separately rounded, like numpy) */
+int wk_axpy_f64(int64_t n, double alpha, const double* x, double* y, wk_stream_t stream);
+/* y = x + beta * y  (p = r + beta p) */
+int wk_xpby_f64(int64_t n, const double* x, double beta, double* y, wk_stream_t stream);
+/* x = alpha * x */
+int wk_scal_f64(int64_t n, double alpha, double* x, wk_stream_t stream);
+/* batched dots: result[i] = V_i . w for i < k, V row-major k x ld (CGS) */
+int wk_multidot_f64(int64_t n, int64_t k, const double* V, int64_t ld, const double* w, double* result,
+                    void* workspace, wk_stream_t stream);
+/* dst[i] = src[idx[i]] (halo pack) */
+int wk_gather_f64(int64_t n, const int32_t* idx, const double* src, double* dst, wk_stream_t stream);
+
+/* ---- conversions (replace coo_to_csr / coo_to_sellp, sparse.py:212-242;
+ *      CSR->ELL / Hybrid have no reference). Bit-exact copies. ----------- */
+
+/* row_lengths[r] = row_ptrs[r+1]-row_ptrs[r] */
+int wk_csr_row_lengths(int64_t nrows, const int32_t* row_ptrs, int32_t* row_lengths, wk_stream_t stream);
+/* *result (device, int64) = max row length */
+int wk_csr_max_row_length(int64_t nrows, const int32_t* row_ptrs, int64_t* result, wk_stream_t stream);
+/* hist[min(len, nbins-1)] += 1 ; hist zeroed by the call */
+int wk_csr_row_length_histogram(int64_t nrows, const int32_t* row_ptrs, int64_t nbins, int64_t* hist,
+                                wk_stream_t stream);
+/* SELL-P pass 1: slice_sets[0..nslices] (cumulative widths, sparse.py:225-229) and
+ * int32 row_lengths. scan_ws: wk_scan_workspace_bytes(nslices) bytes. */
+int wk_csr_to_sellp_sets(int64_t nrows, int64_t slice_size, const int32_t* row_ptrs, int64_t* slice_sets,
+                         int32_t* row_lengths, void* scan_ws, wk_stream_t stream);
+/* SELL-P pass 2: scatter (sparse.py:230-241) incl. zero padding. */
+int wk_csr_to_sellp_fill(int64_t nrows, int64_t slice_size, const int32_t* row_ptrs, const int32_t* col_idx,
+                         const double* values, const int64_t* slice_sets, int32_t* s_col, double* s_val,
+                         wk_stream_t stream);
+/* ELL(width, stride) from CSR: each row's first min(len, width) entries,
+ * padding (0, 0.0); e_row_lengths = min(len, width). Also the ELL part of Hybrid. */
+int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32_t* row_ptrs,
+                       const int32_t* col_idx, const double* values, int32_t* e_col, double* e_val,
+                       int32_t* e_row_lengths, wk_stream_t stream);
+/* Hybrid COO part, pass 1: offsets[0..nrows] = exclusive scan of max(len-width, 0) */
+int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs, int64_t* offsets, void* scan_ws,
+                          wk_stream_t stream);
+/* Hybrid COO part, pass 2 */
+int wk_hybrid_coo_fill(int64_t nrows, int64_t width, const int32_t* row_ptrs, const int32_t* col_idx,
+                       const double* values, const int64_t* offsets, int32_t* c_row, int32_t* c_col,
+                       double* c_val, wk_stream_t stream);
+/* sorted COO -> CSR row_ptrs (sparse.py:212-216) */
+int wk_coo_to_csr_ptrs(int64_t nrows, int64_t nnz, const int32_t* row_idx, int32_t* row_ptrs, wk_stream_t stream);
+/* CSR -> COO row indices */
+int wk_csr_to_coo_rows(int64_t nrows, const int32_t* row_ptrs, int32_t* row_idx, wk_stream_t stream);
+
+/* ---- scans (device-wide, decoupled three-pass) -------------------------- */
+int64_t wk_scan_workspace_bytes(int64_t n);
+/* out[0] = 0, out[i+1] = out[i] + in[i]  (n+1 outputs) */
+int wk_exclusive_scan_i64(int64_t n, const int64_t* in, int64_t* out, void* ws, wk_stream_t stream);
+
+/* ---- synthetic matrices (device generators) ----------------------------- */
+
+/* Constant-coefficient stencil on an nx*ny*nz grid (row r = (k*ny+j)*nx+i),
+ * points given on the host; columns ascend. Call with col_idx == NULL to get
+ * row_ptrs (n+1, int32) only; then again with storage for row_ptrs[n]
+ * entries. Restates corpus.py:33-50 for 3-D. scan_ws: wk_scan_workspace_bytes(n). */
+int wk_gen_stencil_csr(int64_t nx, int64_t ny, int64_t nz, int32_t npoints, const int32_t* h_dx,
+                       const int32_t* h_dy, const int32_t* h_dz, const double* h_values, int32_t* row_ptrs,
+                       int32_t* col_idx, double* values, void* scan_ws, wk_stream_t stream);
+/* R-MAT edges [edge_lo, edge_lo+count): key = row * 2^scale + col, value U[0,1)
+ * (oracle/corpus_ref.py rmat_edges restates the same hash) */
+int wk_gen_rmat_edges(int32_t scale, int32_t edge_factor, double a, double b, double c, uint64_t seed,
+                      int64_t edge_lo, int64_t count, int64_t* keys, double* values, wk_stream_t stream);
+/* duplicate summation over keys sorted stably (sparse.py:73-79):
+ * pass 1 flags[i] = (i == 0 || key[i] != key[i-1]) scanned into offsets (n+1) */
+int wk_coo_unique_offsets(int64_t n, const int64_t* keys, int64_t* offsets, void* scan_ws, wk_stream_t stream);
+/* pass 2: out entry per unique key (row = key / ncols, col = key % ncols),
+ * value = 0.0 + v1 + v2 + ... in order */
+int wk_coo_sum_duplicates(int64_t n, int64_t ncols, const int64_t* keys, const double* values,
+                          const int64_t* offsets, int32_t* row, int32_t* col, double* out_values,
+                          wk_stream_t stream);
+
+/* ---- Krylov solvers (replace cg_solve, kernels.py:283-331; BiCGSTAB and
+ *      GMRES(m) have no reference). x, hist are device arrays; hist holds
+ *      max_iters + 1 entries; *iterations (host) receives the count.
+ *      Synchronises. Returns WK_ERR_BREAKDOWN on breakdown. ------------- */
+
+int64_t wk_cg_workspace_bytes(int64_t n);
+int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, double* x, double* hist,
+                int64_t* iterations, void* workspace, wk_stream_t stream);
+int64_t wk_bicgstab_workspace_bytes(int64_t n);
+int wk_bicgstab_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, double* x,
+                      double* hist, int64_t* iterations, void* workspace, wk_stream_t stream);
+int64_t wk_gmres_workspace_bytes(int64_t n, int32_t restart);
+int wk_gmres_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, int32_t restart,
+                   double* x, double* hist, int64_t* iterations, void* workspace, wk_stream_t stream);
+
+/* ---- CG building blocks for the row-block distributed solver. The caller
+ *      all-reduces the local dot results between steps (NCCL). State layout:
+ *      wk_cg_state (device). ------------------------------------------- */
+typedef struct wk_cg_state {
+    double rho;        /* r.r of the current residual                        */
+    double pq;         /* p.Ap (local, then all-reduced by the caller)        */
+    double rr;         /* r.r after the update (local, then all-reduced)      */
+    double threshold;  /* tol * ||b||                                          */
+    double alpha, beta;
+    int64_t iteration;
+    int64_t max_iters;
+    int32_t done;      /* converged / max_iters reached / breakdown          */
+    int32_t breakdown;
+} wk_cg_state;
+
+/* rho := b.b (local), x = 0, r = p = b */
+int wk_cg_init_local(int64_t n, const double* b, double* x, double* r, double* p, wk_cg_state* state,
+                     void* workspace, wk_stream_t stream);
+/* after all-reduce of rho: threshold, hist[0], done */
+int wk_cg_init_finish(wk_cg_state* state, double tol, int64_t max_iters, double* hist, wk_stream_t stream);
+/* state->pq = p.q (local) ; skipped when done */
+int wk_cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* state, void* workspace,
+                 wk_stream_t stream);
+/* after all-reduce of pq: breakdown check, alpha, iteration += 1 */
+int wk_cg_step_alpha(wk_cg_state* state, wk_stream_t stream);
+/* x += alpha p ; unless replacement (iteration % 50 == 0): r -= alpha q and
+ * state->rr = r.r (local) */
+int wk_cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* state,
+                    void* workspace, wk_stream_t stream);
+/* replacement iteration only: r = b - q (q = A x) ; state->rr = r.r (local) */
+int wk_cg_replace_r(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state, void* workspace,
+                    wk_stream_t stream);
+/* after all-reduce of rr: hist, beta, rho := rr, done */
+int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream);
+/* p = r + beta p ; skipped when done */
+int wk_cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* state, wk_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WK_SPARSE_H */

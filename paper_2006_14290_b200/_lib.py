@@ -1,0 +1,159 @@
+"""ctypes binding of libwk_sparse.so (C ABI declared in include/wk_sparse.h).
+
+The library is built in-tree (`make -C paper_2006_14290_b200`, or
+`__graft_entry__.build()`); loading fails loudly if it is missing — there
+is no CPU fallback anywhere in the package.
+"""
+
+import ctypes
+import os
+
+from .errors import BreakdownError, DeviceError, DimensionMismatch, InvalidSliceSize, NativeLibraryMissing
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libwk_sparse.so")
+
+WK_OK = 0
+WK_ERR_INVALID = 1001
+WK_ERR_DIMENSION = 1002
+WK_ERR_BREAKDOWN = 1003
+WK_ERR_SLICE = 1004
+
+WK_FMT_CSR, WK_FMT_COO, WK_FMT_ELL, WK_FMT_SELLP, WK_FMT_HYBRID = range(5)
+WK_CSR_STREAM, WK_CSR_SUBWARP = 0, 1
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+F64 = ctypes.c_double
+U64 = ctypes.c_uint64
+
+
+class WkMatrix(ctypes.Structure):
+    """Mirror of `wk_matrix` (include/wk_sparse.h)."""
+
+    _fields_ = [
+        ("format", I32), ("csr_strategy", I32), ("subwarp_size", I32), ("reserved", I32),
+        ("nrows", I64), ("ncols", I64), ("nnz", I64),
+        ("row_ptrs", P), ("row_idx", P), ("col_idx", P), ("values", P),
+        ("slice_size", I64), ("slice_sets", P),
+        ("width", I64), ("stride", I64), ("row_lengths", P),
+        ("coo_nnz", I64), ("coo_row", P), ("coo_col", P), ("coo_val", P),
+        ("plan", P),
+    ]
+
+
+class WkCgState(ctypes.Structure):
+    _fields_ = [("rho", F64), ("pq", F64), ("rr", F64), ("threshold", F64), ("alpha", F64), ("beta", F64),
+                ("iteration", I64), ("max_iters", I64), ("done", I32), ("breakdown", I32)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "wk_last_error": (ctypes.c_char_p, []),
+    "wk_version": (ctypes.c_int, []),
+    "wk_device_sm_count": (ctypes.c_int, []),
+    "wk_spmv_sellp_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, P, P]),
+    "wk_spmv_ell_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, P, P, P]),
+    "wk_spmv_csr_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, I32, P, P]),
+    "wk_csr_plan_chunks": (I64, [I64]),
+    "wk_csr_plan_bytes": (I64, [I64]),
+    "wk_csr_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
+    "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),
+    "wk_spmv_hybrid_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P]),
+    "wk_spmv": (ctypes.c_int, [P, P, P, P]),
+    "wk_spmv_masked": (ctypes.c_int, [P, P, P, P, P]),
+    "wk_reduce_workspace_bytes": (I64, []),
+    "wk_dot_f64": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_norm2_f64": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_axpy_f64": (ctypes.c_int, [I64, F64, P, P, P]),
+    "wk_xpby_f64": (ctypes.c_int, [I64, P, F64, P, P]),
+    "wk_scal_f64": (ctypes.c_int, [I64, F64, P, P]),
+    "wk_multidot_f64": (ctypes.c_int, [I64, I64, P, I64, P, P, P, P]),
+    "wk_gather_f64": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_csr_row_lengths": (ctypes.c_int, [I64, P, P, P]),
+    "wk_csr_max_row_length": (ctypes.c_int, [I64, P, P, P]),
+    "wk_csr_row_length_histogram": (ctypes.c_int, [I64, P, I64, P, P]),
+    "wk_csr_to_sellp_sets": (ctypes.c_int, [I64, I64, P, P, P, P, P]),
+    "wk_csr_to_sellp_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P]),
+    "wk_csr_to_ell_fill": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, P, P]),
+    "wk_hybrid_coo_offsets": (ctypes.c_int, [I64, I64, P, P, P, P]),
+    "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
+    "wk_coo_to_csr_ptrs": (ctypes.c_int, [I64, I64, P, P, P]),
+    "wk_csr_to_coo_rows": (ctypes.c_int, [I64, P, P, P]),
+    "wk_scan_workspace_bytes": (I64, [I64]),
+    "wk_exclusive_scan_i64": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_gen_stencil_csr": (ctypes.c_int, [I64, I64, I64, I32, P, P, P, P, P, P, P, P, P]),
+    "wk_gen_rmat_edges": (ctypes.c_int, [I32, I32, F64, F64, F64, U64, I64, I64, P, P, P]),
+    "wk_coo_unique_offsets": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_coo_sum_duplicates": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P]),
+    "wk_cg_workspace_bytes": (I64, [I64]),
+    "wk_cg_solve": (ctypes.c_int, [P, P, F64, I64, P, P, P, P, P]),
+    "wk_bicgstab_workspace_bytes": (I64, [I64]),
+    "wk_bicgstab_solve": (ctypes.c_int, [P, P, F64, I64, P, P, P, P, P]),
+    "wk_gmres_workspace_bytes": (I64, [I64, I32]),
+    "wk_gmres_solve": (ctypes.c_int, [P, P, F64, I64, I32, P, P, P, P, P]),
+    "wk_cg_init_local": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
+    "wk_cg_init_finish": (ctypes.c_int, [P, F64, I64, P, P]),
+    "wk_cg_dot_pq": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_cg_step_alpha": (ctypes.c_int, [P, P]),
+    "wk_cg_update_xr": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
+    "wk_cg_replace_r": (ctypes.c_int, [I64, P, P, P, P, P, P]),
+    "wk_cg_step_beta": (ctypes.c_int, [P, P, P]),
+    "wk_cg_update_p": (ctypes.c_int, [I64, P, P, P, P]),
+}
+
+EXPORTED = tuple(sorted(_SIGS))
+
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes library handle."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} not found; build it with `make -C {_HERE}` or __graft_entry__.build() — "
+            "this package has no CPU fallback")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise NativeLibraryMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    msg = load().wk_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = ""):
+    """Map a libwk_sparse status to the reference's exception types."""
+    if rc == WK_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == WK_ERR_BREAKDOWN:
+        raise BreakdownError(msg)
+    if rc == WK_ERR_DIMENSION:
+        raise DimensionMismatch(msg)
+    if rc == WK_ERR_SLICE:
+        raise InvalidSliceSize(msg)
+    if rc == WK_ERR_INVALID:
+        raise ValueError(msg)
+    raise DeviceError(rc, msg)
+
+
+def call(name: str, *args):
+    """Invoke `name` and raise on a non-zero status."""
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc

@@ -1,0 +1,105 @@
+// Shared helpers for the wk_* C-ABI library (sm_100a only).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/wk_sparse.h"
+
+namespace cg = cooperative_groups;
+
+namespace wk {
+
+// ---- error plumbing: every C entry point returns a status and records a
+// thread-local message retrievable through wk_last_error() --------------------
+void set_error(const char* fmt, ...);
+void clear_error();
+
+#define WK_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            ::wk::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),     \
+                            __FILE__, __LINE__);                                        \
+            return (int)_e;                                                             \
+        }                                                                               \
+    } while (0)
+
+#define WK_REQUIRE(cond, code, ...)                                                     \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            ::wk::set_error(__VA_ARGS__);                                               \
+            return (code);                                                              \
+        }                                                                               \
+    } while (0)
+
+#define WK_LAUNCH_CHECK()                                                               \
+    do {                                                                                \
+        cudaError_t _e = cudaGetLastError();                                            \
+        if (_e != cudaSuccess) {                                                        \
+            ::wk::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \
+                            __FILE__, __LINE__);                                        \
+            return (int)_e;                                                             \
+        }                                                                               \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Number of SMs of the current device (cached per device).
+int sm_count();
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- device helpers ------------------------------------------------------------
+
+// Streaming loads for matrix data that is touched exactly once per SpMV:
+// evict-first in L2 so the x vector (gathered, reused) stays resident.
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ int2 ld_stream(const int2* p) { return __ldcs(p); }
+__device__ __forceinline__ int4 ld_stream(const int4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(double* p, double v) { __stcs(p, v); }
+
+// Gathered x: read-only path (L1-allocating) — neighbouring rows reuse it.
+__device__ __forceinline__ double ld_x(const double* x, int c) { return __ldg(x + c); }
+
+// Separately rounded multiply-add, matching the reference's Python floats
+// (sparse.py:391-395). The library is also compiled with -fmad=false.
+__device__ __forceinline__ double mul_add_rn(double acc, double v, double xv) {
+    return __dadd_rn(acc, __dmul_rn(v, xv));
+}
+
+// Butterfly all-reduce over a power-of-two tile: exactly log2(size)
+// shfl_xor rounds (kernels.py:35-49, reduce.cuh:8-16) expressed with
+// cooperative-groups tiles.
+template <unsigned Size, typename T, typename Parent>
+__device__ __forceinline__ T reduce_subwarp(const cg::thread_block_tile<Size, Parent>& tile, T v) {
+#pragma unroll
+    for (unsigned mask = Size / 2; mask > 0; mask >>= 1) v += tile.shfl_xor(v, mask);
+    return v;
+}
+
+// Deterministic block sum (fixed tree for a fixed blockDim): warp
+// butterflies, then warp 0 reduces the per-warp partials.
+template <int kThreads>
+__device__ __forceinline__ double block_sum(double v, double* smem /* >= kThreads/32 */) {
+    auto block = cg::this_thread_block();
+    auto warp = cg::tiled_partition<32>(block);
+    v = reduce_subwarp(warp, v);
+    if (warp.thread_rank() == 0) smem[warp.meta_group_rank()] = v;
+    block.sync();
+    double r = 0.0;
+    if (warp.meta_group_rank() == 0) {
+        r = warp.thread_rank() < kThreads / 32 ? smem[warp.thread_rank()] : 0.0;
+        r = reduce_subwarp(warp, r);
+    }
+    return r;  // valid in thread 0
+}
+
+}  // namespace wk

@@ -1,0 +1,301 @@
+// Format conversions on the device. Every output array is bit-identical to
+// the reference's host conversion:
+//   coo_to_csr     sparse.py:212-216  (row counts -> cumsum)
+//   coo_to_sellp   sparse.py:219-242  (per-slice max length -> cumulative
+//                  widths -> zero-filled storage -> k = sets[s]*ss + j*ss + l)
+//   CSR -> ELL     the same rule with one slice of stride `stride`
+//   CSR -> Hybrid  ELL(width) of each row's leading entries + row-major COO rest
+//
+// The scatter kernels stage a row block's CSR entries in shared memory with
+// coalesced loads and then write the column-major destination with
+// consecutive threads on consecutive addresses (the transpose-through-smem
+// pattern), so both sides of the conversion stream at full width.
+#include "reduce.cuh"
+
+namespace wk {
+
+constexpr int kConvThreads = 256;
+constexpr int kStageCap = 2048;  // staged entries per block (24 KB)
+
+__global__ void row_lengths_kernel(int64_t nrows, const int* __restrict__ ptrs, int* __restrict__ lengths) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r < nrows) lengths[r] = ptrs[r + 1] - ptrs[r];
+}
+
+// Column-major scatter of rows [r0, r0 + nrb) into destination slots
+// dst(j, l) = dbase + j * dstride + l for j < width, l < nrb_slots (rows
+// beyond nrows or j >= len are padding (0, 0.0)). Rows longer than `width`
+// are clipped (the Hybrid ELL part).
+__device__ void scatter_block(int64_t nrows, int64_t r0, int64_t nrb_slots, int64_t width, int64_t dbase,
+                              int64_t dstride, const int* __restrict__ ptrs, const int* __restrict__ col,
+                              const double* __restrict__ val, int* __restrict__ dcol, double* __restrict__ dval,
+                              int* s_col, double* s_val, int* s_ptr) {
+    const int64_t r_hi = (r0 + nrb_slots < nrows) ? r0 + nrb_slots : nrows;
+    const int64_t nreal = r_hi > r0 ? r_hi - r0 : 0;
+    const int64_t src_lo = nreal ? ptrs[r0] : 0;
+    const int64_t src_hi = nreal ? ptrs[r_hi] : 0;
+    const int64_t cnt = src_hi - src_lo;
+    const bool staged = cnt <= kStageCap && nrb_slots <= kConvThreads * 4;
+    if (staged) {
+        for (int64_t i = threadIdx.x; i <= nreal; i += kConvThreads) s_ptr[i] = ptrs[r0 + i] - int(src_lo);
+        for (int64_t i = threadIdx.x; i < cnt; i += kConvThreads) {
+            s_col[i] = __ldcs(col + src_lo + i);
+            s_val[i] = __ldcs(val + src_lo + i);
+        }
+        __syncthreads();
+    }
+    const int64_t total = width * nrb_slots;
+    const bool pow2 = (nrb_slots & (nrb_slots - 1)) == 0;
+    const int sh = pow2 ? __ffsll(nrb_slots) - 1 : 0;
+    for (int64_t e = threadIdx.x; e < total; e += kConvThreads) {
+        const int64_t j = pow2 ? (e >> sh) : e / nrb_slots;
+        const int64_t l = e - j * nrb_slots;
+        int c = 0;
+        double v = 0.0;
+        if (l < nreal) {
+            if (staged) {
+                const int lo = s_ptr[l], hi = s_ptr[l + 1];
+                if (j < hi - lo) {
+                    c = s_col[lo + j];
+                    v = s_val[lo + j];
+                }
+            } else {
+                const int64_t lo = ptrs[r0 + l], hi = ptrs[r0 + l + 1];
+                if (j < hi - lo) {
+                    c = col[lo + j];
+                    v = val[lo + j];
+                }
+            }
+        }
+        const int64_t d = dbase + j * dstride + l;
+        __stcs(dcol + d, c);
+        __stcs(dval + d, v);
+    }
+}
+
+__global__ void __launch_bounds__(kConvThreads)
+sellp_fill_kernel(int64_t nrows, int log2ss, const int* __restrict__ ptrs, const int* __restrict__ col,
+                  const double* __restrict__ val, const int64_t* __restrict__ sets, int* __restrict__ dcol,
+                  double* __restrict__ dval) {
+    __shared__ int s_col[kStageCap];
+    __shared__ double s_val[kStageCap];
+    __shared__ int s_ptr[kConvThreads * 4 + 1];
+    const int64_t s = blockIdx.x;
+    const int64_t ss = int64_t(1) << log2ss;
+    const int64_t w = sets[s + 1] - sets[s];
+    scatter_block(nrows, s * ss, ss, w, sets[s] * ss, ss, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
+}
+
+__global__ void __launch_bounds__(kConvThreads)
+ell_fill_kernel(int64_t nrows, int64_t width, int64_t stride, const int* __restrict__ ptrs,
+                const int* __restrict__ col, const double* __restrict__ val, int* __restrict__ dcol,
+                double* __restrict__ dval, int* __restrict__ dlen) {
+    __shared__ int s_col[kStageCap];
+    __shared__ double s_val[kStageCap];
+    __shared__ int s_ptr[kConvThreads * 4 + 1];
+    const int64_t r0 = int64_t(blockIdx.x) * kConvThreads;
+    const int64_t nslots = (r0 + kConvThreads <= stride) ? kConvThreads : stride - r0;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < nrows) {
+        const int len = ptrs[r + 1] - ptrs[r];
+        dlen[r] = len < width ? len : int(width);
+    }
+    scatter_block(nrows, r0, nslots, width, r0, stride, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
+}
+
+__global__ void hybrid_coo_fill_kernel(int64_t nrows, int64_t width, const int* __restrict__ ptrs,
+                                       const int* __restrict__ col, const double* __restrict__ val,
+                                       const int64_t* __restrict__ offsets, int* __restrict__ crow,
+                                       int* __restrict__ ccol, double* __restrict__ cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < nrows; r += warps) {
+        const int64_t lo = int64_t(ptrs[r]) + width, hi = ptrs[r + 1];
+        const int64_t o = offsets[r];
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+            crow[o + k - lo] = int(r);
+            ccol[o + k - lo] = col[k];
+            cval[o + k - lo] = val[k];
+        }
+    }
+}
+
+// first[r] style boundary fill: for sorted row indices, row_ptrs[r] =
+// lower_bound(row_idx, r), computed from the row changes.
+__global__ void coo_ptrs_kernel(int64_t nrows, int64_t nnz, const int* __restrict__ row, int* __restrict__ ptrs) {
+    const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k > nnz) return;
+    const int64_t prev = (k == 0) ? -1 : row[k - 1];
+    const int64_t cur = (k == nnz) ? nrows : row[k];
+    for (int64_t r = prev + 1; r <= cur; ++r) ptrs[r] = int(k);
+}
+
+__global__ void csr_rows_kernel(int64_t nrows, const int* __restrict__ ptrs, int* __restrict__ row) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < nrows; r += warps)
+        for (int64_t k = ptrs[r] + lane; k < ptrs[r + 1]; k += 32) row[k] = int(r);
+}
+
+static int warp_grid(int64_t nrows) {
+    int64_t b = ceil_div(nrows * 32, 256);
+    const int64_t cap = int64_t(sm_count()) * 32;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return int(b);
+}
+
+__global__ void __launch_bounds__(256) max_len_kernel(int64_t nrows, const int* __restrict__ ptrs,
+                                                      unsigned long long* __restrict__ result) {
+    unsigned long long m = 0;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += stride) {
+        const unsigned long long len = (unsigned long long)(ptrs[r + 1] - ptrs[r]);
+        m = len > m ? len : m;
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, m, d);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(result, m);
+}
+
+__global__ void __launch_bounds__(256) len_hist_kernel(int64_t nrows, int64_t nbins, const int* __restrict__ ptrs,
+                                                       unsigned long long* __restrict__ hist) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += stride) {
+        int64_t len = ptrs[r + 1] - ptrs[r];
+        if (len > nbins - 1) len = nbins - 1;
+        atomicAdd(hist + len, 1ull);
+    }
+}
+
+}  // namespace wk
+
+using namespace wk;
+
+extern "C" {
+
+int wk_csr_row_lengths(int64_t nrows, const int32_t* row_ptrs, int32_t* row_lengths, wk_stream_t stream) {
+    clear_error();
+    if (nrows == 0) return 0;
+    row_lengths_kernel<<<(unsigned)ceil_div(nrows, 256), 256, 0, as_stream(stream)>>>(nrows, row_ptrs, row_lengths);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_max_row_length(int64_t nrows, const int32_t* row_ptrs, int64_t* result, wk_stream_t stream) {
+    clear_error();
+    cudaStream_t st = as_stream(stream);
+    WK_CUDA(cudaMemsetAsync(result, 0, sizeof(int64_t), st));
+    if (nrows == 0) return 0;
+    int64_t blocks = ceil_div(nrows, 256);
+    if (blocks > int64_t(sm_count()) * 8) blocks = int64_t(sm_count()) * 8;
+    max_len_kernel<<<(unsigned)blocks, 256, 0, st>>>(nrows, row_ptrs, reinterpret_cast<unsigned long long*>(result));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_row_length_histogram(int64_t nrows, const int32_t* row_ptrs, int64_t nbins, int64_t* hist,
+                                wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(nbins >= 1, WK_ERR_INVALID, "nbins must be >= 1");
+    cudaStream_t st = as_stream(stream);
+    WK_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * size_t(nbins), st));
+    if (nrows == 0) return 0;
+    int64_t blocks = ceil_div(nrows, 256);
+    if (blocks > int64_t(sm_count()) * 8) blocks = int64_t(sm_count()) * 8;
+    len_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(nrows, nbins, row_ptrs,
+                                                      reinterpret_cast<unsigned long long*>(hist));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_to_sellp_sets(int64_t nrows, int64_t slice_size, const int32_t* row_ptrs, int64_t* slice_sets,
+                         int32_t* row_lengths, void* scan_ws, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(slice_size > 0 && (slice_size & (slice_size - 1)) == 0, WK_ERR_SLICE,
+               "slice_size must be a positive power of two, got %lld", (long long)slice_size);
+    cudaStream_t st = as_stream(stream);
+    const int64_t nslices = ceil_div(nrows, slice_size);
+    if (nrows) {
+        row_lengths_kernel<<<(unsigned)ceil_div(nrows, 256), 256, 0, st>>>(nrows, row_ptrs, row_lengths);
+        WK_LAUNCH_CHECK();
+    }
+    const int32_t* len = row_lengths;
+    auto width = [=] __device__(int64_t s) {
+        const int64_t lo = s * slice_size;
+        const int64_t hi = (lo + slice_size < nrows) ? lo + slice_size : nrows;
+        int64_t w = 0;
+        for (int64_t r = lo; r < hi; ++r) w = len[r] > w ? len[r] : w;
+        return w;
+    };
+    return exclusive_scan(nslices, width, slice_sets, scan_ws, st);
+}
+
+int wk_csr_to_sellp_fill(int64_t nrows, int64_t slice_size, const int32_t* row_ptrs, const int32_t* col_idx,
+                         const double* values, const int64_t* slice_sets, int32_t* s_col, double* s_val,
+                         wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(slice_size > 0 && (slice_size & (slice_size - 1)) == 0, WK_ERR_SLICE,
+               "slice_size must be a positive power of two, got %lld", (long long)slice_size);
+    const int64_t nslices = ceil_div(nrows, slice_size);
+    if (nslices == 0) return 0;
+    int l2 = 0;
+    while ((int64_t(1) << l2) < slice_size) ++l2;
+    sellp_fill_kernel<<<(unsigned)nslices, kConvThreads, 0, as_stream(stream)>>>(nrows, l2, row_ptrs, col_idx, values,
+                                                                               slice_sets, s_col, s_val);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32_t* row_ptrs,
+                       const int32_t* col_idx, const double* values, int32_t* e_col, double* e_val,
+                       int32_t* e_row_lengths, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(stride >= nrows, WK_ERR_INVALID, "ELL stride %lld < nrows %lld", (long long)stride,
+               (long long)nrows);
+    if (stride == 0) return 0;
+    ell_fill_kernel<<<(unsigned)ceil_div(stride, kConvThreads), kConvThreads, 0, as_stream(stream)>>>(
+        nrows, width, stride, row_ptrs, col_idx, values, e_col, e_val, e_row_lengths);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs, int64_t* offsets, void* scan_ws,
+                          wk_stream_t stream) {
+    clear_error();
+    auto rem = [=] __device__(int64_t r) {
+        const int64_t len = row_ptrs[r + 1] - row_ptrs[r];
+        return len > width ? len - width : int64_t(0);
+    };
+    return exclusive_scan(nrows, rem, offsets, scan_ws, as_stream(stream));
+}
+
+int wk_hybrid_coo_fill(int64_t nrows, int64_t width, const int32_t* row_ptrs, const int32_t* col_idx,
+                       const double* values, const int64_t* offsets, int32_t* c_row, int32_t* c_col,
+                       double* c_val, wk_stream_t stream) {
+    clear_error();
+    if (nrows == 0) return 0;
+    hybrid_coo_fill_kernel<<<warp_grid(nrows), 256, 0, as_stream(stream)>>>(nrows, width, row_ptrs, col_idx, values,
+                                                                            offsets, c_row, c_col, c_val);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_coo_to_csr_ptrs(int64_t nrows, int64_t nnz, const int32_t* row_idx, int32_t* row_ptrs, wk_stream_t stream) {
+    clear_error();
+    coo_ptrs_kernel<<<(unsigned)ceil_div(nnz + 1, 256), 256, 0, as_stream(stream)>>>(nrows, nnz, row_idx, row_ptrs);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_to_coo_rows(int64_t nrows, const int32_t* row_ptrs, int32_t* row_idx, wk_stream_t stream) {
+    clear_error();
+    if (nrows == 0) return 0;
+    csr_rows_kernel<<<warp_grid(nrows), 256, 0, as_stream(stream)>>>(nrows, row_ptrs, row_idx);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // extern "C"

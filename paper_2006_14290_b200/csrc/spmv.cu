@@ -1,0 +1,580 @@
+// SpMV kernels for B200 (sm_100a), fp64 values, int32 indices.
+//
+// Formats and their reference anchors:
+//   SELL-P  warpkit/sparse.py:147-209 (layout), kernels.py:116-157 (thread per
+//           row over the full slice width), sparse.py:397-417 (oracle fold)
+//   ELL     SELL-P with one slice of stride `stride` (no reference)
+//   CSR     kernels.py:163-203 (subwarp per row), sparse.py:384-396 (fold)
+//   COO     kernels.py:209-264 (segmented reduction + atomics), sparse.py:374-383
+//   Hybrid  ELL part + COO remainder (no reference; Ginkgo's hybrid format)
+//
+// Bit-exactness: the column-major kernels (SELL-P, ELL) and the CSR "stream"
+// kernel fold every row sequentially in stored order with separately rounded
+// multiply and add — the reference fold — so they are bitwise equal to the
+// oracle. The library is compiled with -fmad=false and the folds use
+// __dmul_rn/__dadd_rn explicitly. Padding slots hold (col 0, 0.0): adding
+// 0.0*x[0] never changes a fold (acc starts at +0.0 and x + (+-0) == x for
+// x != 0, +0 + -0 == +0) as long as x[0] is finite; if it is not, the
+// kernels switch to the `row_lengths`-bounded loop of the oracle.
+#include "common.cuh"
+
+namespace wk {
+
+constexpr int kSpmvThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Column-major sliced storage (SELL-P, ELL). Thread handles R adjacent rows of
+// one slice; R == 2 uses 128-bit value loads and 64-bit index loads.
+// ---------------------------------------------------------------------------
+template <int R, bool kEll>
+__global__ void __launch_bounds__(kSpmvThreads)
+sliced_spmv_kernel(int64_t nrows, int64_t ncols, int log2ss, int64_t ell_width, int64_t ell_stride,
+                   const int64_t* __restrict__ sets, const int* __restrict__ col,
+                   const double* __restrict__ val, const int* __restrict__ row_lengths,
+                   const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    const int64_t r0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * R;
+    if (r0 >= nrows) return;
+    const bool finite0 = ncols == 0 || isfinite(__ldg(x));
+    int64_t k, stride, width;
+    if (kEll) {
+        k = r0;
+        stride = ell_stride;
+        width = ell_width;
+    } else {
+        const int64_t s = r0 >> log2ss;
+        const int64_t s0 = __ldg(sets + s);
+        k = (s0 << log2ss) + (r0 & ((int64_t(1) << log2ss) - 1));
+        stride = int64_t(1) << log2ss;
+        width = __ldg(sets + s + 1) - s0;
+    }
+    if (R == 1) {
+        const int64_t len = finite0 ? width : row_lengths[r0];
+        double acc = 0.0;
+        int64_t j = 0;
+        for (; j + 4 <= len; j += 4) {
+            double v[4];
+            int c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                v[u] = ld_stream(val + k + u * stride);
+                c[u] = ld_stream(col + k + u * stride);
+            }
+            double xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u] = ld_x(x, c[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc = mul_add_rn(acc, v[u], xv[u]);
+            k += 4 * stride;
+        }
+        for (; j < len; ++j, k += stride) acc = mul_add_rn(acc, ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+        st_stream(y + r0, acc);
+    } else {
+        const bool has1 = r0 + 1 < nrows;
+        int64_t len0 = width, len1 = width;
+        if (!finite0) {
+            len0 = row_lengths[r0];
+            len1 = has1 ? row_lengths[r0 + 1] : 0;
+        }
+        const int64_t len = len0 > len1 ? len0 : len1;
+        double a0 = 0.0, a1 = 0.0;
+        int64_t j = 0;
+        if (finite0) {
+            for (; j + 4 <= len; j += 4) {
+                double2 v[4];
+                int2 c[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    v[u] = ld_stream(reinterpret_cast<const double2*>(val + k + u * stride));
+                    c[u] = ld_stream(reinterpret_cast<const int2*>(col + k + u * stride));
+                }
+                double x0[4], x1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    x0[u] = ld_x(x, c[u].x);
+                    x1[u] = ld_x(x, c[u].y);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    a0 = mul_add_rn(a0, v[u].x, x0[u]);
+                    a1 = mul_add_rn(a1, v[u].y, x1[u]);
+                }
+                k += 4 * stride;
+            }
+        }
+        for (; j < len; ++j, k += stride) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(val + k));
+            const int2 c = ld_stream(reinterpret_cast<const int2*>(col + k));
+            if (j < len0) a0 = mul_add_rn(a0, v.x, ld_x(x, c.x));
+            if (j < len1) a1 = mul_add_rn(a1, v.y, ld_x(x, c.y));
+        }
+        if (has1) {
+            // y + r0 is 16-byte aligned when y is (r0 even).
+            __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
+        } else {
+            st_stream(y + r0, a0);
+        }
+    }
+}
+
+static bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+static int log2i(int64_t v) {
+    int l = 0;
+    while ((int64_t(1) << l) < v) ++l;
+    return l;
+}
+
+int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, const int* col,
+                 const double* val, const int* row_lengths, const double* x, double* y,
+                 const int* skip, cudaStream_t st) {
+    if (nrows == 0) return 0;
+    const int l2 = log2i(ss);
+    const bool vec = ss >= 2 && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
+    if (vec) {
+        const int64_t threads = ceil_div(nrows, 2);
+        sliced_spmv_kernel<2, false><<<(unsigned)ceil_div(threads, kSpmvThreads), kSpmvThreads, 0, st>>>(
+            nrows, ncols, l2, 0, 0, sets, col, val, row_lengths, x, y, skip);
+    } else {
+        sliced_spmv_kernel<1, false><<<(unsigned)ceil_div(nrows, kSpmvThreads), kSpmvThreads, 0, st>>>(
+            nrows, ncols, l2, 0, 0, sets, col, val, row_lengths, x, y, skip);
+    }
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col,
+               const double* val, const int* row_lengths, const double* x, double* y, const int* skip,
+               cudaStream_t st) {
+    if (nrows == 0) return 0;
+    const bool vec = (stride % 2 == 0) && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
+    if (vec) {
+        const int64_t threads = ceil_div(nrows, 2);
+        sliced_spmv_kernel<2, true><<<(unsigned)ceil_div(threads, kSpmvThreads), kSpmvThreads, 0, st>>>(
+            nrows, ncols, 0, width, stride, nullptr, col, val, row_lengths, x, y, skip);
+    } else {
+        sliced_spmv_kernel<1, true><<<(unsigned)ceil_div(nrows, kSpmvThreads), kSpmvThreads, 0, st>>>(
+            nrows, ncols, 0, width, stride, nullptr, col, val, row_lengths, x, y, skip);
+    }
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// CSR "stream" (load-balanced, bitwise for rows of <= kCsrChunk entries).
+//
+// The nonzeros are cut into chunks of kCsrChunk entries; work item c owns the
+// rows whose first entry lies in chunk c (first[c] .. first[c+1]), so every
+// item covers < 2*kCsrChunk entries of short rows. The products v*x[c] of an
+// item are staged in shared memory with coalesced 128-bit loads, then each
+// thread folds whole rows sequentially from shared memory (the reference
+// fold, bit for bit). A "long" row (> kCsrChunk entries) is split across the
+// items its entries fall into; each item writes a partial and the last one to
+// arrive (atomic ticket) adds the partials in chunk order — deterministic,
+// but reassociated, so long rows are checked with the 1e-12 tolerance.
+// ---------------------------------------------------------------------------
+constexpr int kCsrChunk = 1024;
+constexpr int kCsrCap = 2 * kCsrChunk;
+
+__global__ void csr_plan_kernel(int64_t nrows, int64_t nnz, int64_t nchunks, const int* __restrict__ ptrs,
+                                int* __restrict__ first) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r > nrows) return;
+    // first[c] = min{ r : ptrs[r] >= c*S }, rows r in [0, nrows]; ptrs[nrows] = nnz.
+    // Only the virtual row r == nrows writes first[nchunks] (= nrows), so the
+    // last item also covers trailing empty rows.
+    int64_t hi = (r == nrows) ? nchunks : int64_t(ptrs[r]) / kCsrChunk;
+    if (r < nrows && hi > nchunks - 1) hi = nchunks - 1;
+    const int64_t lo = (r == 0) ? 0 : int64_t(ptrs[r - 1]) / kCsrChunk + 1;
+    for (int64_t c = lo; c <= hi; ++c) first[c] = int(r);
+}
+
+__device__ __forceinline__ double long_row_part(const int* __restrict__ col, const double* __restrict__ val,
+                                                const double* __restrict__ x, int64_t lo, int64_t hi,
+                                                double* red) {
+    double acc = 0.0;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += kSpmvThreads)
+        acc += __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+    return block_sum<kSpmvThreads>(acc, red);
+}
+
+// Partial slots: 2*c for the tail of a long row entering chunk c, 2*c+1 for
+// the head of a long row starting in chunk c.
+__device__ void long_row_finish(int64_t L, int64_t c_head, int64_t c_last, double* __restrict__ partials,
+                                unsigned* __restrict__ tickets, double* __restrict__ y) {
+    // caller: thread 0 only, after writing its partial
+    __threadfence();
+    const unsigned parts = unsigned(c_last - c_head + 1);
+    const unsigned t = atomicAdd(tickets + c_head, 1u);
+    if (t == parts - 1) {
+        __threadfence();
+        double acc = 0.0;
+        acc += __ldcg(partials + 2 * c_head + 1);
+        for (int64_t c = c_head + 1; c <= c_last; ++c) acc += __ldcg(partials + 2 * c);
+        y[L] = acc;
+        tickets[c_head] = 0;  // self-cleaning for the next call
+    }
+}
+
+__global__ void __launch_bounds__(kSpmvThreads)
+csr_stream_kernel(int64_t nrows, int64_t nnz, const int* __restrict__ ptrs, const int* __restrict__ col,
+                  const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                  const int* __restrict__ first, double* __restrict__ partials,
+                  unsigned* __restrict__ tickets, const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    __shared__ double prod[kCsrCap];
+    __shared__ double red[kSpmvThreads / 32];
+    const int64_t c = blockIdx.x;
+    const int64_t rb = first[c], re = first[c + 1];
+    const int64_t chunk_lo = c * kCsrChunk, chunk_hi = chunk_lo + kCsrChunk;
+
+    // (a) tail of a long row that started in an earlier chunk
+    if (rb > 0) {
+        const int64_t L = rb - 1;
+        const int64_t Ls = ptrs[L], Le = ptrs[rb];
+        if (Le - Ls > kCsrChunk && Le > chunk_lo) {
+            const int64_t hi = Le < chunk_hi ? Le : chunk_hi;
+            const double part = long_row_part(col, val, x, chunk_lo, hi, red);
+            if (threadIdx.x == 0) {
+                partials[2 * c] = part;
+                long_row_finish(L, Ls / kCsrChunk, (Le - 1) / kCsrChunk, partials, tickets, y);
+            }
+        }
+    }
+    if (rb >= re) return;
+    // (b) head of a long row that starts in this chunk (always the item's last row)
+    int64_t rs_end = re;
+    {
+        const int64_t L = re - 1;
+        const int64_t Ls = ptrs[L], Le = ptrs[re];
+        if (Le - Ls > kCsrChunk) {
+            rs_end = L;
+            const double part = long_row_part(col, val, x, Ls, chunk_hi, red);
+            if (threadIdx.x == 0) {
+                partials[2 * c + 1] = part;
+                long_row_finish(L, c, (Le - 1) / kCsrChunk, partials, tickets, y);
+            }
+        }
+    }
+    if (rb >= rs_end) return;
+    // (c) short rows: stage products, then fold row by row
+    const int64_t base = ptrs[rb];
+    const int64_t cnt = int64_t(ptrs[rs_end]) - base;  // < kCsrCap
+    const int64_t abase = base & ~int64_t(1);
+    const int64_t npairs = (base - abase + cnt + 1) >> 1;
+    for (int64_t i = threadIdx.x; i < npairs; i += kSpmvThreads) {
+        const int64_t k = abase + 2 * i;
+        if (k >= base && k + 1 < base + cnt) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(val + k));
+            const int2 cc = ld_stream(reinterpret_cast<const int2*>(col + k));
+            prod[k - base] = __dmul_rn(v.x, ld_x(x, cc.x));
+            prod[k + 1 - base] = __dmul_rn(v.y, ld_x(x, cc.y));
+        } else {
+            if (k >= base && k < base + cnt) prod[k - base] = __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+            if (k + 1 >= base && k + 1 < base + cnt)
+                prod[k + 1 - base] = __dmul_rn(ld_stream(val + k + 1), ld_x(x, ld_stream(col + k + 1)));
+        }
+    }
+    __syncthreads();
+    for (int64_t r = rb + threadIdx.x; r < rs_end; r += kSpmvThreads) {
+        const int64_t lo = int64_t(ptrs[r]) - base, hi = int64_t(ptrs[r + 1]) - base;
+        double acc = 0.0;
+        for (int64_t k = lo; k < hi; ++k) acc = __dadd_rn(acc, prod[k]);
+        y[r] = acc;
+    }
+}
+
+int64_t csr_stream_chunks(int64_t nnz) {
+    const int64_t n = ceil_div(nnz, kCsrChunk);
+    return n < 1 ? 1 : n;
+}
+
+// ---------------------------------------------------------------------------
+// CSR subwarp-per-row (Ginkgo "classical"; kernels.py:163-196): a tile of T
+// lanes strides the row, butterfly reduction, rank 0 writes. T == 1 is the
+// sequential thread-per-row fold (bitwise).
+// ---------------------------------------------------------------------------
+template <unsigned T>
+__global__ void __launch_bounds__(kSpmvThreads)
+csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __restrict__ col,
+                   const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                   const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    auto tile = cg::tiled_partition<T>(cg::this_thread_block());
+    const int64_t tiles_per_grid = int64_t(gridDim.x) * (kSpmvThreads / T);
+    for (int64_t row = int64_t(blockIdx.x) * (kSpmvThreads / T) + tile.meta_group_rank(); row < nrows;
+         row += tiles_per_grid) {
+        const int64_t lo = ptrs[row], hi = ptrs[row + 1];
+        double acc = 0.0;
+        for (int64_t k = lo + tile.thread_rank(); k < hi; k += T)
+            acc = mul_add_rn(acc, ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+        acc = reduce_subwarp(tile, acc);
+        if (tile.thread_rank() == 0) y[row] = acc;
+    }
+}
+
+int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const int* col, const double* val,
+               const double* x, double* y, int strategy, int subwarp, const int* first, double* partials,
+               unsigned* tickets, const int* skip, cudaStream_t st) {
+    (void)ncols;
+    if (nrows == 0) return 0;
+    if (strategy == WK_CSR_STREAM) {
+        WK_REQUIRE(first != nullptr && partials != nullptr && tickets != nullptr, WK_ERR_INVALID,
+                   "csr stream strategy needs a plan (wk_csr_plan_build)");
+        const int64_t nchunks = csr_stream_chunks(nnz);
+        csr_stream_kernel<<<(unsigned)nchunks, kSpmvThreads, 0, st>>>(nrows, nnz, ptrs, col, val, x, y, first,
+                                                                     partials, tickets, skip);
+        WK_LAUNCH_CHECK();
+        return 0;
+    }
+    WK_REQUIRE(strategy == WK_CSR_SUBWARP, WK_ERR_INVALID, "unknown CSR strategy %d", strategy);
+    int T = subwarp;
+    if (T <= 0) {  // auto: next power of two of the mean row length, clamped to [1, 32]
+        const int64_t avg = ceil_div(nnz, nrows);
+        T = 1;
+        while (T < avg && T < 32) T <<= 1;
+    }
+    const int64_t tiles_per_block = kSpmvThreads / T;
+    int64_t blocks = ceil_div(nrows, tiles_per_block);
+    const int64_t cap = int64_t(sm_count()) * 16;
+    if (blocks > cap) blocks = cap;
+    switch (T) {
+#define WK_SW(N) \
+    case N: csr_subwarp_kernel<N><<<(unsigned)blocks, kSpmvThreads, 0, st>>>(nrows, ptrs, col, val, x, y, skip); break;
+        WK_SW(1) WK_SW(2) WK_SW(4) WK_SW(8) WK_SW(16) WK_SW(32)
+#undef WK_SW
+        default:
+            WK_REQUIRE(false, WK_ERR_INVALID, "csr subwarp size must be a power of two <= 32, got %d", T);
+    }
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// COO: each warp owns a contiguous range of kCooPerWarp sorted entries and
+// walks it in batches of 32 (4 batches loaded up front for memory-level
+// parallelism). Within a batch a segmented inclusive scan keyed by row
+// (rows are sorted, so equal rows are contiguous) gives every segment's sum
+// at its tail lane. Rows that begin and end inside the warp's range are
+// stored directly; the first and last row of the range (possibly shared with
+// a neighbouring warp) go through atomicAdd. The running tail of lane 31 is
+// carried into the next batch (kernels.py:229-253 semantics: flush on row
+// change, merge equal-row tails, atomic at run heads).
+// ---------------------------------------------------------------------------
+constexpr int kCooPerWarp = 1024;
+
+__global__ void __launch_bounds__(kSpmvThreads)
+coo_kernel(int64_t nnz, int accumulate, const int* __restrict__ row, const int* __restrict__ col,
+           const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+           const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    const unsigned lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wlo = warp * kCooPerWarp;
+    if (wlo >= nnz) return;
+    const int64_t whi = (wlo + kCooPerWarp < nnz) ? wlo + kCooPerWarp : nnz;
+    const int first_row = row[wlo];
+    const int last_row = row[whi - 1];
+    int carry_row = -1;
+    double carry = 0.0;
+    for (int64_t b0 = wlo; b0 < whi; b0 += 4 * 32) {
+        int r[4];
+        double p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t k = b0 + u * 32 + lane;
+            r[u] = -1;
+            p[u] = 0.0;
+            if (k < whi) {
+                r[u] = ld_stream(row + k);
+                p[u] = __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (b0 + u * 32 >= whi) break;
+            int rr = r[u];
+            double v = p[u];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double pv = __shfl_up_sync(0xffffffffu, v, d);
+                const int pr = __shfl_up_sync(0xffffffffu, rr, d);
+                if (lane >= unsigned(d) && pr == rr) v += pv;
+            }
+            const int nr = __shfl_down_sync(0xffffffffu, rr, 1);
+            const bool valid = rr >= 0;
+            const bool tail = valid && (lane == 31 || nr != rr);
+            const int r0 = __shfl_sync(0xffffffffu, rr, 0);
+            // merge the carried tail into the first segment of this batch
+            if (carry_row >= 0) {
+                if (carry_row == r0) {
+                    if (tail && rr == r0) v += carry;
+                } else if (lane == 0) {
+                    if (carry_row == first_row || carry_row == last_row) atomicAdd(y + carry_row, carry);
+                    else y[carry_row] = accumulate ? y[carry_row] + carry : carry;
+                }
+            }
+            const int r31 = __shfl_sync(0xffffffffu, rr, 31);
+            const double v31 = __shfl_sync(0xffffffffu, v, 31);
+            if (tail && lane != 31) {
+                if (rr == first_row || rr == last_row) atomicAdd(y + rr, v);
+                else y[rr] = accumulate ? y[rr] + v : v;
+            }
+            if (r31 >= 0) {
+                carry_row = r31;
+                carry = v31;
+            } else {
+                carry_row = -1;
+            }
+        }
+    }
+    if (carry_row >= 0 && lane == 0) {
+        if (carry_row == first_row || carry_row == last_row) atomicAdd(y + carry_row, carry);
+        else y[carry_row] = accumulate ? y[carry_row] + carry : carry;
+    }
+}
+
+int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const double* val, const double* x,
+               double* y, int accumulate, const int* skip, cudaStream_t st) {
+    if (nrows == 0) return 0;
+    if (!accumulate) {
+        // skip-aware zero fill is not needed: a skipped SpMV leaves y untouched
+        // only in the solver loops, which never use COO with accumulate == 0
+        // behind a skip flag (they call wk_spmv with the full operator).
+        WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
+    }
+    if (nnz == 0) return 0;
+    const int64_t warps = ceil_div(nnz, kCooPerWarp);
+    const int64_t blocks = ceil_div(warps * 32, kSpmvThreads);
+    coo_kernel<<<(unsigned)blocks, kSpmvThreads, 0, st>>>(nnz, accumulate, row, col, val, x, y, skip);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // namespace wk
+
+// ============================ C ABI ==========================================
+using namespace wk;
+
+extern "C" {
+
+int wk_spmv_sellp_f64(int64_t nrows, int64_t ncols, int64_t slice_size, const int64_t* slice_sets,
+                      const int32_t* col_idx, const double* values, const int32_t* row_lengths, const double* x,
+                      double* y, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(slice_size > 0 && (slice_size & (slice_size - 1)) == 0, WK_ERR_SLICE,
+               "slice_size must be a positive power of two, got %lld", (long long)slice_size);
+    return launch_sellp(nrows, ncols, slice_size, slice_sets, col_idx, values, row_lengths, x, y, nullptr,
+                        as_stream(stream));
+}
+
+int wk_spmv_ell_f64(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int32_t* col_idx,
+                    const double* values, const int32_t* row_lengths, const double* x, double* y,
+                    wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(stride >= nrows, WK_ERR_INVALID, "ELL stride %lld < nrows %lld", (long long)stride,
+               (long long)nrows);
+    return launch_ell(nrows, ncols, width, stride, col_idx, values, row_lengths, x, y, nullptr, as_stream(stream));
+}
+
+int64_t wk_csr_plan_chunks(int64_t nnz) { return csr_stream_chunks(nnz); }
+
+int64_t wk_csr_plan_bytes(int64_t nnz) {
+    const int64_t c = csr_stream_chunks(nnz);
+    // first[c+1] int32 | pad | partials[2c] f64 | tickets[c] u32
+    return ceil_div((c + 1) * 4, 16) * 16 + 2 * c * 8 + ceil_div(c * 4, 16) * 16;
+}
+
+int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream) {
+    clear_error();
+    const int64_t c = csr_stream_chunks(nnz);
+    cudaStream_t st = as_stream(stream);
+    WK_CUDA(cudaMemsetAsync(plan, 0, size_t(wk_csr_plan_bytes(nnz)), st));
+    csr_plan_kernel<<<(unsigned)ceil_div(nrows + 1, 256), 256, 0, st>>>(nrows, nnz, c, row_ptrs,
+                                                                      reinterpret_cast<int*>(plan));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+static void csr_plan_views(void* plan, int64_t nnz, int** first, double** partials, unsigned** tickets) {
+    const int64_t c = csr_stream_chunks(nnz);
+    char* p = reinterpret_cast<char*>(plan);
+    *first = reinterpret_cast<int*>(p);
+    p += ceil_div((c + 1) * 4, 16) * 16;
+    *partials = reinterpret_cast<double*>(p);
+    p += 2 * c * 8;
+    *tickets = reinterpret_cast<unsigned*>(p);
+}
+
+int wk_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idx,
+                    const double* values, const double* x, double* y, int32_t strategy, int32_t subwarp_size,
+                    void* plan, wk_stream_t stream) {
+    clear_error();
+    int* first = nullptr;
+    double* partials = nullptr;
+    unsigned* tickets = nullptr;
+    if (plan != nullptr) csr_plan_views(plan, nnz, &first, &partials, &tickets);
+    return launch_csr(nrows, ncols, nnz, row_ptrs, col_idx, values, x, y, strategy, subwarp_size, first, partials,
+                      tickets, nullptr, as_stream(stream));
+}
+
+int wk_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_idx, const int32_t* col_idx,
+                    const double* values, const double* x, double* y, int32_t accumulate, wk_stream_t stream) {
+    clear_error();
+    (void)ncols;
+    return launch_coo(nrows, nnz, row_idx, col_idx, values, x, y, accumulate, nullptr, as_stream(stream));
+}
+
+int wk_spmv_hybrid_f64(int64_t nrows, int64_t ncols, int64_t ell_width, int64_t ell_stride,
+                       const int32_t* ell_col, const double* ell_val, const int32_t* ell_row_lengths,
+                       int64_t coo_nnz, const int32_t* coo_row, const int32_t* coo_col, const double* coo_val,
+                       const double* x, double* y, wk_stream_t stream) {
+    clear_error();
+    cudaStream_t st = as_stream(stream);
+    int rc = launch_ell(nrows, ncols, ell_width, ell_stride, ell_col, ell_val, ell_row_lengths, x, y, nullptr, st);
+    if (rc) return rc;
+    return launch_coo(nrows, coo_nnz, coo_row, coo_col, coo_val, x, y, /*accumulate=*/1, nullptr, st);
+}
+
+int wk_spmv(const wk_matrix* A, const double* x, double* y, wk_stream_t stream) {
+    clear_error();
+    return wk_spmv_masked(A, x, y, nullptr, stream);
+}
+
+int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t* skip, wk_stream_t stream) {
+    cudaStream_t st = as_stream(stream);
+    switch (A->format) {
+        case WK_FMT_CSR: {
+            int* first = nullptr;
+            double* partials = nullptr;
+            unsigned* tickets = nullptr;
+            if (A->plan != nullptr) csr_plan_views(A->plan, A->nnz, &first, &partials, &tickets);
+            return launch_csr(A->nrows, A->ncols, A->nnz, A->row_ptrs, A->col_idx, A->values, x, y,
+                              A->csr_strategy, A->subwarp_size, first, partials, tickets, skip, st);
+        }
+        case WK_FMT_COO:
+            WK_REQUIRE(skip == nullptr, WK_ERR_INVALID, "masked COO SpMV is not supported");
+            return launch_coo(A->nrows, A->nnz, A->row_idx, A->col_idx, A->values, x, y, 0, nullptr, st);
+        case WK_FMT_ELL:
+            return launch_ell(A->nrows, A->ncols, A->width, A->stride, A->col_idx, A->values, A->row_lengths, x,
+                              y, skip, st);
+        case WK_FMT_SELLP:
+            return launch_sellp(A->nrows, A->ncols, A->slice_size, A->slice_sets, A->col_idx, A->values,
+                                A->row_lengths, x, y, skip, st);
+        case WK_FMT_HYBRID: {
+            int rc = launch_ell(A->nrows, A->ncols, A->width, A->stride, A->col_idx, A->values, A->row_lengths, x,
+                                y, skip, st);
+            if (rc) return rc;
+            if (A->coo_nnz == 0) return 0;
+            const int64_t warps = ceil_div(A->coo_nnz, kCooPerWarp);
+            coo_kernel<<<(unsigned)ceil_div(warps * 32, kSpmvThreads), kSpmvThreads, 0, st>>>(
+                A->coo_nnz, 1, A->coo_row, A->coo_col, A->coo_val, x, y, skip);
+            WK_LAUNCH_CHECK();
+            return 0;
+        }
+        default:
+            WK_REQUIRE(false, WK_ERR_INVALID, "unknown matrix format %d", A->format);
+    }
+}
+
+}  // extern "C"

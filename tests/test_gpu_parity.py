@@ -1,0 +1,329 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle and the
+reference's golden vectors. Bars:
+  * SELL-P, ELL, CSR-stream SpMV and every conversion: bitwise;
+  * CSR-subwarp, COO, Hybrid SpMV: max_scaled_rel_err <= 1e-12
+    (integer-valued data: exact);
+  * CG: equal iteration count, max |res_k - res_ref_k| / ||b|| <= 1e-10,
+    max_scaled_rel_err(x) <= 1e-10.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import corpus_ref, krylov_ref, sparse_ref  # noqa: E402
+from tests import golden_io  # noqa: E402
+
+SPMV = golden_io.spmv_cases()
+CG = golden_io.cg_cases()
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def wk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_14290_b200 as wk
+
+    return wk
+
+
+@pytest.fixture
+def ex(wk):
+    return wk.make_executor("b200", device=0)
+
+
+def _host(wk, ns, kind):
+    if kind == "coo":
+        return wk.CooMatrix(ns.nrows, ns.ncols, ns.row_idx, ns.col_idx, ns.values)
+    if kind == "csr":
+        return wk.CsrMatrix(ns.nrows, ns.ncols, ns.row_ptrs, ns.col_idx, ns.values)
+    if kind == "sellp":
+        return wk.SellpMatrix(ns.nrows, ns.ncols, ns.slice_size, ns.slice_sets, ns.col_idx, ns.values, ns.row_lengths)
+    raise ValueError(kind)
+
+
+def _is_int(case):
+    return np.all(case.coo.values == np.round(case.coo.values)) and np.all(case.x == np.round(case.x))
+
+
+# ---- SpMV on the reference's golden cases ---------------------------------------------------
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_sellp_golden_bitwise(wk, ex, case):
+    for s, sp in case.sellp.items():
+        y = wk.spmv_sellp(_host(wk, sp, "sellp"), case.x, ex)
+        assert y.tobytes() == case.y.tobytes(), f"slice {s}"
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_csr_stream_golden_bitwise(wk, ex, case):
+    y = wk.spmv_csr(_host(wk, case.csr, "csr"), case.x, ex)
+    assert y.tobytes() == case.y.tobytes()
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_csr_subwarp_golden(wk, case):
+    m = _host(wk, case.csr, "csr")
+    nnz = sparse_ref.row_nnz(case.csr)
+    for tile in (0, 1, 2, 4, 8, 16, 32):
+        e = wk.make_executor("b200", device=0, tuning={"csr_strategy": "subwarp", "csr_subwarp_size": tile})
+        y = wk.spmv_csr(m, case.x, e)
+        if tile == 1 or _is_int(case):
+            assert np.array_equal(y, case.y), tile
+        else:
+            assert sparse_ref.max_scaled_rel_err(y, case.y, nnz) <= TOL, tile
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_coo_golden(wk, ex, case):
+    y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, ex)
+    if _is_int(case):
+        assert np.array_equal(y, case.y)
+    else:
+        assert sparse_ref.max_scaled_rel_err(y, case.y, sparse_ref.row_nnz(case.csr)) <= TOL
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_conversions_golden_bitwise(wk, ex, case):
+    coo = _host(wk, case.coo, "coo")
+    csr = wk.coo_to_csr(coo, ex)
+    assert np.array_equal(csr.row_ptrs, case.csr.row_ptrs)
+    assert np.array_equal(csr.col_idx, case.csr.col_idx)
+    assert csr.values.tobytes() == case.csr.values.tobytes()
+    for s, ref in case.sellp.items():
+        got = wk.coo_to_sellp(coo, s, ex)
+        assert np.array_equal(got.slice_sets, ref.slice_sets), s
+        assert np.array_equal(got.row_lengths, ref.row_lengths), s
+        assert np.array_equal(got.col_idx, ref.col_idx), s
+        assert got.values.tobytes() == ref.values.tobytes(), s
+
+
+@pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
+def test_ell_hybrid_golden(wk, ex, case):
+    csr = _host(wk, case.csr, "csr")
+    ell = wk.csr_to_ell(csr, exec=ex)
+    ref = sparse_ref.csr_to_ell(case.csr)
+    assert ell.width == ref.width and ell.stride == ref.stride
+    assert np.array_equal(ell.col_idx, ref.col_idx) and ell.values.tobytes() == ref.values.tobytes()
+    assert np.array_equal(ell.row_lengths, ref.row_lengths)
+    assert wk.spmv_ell(ell, case.x, ex).tobytes() == case.y.tobytes()
+    nnz = sparse_ref.row_nnz(case.csr)
+    for k in (0, 1, 3, None):
+        hyb = wk.csr_to_hybrid(csr, width=k, exec=ex)
+        kk = hyb.ell.width
+        href = sparse_ref.csr_to_hybrid(case.csr, kk)
+        assert np.array_equal(hyb.ell.col_idx, href.ell.col_idx)
+        assert hyb.ell.values.tobytes() == href.ell.values.tobytes()
+        assert np.array_equal(hyb.coo.row_idx, href.coo.row_idx)
+        assert np.array_equal(hyb.coo.col_idx, href.coo.col_idx)
+        assert hyb.coo.values.tobytes() == href.coo.values.tobytes()
+        y = wk.spmv_hybrid(hyb, case.x, ex)
+        if _is_int(case):
+            assert np.array_equal(y, case.y)
+        else:
+            assert sparse_ref.max_scaled_rel_err(y, case.y, nnz) <= TOL
+
+
+def test_from_entries_duplicates(wk):
+    case = next(c for c in SPMV if c.name == "duplicates")
+    m = wk.CooMatrix.from_entries(3, 3, [2, 0, 2, 2, 1, 0], [1, 0, 1, 1, 2, 0], [0.1, 0.2, 0.3, 0.7, 1.0, 1e-17])
+    assert np.array_equal(m.row_idx, case.coo.row_idx) and np.array_equal(m.col_idx, case.coo.col_idx)
+    assert m.values.tobytes() == case.coo.values.tobytes()
+    ez = next(c for c in SPMV if c.name == "explicit_zeros")
+    m = wk.CooMatrix.from_entries(5, 5, [0, 0, 1, 2, 3, 3, 4], [0, 3, 1, 4, 0, 2, 4],
+                                  [0.0, -1.5, 2.25, -0.0, 1e-300, -7.0, 3.0])
+    assert m.values.tobytes() == ez.coo.values.tobytes()
+
+
+# ---- edge cases -----------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("x0", [np.inf, -np.inf, np.nan])
+def test_nonfinite_x0_follows_oracle(wk, ex, x0, rng):
+    m = corpus_ref.random_sparse(70, 70, 0.1, rng)
+    csr = sparse_ref.coo_to_csr(m)
+    x = rng.standard_normal(70)
+    x[0] = x0
+    y_ref = sparse_ref.spmv(csr, x)
+    for s in (1, 8, 64):
+        sp = sparse_ref.csr_to_sellp(csr, s)
+        y = wk.spmv_sellp(_host(wk, sp, "sellp"), x, ex)
+        assert np.array_equal(y, y_ref, equal_nan=True)
+    hc = _host(wk, csr, "csr")
+    y = wk.spmv_ell(wk.csr_to_ell(hc, exec=ex), x, ex)
+    assert np.array_equal(y, y_ref, equal_nan=True)
+    assert np.array_equal(wk.spmv_csr(hc, x, ex), y_ref, equal_nan=True)
+
+
+def test_dimension_mismatch(wk, ex):
+    case = SPMV[0]
+    with pytest.raises(wk.DimensionMismatch):
+        wk.spmv_coo(_host(wk, case.coo, "coo"), np.ones(5), ex)
+    with pytest.raises(wk.DimensionMismatch):
+        wk.spmv_sellp(_host(wk, case.sellp[2], "sellp"), np.ones(2), ex)
+    with pytest.raises(wk.InvalidSliceSize):
+        wk.coo_to_sellp(_host(wk, case.coo, "coo"), 12, ex)
+
+
+def test_empty_matrices(wk, ex):
+    z = wk.CsrMatrix(4, 3, [0, 0, 0, 0, 0], [], [])
+    assert np.array_equal(wk.spmv_csr(z, np.ones(3), ex), np.zeros(4))
+    sp = wk.csr_to_sellp(z, 2, ex)
+    assert sp.slice_sets.tolist() == [0, 0, 0]
+    assert np.array_equal(wk.spmv_sellp(sp, np.ones(3), ex), np.zeros(4))
+    e = wk.CsrMatrix(0, 0, [0], [], [])
+    assert wk.spmv_csr(e, np.zeros(0), ex).shape == (0,)
+
+
+def test_long_rows_stream_kernel(wk, ex, rng):
+    # rows much longer than the 1024-entry chunk: split across work items,
+    # partials combined deterministically
+    n, ncols = 600, 50000
+    lens = np.zeros(n, dtype=np.int64)
+    lens[[0, 1, 7, 300, 599]] = [30000, 2500, 1025, 40000, 9000]
+    lens[lens == 0] = rng.integers(0, 40, size=int((lens == 0).sum()))
+    ptrs = np.concatenate(([0], np.cumsum(lens)))
+    cols = np.concatenate([np.sort(rng.choice(ncols, size=int(L), replace=False)) for L in lens])
+    vals = rng.standard_normal(len(cols))
+    csr = wk.CsrMatrix(n, ncols, ptrs, cols, vals)
+    x = rng.standard_normal(ncols)
+    y_ref = sparse_ref.spmv(csr, x)
+    y = wk.spmv_csr(csr, x, ex)
+    short = lens <= 1024
+    assert y[short].tobytes() == y_ref[short].tobytes()
+    assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
+    assert wk.spmv_csr(csr, x, ex).tobytes() == y.tobytes()  # deterministic
+    coo = wk.csr_to_coo(csr, ex)
+    assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
+    hyb = wk.csr_to_hybrid(csr, exec=ex)
+    assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
+
+
+# ---- generators ---------------------------------------------------------------------------
+
+
+def test_device_generators_match_oracle(wk):
+    from paper_2006_14290_b200 import corpus
+
+    for dev, ref in (
+        (corpus.poisson2d_matrix(17), corpus_ref.poisson2d(17)),
+        (corpus.stencil3d(9, 7), corpus_ref.stencil(9, 9, 9, corpus_ref.points_7pt())),
+        (corpus.stencil3d(8, 27), corpus_ref.stencil(8, 8, 8, corpus_ref.points_27pt())),
+        (corpus.convection_diffusion3d(7), corpus_ref.stencil(7, 7, 7, corpus_ref.points_7pt(beta=(1.0, 0.5, 0.25)))),
+    ):
+        h = dev.to_host()
+        assert np.array_equal(h.row_ptrs, ref.row_ptrs)
+        assert np.array_equal(h.col_idx, ref.col_idx)
+        assert h.values.tobytes() == ref.values.tobytes()
+    r = corpus.rmat(12, edge_factor=8).to_host()
+    rr = corpus_ref.rmat(12, edge_factor=8)
+    assert np.array_equal(r.row_idx, rr.row_idx) and np.array_equal(r.col_idx, rr.col_idx)
+    assert r.values.tobytes() == rr.values.tobytes()
+
+
+# ---- BLAS-1 -------------------------------------------------------------------------------
+
+
+def test_blas1(wk, ex, rng):
+    for n in (0, 1, 31, 1000, 300001):
+        a = rng.standard_normal(n)
+        b = rng.standard_normal(n)
+        d = wk.dot(a, b, ex)
+        assert abs(d - float(a @ b)) <= 1e-12 * max(1.0, float(np.abs(a) @ np.abs(b)))
+        assert abs(wk.norm2(a, ex) - float(np.linalg.norm(a))) <= 1e-12 * max(1.0, float(np.linalg.norm(a)))
+        y = wk.axpy(0.37, a, b, ex)
+        assert y.tobytes() == (b + 0.37 * a).tobytes()
+    a = rng.standard_normal(123457)
+    assert wk.dot(a, a, ex) == wk.dot(a, a, ex)  # deterministic
+
+
+# ---- CG -------------------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("case", CG, ids=[c.name for c in CG])
+@pytest.mark.parametrize("fmt", ["sellp", "csr", "ell"])
+def test_cg_golden(wk, ex, case, fmt):
+    coo = _host(wk, case.coo, "coo")
+    if fmt == "sellp":
+        m = wk.coo_to_sellp(coo, 64, ex)
+    elif fmt == "csr":
+        m = wk.coo_to_csr(coo, ex)
+    else:
+        m = wk.csr_to_ell(wk.coo_to_csr(coo, ex), exec=ex)
+    x, hist = wk.cg_solve(m, case.b, case.tol, case.max_iters, ex)
+    assert len(hist) == len(case.hist)
+    bn = max(float(np.linalg.norm(case.b)), 1e-300)
+    assert np.max(np.abs(hist - case.hist)) / bn <= 1e-10
+    assert sparse_ref.max_scaled_rel_err(x, case.x, sparse_ref.row_nnz(case.coo)) <= 1e-10
+
+
+def test_cg_identity_and_2x2_exact(wk, ex):
+    eye = wk.coo_to_sellp(wk.CooMatrix(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0]), 64, ex)
+    x, hist = wk.cg_solve(eye, np.array([1.0, 2.0, 3.0]), 1e-12, 50, ex)
+    assert np.array_equal(x, [1.0, 2.0, 3.0]) and len(hist) == 2
+    m = wk.coo_to_sellp(wk.CooMatrix(2, 2, [0, 0, 1, 1], [0, 1, 0, 1], [4.0, 1.0, 1.0, 3.0]), 64, ex)
+    x, hist = wk.cg_solve(m, np.array([1.0, 2.0]), 1e-12, 10, ex)
+    assert len(hist) - 1 <= 2 and np.max(np.abs(x - [1 / 11, 7 / 11])) <= 1e-12
+
+
+def test_cg_errors(wk, ex):
+    bad = wk.coo_to_sellp(wk.CooMatrix(2, 2, [0, 1], [0, 1], [1.0, -1.0]), 64, ex)
+    with pytest.raises(wk.BreakdownError):
+        wk.cg_solve(bad, np.array([0.0, 1.0]), 1e-10, 10, ex)
+    rect = wk.coo_to_sellp(wk.CooMatrix(2, 3, [0], [1], [1.0]), 64, ex)
+    with pytest.raises(wk.DimensionMismatch):
+        wk.cg_solve(rect, np.ones(2), 1e-10, 5, ex)
+    sq = wk.coo_to_sellp(wk.CooMatrix(3, 3, [0, 1, 2], [0, 1, 2], [2.0, 2.0, 2.0]), 64, ex)
+    with pytest.raises(wk.DimensionMismatch):
+        wk.cg_solve(sq, np.ones(4), 1e-10, 5, ex)
+    with pytest.raises(ValueError):
+        wk.cg_solve(sq, np.ones(3), 0.0, 5, ex)
+    x, hist = wk.cg_solve(sq, np.zeros(3), 1e-10, 5, ex)
+    assert np.array_equal(x, np.zeros(3)) and len(hist) == 1
+
+
+def test_cg_device_resident_and_factory(wk, ex):
+    from paper_2006_14290_b200 import corpus
+
+    A = wk.csr_to_sellp(corpus.stencil3d(16, 7), 64, ex)
+    b = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    x, hist = wk.cg_solve(A, b, 1e-10, 1000, ex)
+    assert isinstance(x, torch.Tensor) and x.is_cuda
+    Ah = A.to_host()
+    xr, hr = krylov_ref.cg_solve(lambda v: sparse_ref.spmv(Ah, v), np.ones(A.nrows), 1e-10, 1000)
+    assert len(hist) == len(hr)
+    assert np.max(np.abs(hist.cpu().numpy() - hr)) / np.sqrt(A.nrows) <= 1e-10
+    solver = wk.Cg([wk.Iteration(1000), wk.ResidualNorm(1e-10)], ex).generate(A)
+    xs = solver.apply(b)
+    assert solver.iterations == len(hr) - 1
+    assert torch.equal(xs, x)
+
+
+# ---- BiCGSTAB / GMRES (no reference: vs the oracle restatement) ----------------------------------
+
+
+@pytest.mark.parametrize("solver", ["bicgstab", "gmres"])
+def test_nonsymmetric_solvers_match_oracle(wk, ex, solver):
+    from paper_2006_14290_b200 import corpus
+
+    A = corpus.convection_diffusion3d(12)
+    Ah = A.to_host()
+    b = np.ones(A.nrows)
+    f = lambda v: sparse_ref.spmv(Ah, v)  # noqa: E731
+    if solver == "bicgstab":
+        x, hist = wk.bicgstab_solve(A, b, 1e-10, 500, ex)
+        xr, hr = krylov_ref.bicgstab_solve(f, b, 1e-10, 500)
+    else:
+        x, hist = wk.gmres_solve(A, b, 1e-10, 500, ex, restart=30)
+        xr, hr = krylov_ref.gmres_solve(f, b, 1e-10, 500, restart=30)
+    x = x.cpu().numpy() if hasattr(x, "cpu") else x
+    hist = hist.cpu().numpy() if hasattr(hist, "cpu") else hist
+    assert len(hist) == len(hr)
+    assert np.max(np.abs(hist - hr)) / np.linalg.norm(b) <= 1e-10
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(Ah)) <= 1e-10
+    assert hist[-1] <= 1e-10 * np.linalg.norm(b)
