@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 sparse fp64 hot path (driver contract: one JSON line).
+
+Headline (N=1): BASELINE config 2 — fp64 SELL-P(64) SpMV on the 3-D 27-point
+stencil 200^3 (8M rows, 213.8M nonzeros), matrix and vectors resident in HBM.
+A step is one SpMV y = A x. `value` is GFLOP/s (2 * true nnz per SpMV). The
+operands (2.7 GB per SpMV) are 21x the 126 MB L2, so consecutive steps cannot
+hit in L2 (no flush needed; stated in `config`).
+
+N > 1 (torchrun): row-block (z-slab) partitioned SpMV, weak scaling — rank g
+owns a 200x200x200 slab of a 200x200x(200N) grid, halo planes exchanged over
+NCCL inside every step (see paper_2006_14290_b200/distributed.py).
+
+Extra keys (N=1): `formats` (CSR cfg1 with L2 flush, ELL cfg2, CSR->ELL and
+CSR->SELL-P conversions, COO and Hybrid on R-MAT scale 24), `cg` (cfg4: 1000
+CG iterations on the 7-point 256^3 Laplacian, SELL-P) and, for every N, the
+distributed CG iteration rate.
+
+--impl reference: the reference's algorithm on the host cores (the CPU
+restatement in oracle/, C + OpenMP, all threads) on the same workload,
+bounded samples; rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 SpMV GFLOP/s & HBM GB/s per format; CG iterations/sec at 1/2/4/8 B200"
+GRID = 200          # config 2: 27-point stencil on GRID^3
+SLICE = 64
+CG_GRID = 256       # config 4
+CG_ITERS = 1000
+RMAT_SCALE = 24     # config 3
+CPU_SAMPLE_PLANES = 25
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- clocks ------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.path is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---- timing --------------------------------------------------------------------------------
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def timed(fn, steps, warmup, dist=None, flush=None):
+    """W untimed warm-up calls, then K timed calls bracketed by barrier +
+    synchronize; per-call CUDA events on the launching (current) stream.
+    Returns (total_ms over the K calls, per-call ms list). With `flush`, an
+    L2-flushing write runs before every call, outside the per-call events
+    (total_ms then sums the per-call times)."""
+    import torch
+
+    for _ in range(warmup):
+        if flush is not None:
+            flush()
+        fn()
+    torch.cuda.synchronize()
+    barrier(dist)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for a, b in ev:
+        if flush is not None:
+            flush()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier(dist)
+    per = [a.elapsed_time(b) for a, b in ev]
+    total = sum(per) if flush is not None else t0.elapsed_time(t1)
+    return total, per
+
+
+def max_over_ranks(v, dist):
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sellp_bytes(d):
+    return d.algorithmic_bytes()
+
+
+def load_traffic(name):
+    """dram bytes per launch from a committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
+            s = json.load(fh)
+        k = s["kernels"][name]
+        return int(k["dram_bytes_read"] + k["dram_bytes_write"])
+    except Exception:
+        return None
+
+
+# ---- CPU baseline (oracle C port, all host threads) ---------------------------------------------
+
+
+def cpu_sample(budget_s=10.0, steps=None):
+    """Middle z-slab of the 27-point 200^3 matrix (25 planes, 1M rows, full x),
+    SELL-P(64), folded by oracle/csrc/oracle.c on every host thread."""
+    from oracle import corpus_ref, native, sparse_ref
+
+    plane = GRID * GRID
+    z0 = GRID // 2 - CPU_SAMPLE_PLANES // 2
+    m = corpus_ref.stencil(GRID, GRID, GRID, corpus_ref.points_27pt(), z0 * plane, (z0 + CPU_SAMPLE_PLANES) * plane)
+    sp = sparse_ref.csr_to_sellp(m, SLICE)
+    prep = native.Prepared(sp)
+    x = np.random.default_rng(42).random(m.ncols)
+    threads = native.max_threads()
+    y = prep.spmv(x, nthreads=threads)  # warm-up
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t = time.perf_counter()
+        prep.spmv(x, y, nthreads=threads)
+        times.append(time.perf_counter() - t)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and time.perf_counter() - t_start > budget_s:
+            break
+    nnz = int(m.row_ptrs[-1])
+    mean = sum(times) / len(times)
+    sample = (f"rows of z-planes {z0}..{z0 + CPU_SAMPLE_PLANES - 1} of the 27-pt {GRID}^3 matrix "
+              f"({m.nrows} rows, {nnz} nnz, full x), SELL-P({SLICE}), {len(times)} reps")
+    return {"value": round(2 * nnz / mean / 1e9, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": sample, "ms_per_rep": round(mean * 1e3, 3), "impl": "oracle/csrc/oracle.c or_spmv_sellp",
+            "nnz": nnz}, times
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle import native
+
+    native.lib()
+    base, times = cpu_sample(steps=args.steps + args.warmup)
+    times = times[args.warmup:] or times
+    ms = 1e3 * sum(times) / len(times)
+    base["value"] = round(2 * base["nnz"] / (ms * 1e-3) / 1e9, 4)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 (bounded sample, see cpu_baseline)",
+                   "cpu_threads": base["cores"]},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---- GPU arm ---------------------------------------------------------------------------------
+
+
+def run_gpu(args, rank, world, dist):
+    import torch
+
+    import paper_2006_14290_b200 as wk
+    from paper_2006_14290_b200 import corpus
+    from paper_2006_14290_b200 import device as D
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ex = wk.make_executor("b200", device=dev.index)
+    peak, peak_src = peaks()
+    out = {}
+
+    if world == 1:
+        A_csr = corpus.stencil3d(GRID, 27)
+        A = D.csr_to_sellp(A_csr, SLICE)
+        nnz = A_csr.nnz
+    else:
+        from paper_2006_14290_b200 import distributed as DI
+
+        part = DI.stencil_slab_operator(GRID, GRID, GRID, corpus.points_27pt(), dist, fmt="sellp",
+                                        slice_size=SLICE)
+        A = part.local
+        nnz = part.local_nnz
+    n_local = A.nrows
+    x = torch.rand(A.ncols, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(42))
+    y = torch.empty(n_local, dtype=torch.float64, device=dev)
+    if world == 1:
+        step = lambda: wk.kernels.spmv_device(A, x, y)  # noqa: E731
+    else:
+        step = lambda: part.spmv(x, y)  # noqa: E731
+
+    with ClockSampler(dev.index) as clk:
+        total_ms, per = timed(step, args.steps, args.warmup, dist)
+    clocks = clk.summary()
+    total_ms = max_over_ranks(total_ms, dist)
+    flops_all = 2.0 * nnz * args.steps * world
+    value = flops_all / (total_ms * 1e-3) / 1e9
+    # roofline of the dominant kernel (the SELL-P SpMV launch): per-launch events
+    if world == 1:
+        kernel_ms = statistics.mean(per)
+    else:
+        _, kper = timed(lambda: wk.kernels.spmv_device(A, x, y), args.steps, args.warmup, dist)
+        kernel_ms = statistics.mean(kper)
+    bytes_launch = sellp_bytes(A)
+    achieved = bytes_launch / (kernel_ms * 1e-3) / 1e9
+
+    # end to end through the public API: pinned host x in, pinned host y out
+    e2e = None
+    if True:
+        xh = x[: A.ncols].cpu().pin_memory() if world == 1 else None
+        if world == 1:
+            def e2e_step():
+                return wk.spmv_sellp(A, xh, ex)
+
+            e_ms, _ = timed(e2e_step, max(3, args.steps // 2), 2, dist)
+            e_steps = max(3, args.steps // 2)
+            e2e = {"value": round(2.0 * nnz * e_steps / (e_ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(n_local * 8),
+                   "ms_per_step": round(e_ms / e_steps, 4), "api": "paper_2006_14290_b200.spmv_sellp(A, pinned x)"}
+        else:
+            e2e = part.e2e(x, args, timed)
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 per GPU (BASELINE config 2)"
+                               + (f", z-slab partitioned {GRID}x{GRID}x{GRID * world}, halo over NCCL" if world > 1 else ""),
+                   "rows_per_gpu": n_local, "nnz_per_gpu": int(nnz), "stored_per_gpu": int(A.stored),
+                   "bytes_per_spmv": int(bytes_launch),
+                   "l2": "operands 2.7 GB/step >> 126 MB L2: no flush needed between steps",
+                   "parallelism": f"rowblock{world}"},
+        "hbm_gbs": round(bytes_launch * args.steps * world / (total_ms * 1e-3) / 1e9, 1),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000.0, 4),
+                     "peak_source": peak_src, "traffic": load_traffic("sellp_spmv"),
+                     "kernel": "sliced_spmv_kernel<2,false> (SELL-P, 2 rows/thread, 128-bit loads)",
+                     "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": int(bytes_launch)},
+        "e2e": e2e,
+        "gpu_launches": args.steps * (1 if world == 1 else part.launches_per_spmv),
+        "clocks": clocks,
+    }
+    # extra sections
+    if world == 1 and not args.quick:
+        out["formats"] = bench_formats(args, wk, corpus, D, A_csr, A, x, peak)
+        del A_csr
+        torch.cuda.empty_cache()
+        out["cg"] = bench_cg(args, wk, corpus, D)
+        line["cpu_baseline"] = cpu_sample(budget_s=args.cpu_budget)[0] if not args.no_cpu else None
+    elif world > 1 and not args.quick:
+        out["cg"] = part_cg(args, dist, world)
+    line.update(out)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
+    import torch
+
+    res = {}
+    K, W = max(5, args.steps // 2), 3
+    flush_buf = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=x.device)
+
+    def flush():
+        flush_buf.fill_(1.0)
+
+    def rec(name, d, xx, flush_l2=False, nnz=None):
+        yy = torch.empty(d.nrows, dtype=torch.float64, device=x.device)
+        _, per = timed(lambda: wk.kernels.spmv_device(d, xx, yy), K, W, None, flush if flush_l2 else None)
+        ms = statistics.mean(per)
+        b = d.algorithmic_bytes()
+        nz = d.nnz if nnz is None else nnz
+        res[name] = {"ms": round(ms, 4), "GFLOP/s": round(2 * nz / (ms * 1e-3) / 1e9, 2),
+                     "GB/s": round(b / (ms * 1e-3) / 1e9, 1), "frac_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4),
+                     "bytes": int(b), "nnz": int(nz)}
+        if flush_l2:
+            res[name]["l2"] = "flushed (512 MB write) before every launch"
+        return yy
+
+    rec("sellp_27pt_200", A_sellp, x)
+    rec("csr_27pt_200", A_csr, x)
+    A_csr.with_strategy("subwarp", 0)
+    rec("csr_subwarp_27pt_200", A_csr, x)
+    A_csr.with_strategy("stream", 0)
+    ell = D.csr_to_ell(A_csr)
+    rec("ell_27pt_200", ell, x)
+    del ell
+    torch.cuda.empty_cache()
+    # conversions (read CSR, write ELL / SELL-P)
+    for name, fn in (("csr_to_ell", lambda: D.csr_to_ell(A_csr, width=27)),
+                     ("csr_to_sellp", lambda: D.csr_to_sellp(A_csr, SLICE))):
+        _, per = timed(fn, 3, 1, None)
+        ms = statistics.mean(per)
+        if name == "csr_to_ell":
+            b = A_csr.nnz * 12 + 4 * (A_csr.nrows + 1) + 27 * A_csr.nrows * 12 + 4 * A_csr.nrows
+        else:
+            b = A_csr.nnz * 12 + 4 * (A_csr.nrows + 1) + A_sellp.stored * 12 + 8 * (A_sellp.nslices + 1) + 4 * A_csr.nrows
+        res[name] = {"ms": round(ms, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1), "bytes": int(b),
+                     "note": "includes the host sync reading the total storage size"}
+        torch.cuda.empty_cache()
+    # config 1: CSR on the 2-D Poisson 1000^2 (80 MB: flush L2 before every launch)
+    P = corpus.poisson2d_matrix(1000)
+    xp = torch.rand(P.ncols, dtype=torch.float64, device=x.device)
+    rec("csr_poisson2d_1000", P, xp, flush_l2=True)
+    del P
+    # config 3: COO and Hybrid on R-MAT scale 24
+    R = corpus.rmat(RMAT_SCALE)
+    xr = torch.rand(R.ncols, dtype=torch.float64, device=x.device)
+    rec("coo_rmat24", R, xr)
+    Rc = D.coo_to_csr(R)
+    rec("csr_rmat24", Rc, xr)
+    H = D.csr_to_hybrid(Rc)
+    rec("hybrid_rmat24", H, xr, nnz=R.nnz)
+    res["hybrid_rmat24"]["ell_width"] = H.ell.width
+    res["hybrid_rmat24"]["coo_nnz"] = H.coo.nnz
+    del R, Rc, H, flush_buf
+    torch.cuda.empty_cache()
+    return res
+
+
+def bench_cg(args, wk, corpus, D):
+    import torch
+
+    A = D.csr_to_sellp(corpus.stencil3d(CG_GRID, 7), SLICE)
+    b = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    ex = wk.make_executor("b200")
+    wk.cg_solve(A, b, 1e-30, 60, ex)  # warm-up (graph capture path, caches)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    x, hist = wk.cg_solve(A, b, 1e-30, CG_ITERS, ex)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    it = len(hist) - 1
+    spmv_b = A.algorithmic_bytes()
+    per_it = spmv_b + 72 * A.nrows + (spmv_b + 24 * A.nrows) / 50
+    return {"workload": f"CG, 7-point Laplacian {CG_GRID}^3, SELL-P({SLICE}), b = ones, tol 1e-30, {CG_ITERS} iterations",
+            "iterations": it, "ms": round(ms, 2), "it_per_s": round(it / (ms * 1e-3), 1),
+            "GB/s_effective": round(per_it * it / (ms * 1e-3) / 1e9, 1), "bytes_per_iteration": int(per_it),
+            "n_gpus": 1}
+
+
+def part_cg(args, dist, world):
+    from paper_2006_14290_b200 import distributed as DI
+
+    return DI.bench_cg(CG_GRID, CG_ITERS, dist, timed)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true", help="headline only")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    run_gpu(args, rank, world, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

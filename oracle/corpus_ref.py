@@ -66,11 +66,15 @@ def _sorted_points(points, nx, ny):
     return sorted(points, key=lambda p: p[2] * nx * ny + p[1] * nx + p[0])
 
 
-def stencil(nx, ny, nz, points):
-    """CSR of a constant-coefficient stencil on an nx*ny*nz grid."""
+def stencil(nx, ny, nz, points, row_lo=0, row_hi=None):
+    """CSR of a constant-coefficient stencil on an nx*ny*nz grid; with
+    row_lo/row_hi only those rows (global column indices), e.g. a z-slab
+    sample of a large grid."""
     pts = _sorted_points(points, nx, ny)
-    n = nx * ny * nz
-    r = np.arange(n, dtype=np.int64)
+    ncols = nx * ny * nz
+    row_hi = ncols if row_hi is None else row_hi
+    r = np.arange(row_lo, row_hi, dtype=np.int64)
+    n = len(r)
     i = r % nx
     j = (r // nx) % ny
     k = r // (nx * ny)
@@ -85,13 +89,14 @@ def stencil(nx, ny, nz, points):
     col = np.empty(nnz, dtype=np.int64)
     val = np.empty(nnz, dtype=np.float64)
     pos = np.zeros(n, dtype=np.int64)
+    local = np.arange(n, dtype=np.int64)
     for (dx, dy, dz, v), mk in zip(pts, masks):
-        rows = r[mk]
+        rows = local[mk]
         dst = ptrs[rows] + pos[rows]
-        col[dst] = rows + dz * nx * ny + dy * nx + dx
+        col[dst] = r[mk] + dz * nx * ny + dy * nx + dx
         val[dst] = v
         pos[rows] += 1
-    return SimpleNamespace(nrows=n, ncols=n, row_ptrs=ptrs, col_idx=col, values=val)
+    return SimpleNamespace(nrows=n, ncols=ncols, row_ptrs=ptrs, col_idx=col, values=val)
 
 
 def poisson2d(nx, ny=None):

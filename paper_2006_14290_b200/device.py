@@ -374,6 +374,11 @@ def as_device_vector(x, n, device=None, name="x"):
     if isinstance(x, torch.Tensor):
         if x.dim() != 1 or x.numel() != n:
             raise DimensionMismatch(f"{name} has shape {tuple(x.shape)}, expected ({n},)")
+        if x.device.type == "cpu":
+            # host torch tensor (pinned -> asynchronous DMA); the result goes
+            # back to the host as a torch tensor (see to_host_like)
+            xt = x.to(dtype=torch.float64).contiguous().to(dev, non_blocking=x.is_pinned())
+            return xt, "torch_pinned" if x.is_pinned() else "torch"
         if x.device != dev or x.dtype != torch.float64 or not x.is_contiguous():
             x = x.to(device=dev, dtype=torch.float64).contiguous()
         return x, False
@@ -381,6 +386,20 @@ def as_device_vector(x, n, device=None, name="x"):
     if arr.ndim != 1 or len(arr) != n:
         raise DimensionMismatch(f"matrix needs {name} of length {n}, got shape {arr.shape}")
     return torch.from_numpy(np.ascontiguousarray(arr)).to(dev), True
+
+
+def to_host_like(y, host):
+    """Return device result `y` in the caller's host representation."""
+    if not host:
+        return y
+    if host == "torch_pinned":
+        out = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+        out.copy_(y, non_blocking=True)
+        torch.cuda.current_stream(y.device).synchronize()
+        return out
+    if host == "torch":
+        return y.cpu()
+    return y.cpu().numpy()
 
 
 # ---- conversions (bit-exact; sparse.py:212-242 semantics) -------------------------------------

@@ -50,7 +50,7 @@ def _spmv_b200(exec: Executor, m, x, fmt=None):
     exec.counters.launches += _launches(d)
     if d.fmt in ("coo", "hybrid"):
         exec.counters.atomics += int(d.coo.nnz if d.fmt == "hybrid" else d.nnz) // 512
-    return y.cpu().numpy() if host else y
+    return D.to_host_like(y, host)
 
 
 def _spmv_op(fmt):

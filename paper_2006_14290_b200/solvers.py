@@ -69,9 +69,7 @@ def _run(kind, exec: Executor, m, b, tol, max_iters, restart=30):
     hist = hist[: it + 1]
     exec.counters.lane_steps += int(d.nnz) * it
     exec.counters.launches += it * 6
-    if host:
-        return x.cpu().numpy(), hist.cpu().numpy()
-    return x, hist
+    return D.to_host_like(x, host), D.to_host_like(hist, host)
 
 
 def _cg_b200(exec, m, b, tol, max_iters):
