@@ -58,6 +58,10 @@ const char* wk_last_error(void);
 int wk_version(void);
 /* number of SMs of the current device */
 int wk_device_sm_count(void);
+/* process-wide kernel selection knobs (A/B measurement): key "sellp_kernel":
+ * 0 = register-only SELL-P kernel, 1..5 = TMA pipeline configurations
+ * (J.S.W = 8.4.8, 8.2.16, 4.4.16, 16.2.8, 4.3.20) */
+int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */
 

@@ -53,6 +53,7 @@ _SIGS = {
     "wk_last_error": (ctypes.c_char_p, []),
     "wk_version": (ctypes.c_int, []),
     "wk_device_sm_count": (ctypes.c_int, []),
+    "wk_config_set": (ctypes.c_int, [ctypes.c_char_p, I64]),
     "wk_spmv_sellp_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, P, P]),
     "wk_spmv_ell_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, P, P, P]),
     "wk_spmv_csr_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, I32, P, P]),

@@ -1,0 +1,165 @@
+// SELL-P(64) SpMV with TMA bulk-copy staging — the B200 path for slice_size 64.
+//
+// Persistent grid, one CTA per SM, WARPS independent warp pipelines. Warp w
+// owns slices w, w + W, w + 2W, ... (W = warps in the grid); each slice is cut
+// into chunks of J columns (J * 64 entries: 512*J bytes of values + 256*J
+// bytes of column indices, both contiguous in the SELL-P layout). Lane 0
+// streams the chunks with cp.async.bulk (TMA engine, L2 evict-first) into an
+// S-deep per-warp ring in shared memory, completion tracked by one mbarrier
+// per stage; all 32 lanes consume a landed chunk (2 rows per lane, 128-bit
+// shared loads), gather x[col] through L1/L2 and fold sequentially with
+// separately rounded multiply/add (bitwise == reference fold). DRAM streaming
+// is thereby decoupled from the gather latency: S-1 chunks per warp stay in
+// flight while the current chunk's gathers resolve.
+#pragma once
+
+#include "common.cuh"
+
+namespace wk {
+
+template <int J, int S, int WARPS, int CTAS = 1>
+struct SellpTmaCfg {
+    static constexpr int kJ = J, kS = S, kWarps = WARPS, kCtas = CTAS;
+    static constexpr int kChunk = J * 64;
+    static constexpr size_t kSmem = size_t(WARPS) * S * kChunk * (sizeof(double) + sizeof(int)) + WARPS * S * 8;
+};
+
+// Consume one landed chunk: nj <= J columns for this lane's two rows.
+template <int J, bool kLen>
+__device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const int* __restrict__ c, int nj,
+                                            int j0, int len0, int len1, const double* __restrict__ x, double& a0,
+                                            double& a1) {
+    double2 vv[J];
+    double x0[J], x1[J];
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        if (jj < nj) {
+            vv[jj] = *reinterpret_cast<const double2*>(v + jj * 64);
+            const int2 cc = *reinterpret_cast<const int2*>(c + jj * 64);
+            x0[jj] = ld_x(x, cc.x);
+            x1[jj] = ld_x(x, cc.y);
+        }
+    }
+#pragma unroll
+    for (int jj = 0; jj < J; ++jj) {
+        if (jj < nj) {
+            if (!kLen || j0 + jj < len0) a0 = mul_add_rn(a0, vv[jj].x, x0[jj]);
+            if (!kLen || j0 + jj < len1) a1 = mul_add_rn(a1, vv[jj].y, x1[jj]);
+        }
+    }
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
+sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
+                   const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
+                   const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip) {
+    constexpr int J = Cfg::kJ, S = Cfg::kS, WARPS = Cfg::kWarps, CH = Cfg::kChunk;
+    if (skip != nullptr && *skip) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* sval = reinterpret_cast<double*>(smem) + size_t(warp) * S * CH;
+    int* scol = reinterpret_cast<int*>(smem + size_t(WARPS) * S * CH * sizeof(double)) + size_t(warp) * S * CH;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(WARPS) * S * CH * 12) + warp * S;
+    if (lane == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(bars + st, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const bool finite0 = ncols == 0 || isfinite(__ldg(x));
+    const int64_t gwarp = int64_t(blockIdx.x) * WARPS + warp;
+    const int64_t nwarps = int64_t(gridDim.x) * WARPS;
+    const uint64_t pol = policy_evict_first();
+
+    // producer cursor (warp-uniform; lane 0 issues)
+    int64_t ps = gwarp, pbase = 0;
+    int pj = 0, pw = 0;
+    bool pvalid = false;
+    auto seek = [&]() {
+        pvalid = false;
+        while (ps < nslices) {
+            const int64_t s0 = __ldg(sets + ps);
+            pw = int(__ldg(sets + ps + 1) - s0);
+            if (pj < pw) {
+                pbase = s0 * 64;
+                pvalid = true;
+                return;
+            }
+            ps += nwarps;
+            pj = 0;
+        }
+    };
+    auto issue = [&](int st) {
+        if (lane == 0) {
+            const int nj = (pw - pj < J) ? pw - pj : J;
+            const uint32_t bv = uint32_t(nj) * 64 * sizeof(double), bc = uint32_t(nj) * 64 * sizeof(int);
+            mbar_arrive_expect_tx(bars + st, bv + bc);
+            const int64_t off = pbase + int64_t(pj) * 64;
+            bulk_g2s_evict_first(sval + st * CH, val + off, bv, bars + st, pol);
+            bulk_g2s_evict_first(scol + st * CH, col + off, bc, bars + st, pol);
+        }
+        pj += J;
+        seek();
+    };
+    seek();
+    for (int st = 0; st < S && pvalid; ++st) issue(st);
+
+    uint32_t i = 0;  // chunks consumed by this warp
+    for (int64_t s = gwarp; s < nslices; s += nwarps) {
+        const int64_t s0 = __ldg(sets + s);
+        const int w = int(__ldg(sets + s + 1) - s0);
+        const int64_t r0 = s * 64 + 2 * lane;
+        int len0 = w, len1 = w;
+        if (!finite0) {
+            len0 = r0 < nrows ? row_lengths[r0] : 0;
+            len1 = r0 + 1 < nrows ? row_lengths[r0 + 1] : 0;
+        }
+        double a0 = 0.0, a1 = 0.0;
+        for (int j0 = 0; j0 < w; j0 += J) {
+            const int st = int(i % S);
+            mbar_wait(bars + st, (i / S) & 1);
+            const int nj = (w - j0 < J) ? w - j0 : J;
+            const double* v = sval + st * CH + 2 * lane;
+            const int* c = scol + st * CH + 2 * lane;
+            if (finite0)
+                sellp_chunk<J, false>(v, c, nj, j0, len0, len1, x, a0, a1);
+            else
+                sellp_chunk<J, true>(v, c, nj, j0, len0, len1, x, a0, a1);
+            __syncwarp();
+            if (pvalid) {
+                if (lane == 0) fence_proxy_async_smem();
+                issue(st);
+            }
+            ++i;
+        }
+        if (r0 + 1 < nrows) {
+            __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
+        } else if (r0 < nrows) {
+            st_stream(y + r0, a0);
+        }
+    }
+}
+
+// Launch one configuration (persistent grid: one CTA per SM).
+template <class Cfg>
+int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
+                       const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st) {
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Cfg::kSmem)));
+        attr_set[dev & 63] = true;
+    }
+    const int64_t nslices = ceil_div(nrows, 64);
+    int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
+    const int64_t need = ceil_div(nslices, Cfg::kWarps);
+    if (grid > need) grid = need;
+    sellp64_tma_kernel<Cfg><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(nrows, ncols, nslices, sets, col,
+                                                                                val, row_lengths, x, y, skip);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // namespace wk

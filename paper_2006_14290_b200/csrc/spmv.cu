@@ -17,6 +17,7 @@
 // x != 0, +0 + -0 == +0) as long as x[0] is finite; if it is not, the
 // kernels switch to the `row_lengths`-bounded loop of the oracle.
 #include "common.cuh"
+#include "sellp_tma.cuh"
 
 namespace wk {
 
@@ -119,6 +120,28 @@ sliced_spmv_kernel(int64_t nrows, int64_t ncols, int log2ss, int64_t ell_width, 
 
 static bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
+// SELL-P(64) kernel selection for A/B measurements (env WK_SELLP_KERNEL or
+// wk_config_set("sellp_kernel", i)): 0 = register-only kernel, 1..8 = TMA
+// pipeline configurations (table in launch_sellp); default 7 = the best
+// measured configuration (tools/sweep_sellp.py, profiles/r01).
+static int g_sellp_choice = -1;
+
+int set_sellp_kernel(int choice) {
+    WK_REQUIRE(choice >= 0 && choice <= 8, WK_ERR_INVALID, "sellp kernel choice must be in [0, 8]");
+    g_sellp_choice = choice;
+    return 0;
+}
+
+static int sellp_kernel_choice() {
+    int& choice = g_sellp_choice;
+    if (choice < 0) {
+        const char* e = getenv("WK_SELLP_KERNEL");
+        choice = 7;
+        if (e != nullptr) choice = atoi(e);  // index into the table in launch_sellp
+    }
+    return choice;
+}
+
 static int log2i(int64_t v) {
     int l = 0;
     while ((int64_t(1) << l) < v) ++l;
@@ -130,6 +153,22 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
                  const int* skip, cudaStream_t st) {
     if (nrows == 0) return 0;
     const int l2 = log2i(ss);
+    const int choice = sellp_kernel_choice();
+    if (ss == 64 && choice > 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16)) {
+#define WK_TMA(J, S, W, C) \
+    return launch_sellp64_tma<SellpTmaCfg<J, S, W, C>>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st)
+        switch (choice) {
+            case 1: WK_TMA(8, 4, 8, 1);
+            case 3: WK_TMA(2, 8, 16, 1);
+            case 4: WK_TMA(4, 6, 12, 1);
+            case 5: WK_TMA(4, 4, 8, 2);
+            case 6: WK_TMA(2, 6, 20, 1);
+            case 8: WK_TMA(4, 5, 12, 1);
+            case 7: WK_TMA(4, 3, 16, 1);  // best measured (profiles/r01/sellp_sweep.jsonl)
+            default: WK_TMA(4, 4, 16, 1);
+        }
+#undef WK_TMA
+    }
     const bool vec = ss >= 2 && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {
         const int64_t threads = ceil_div(nrows, 2);
