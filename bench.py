@@ -161,7 +161,8 @@ def max_over_ranks(v, dist):
         return v
     import torch
 
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dev = "cpu" if str(dist.get_backend()).lower() == "gloo" else "cuda"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -317,7 +318,7 @@ def run_gpu(args, rank, world, dist):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000.0, 4),
                      "peak_source": peak_src, "traffic": load_traffic("sellp_spmv"),
-                     "kernel": "sliced_spmv_kernel<2,false> (SELL-P, 2 rows/thread, 128-bit loads)",
+                     "kernel": "sellp64_tma_kernel<J=4,S=3,W=16> (SELL-P(64), TMA bulk-copy ring, 2 rows/lane)",
                      "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": int(bytes_launch)},
         "e2e": e2e,
         "gpu_launches": args.steps * (1 if world == 1 else part.launches_per_spmv),
@@ -450,12 +451,19 @@ def main():
     import torch
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # WK_DIST_BACKEND=gloo lets the N>1 path run with several ranks on one
+    # GPU (host-staged exchange) to test it; the driver's runs use NCCL.
+    backend = os.environ.get("WK_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as tdist
 
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
     run_gpu(args, rank, world, dist)
     if dist is not None:

@@ -1,0 +1,463 @@
+"""Row-block partitioned SpMV and Krylov solves across the GPUs of one box.
+
+SURVEY.md §8(e). One process per GPU (torch.distributed, NCCL over NVLink /
+NVSwitch); the reference has no distributed code at all.
+
+Partition: rank g owns the contiguous rows [row_lo_g, row_hi_g) (boundaries
+multiples of 64, so SELL-P slices never straddle ranks). Its local matrix
+keeps every row's entries in the GLOBAL column order, with columns renumbered
+into the rank's extended vector x_ext = [owned (n_local) | halo (n_halo)]:
+owned column c -> c - row_lo, non-owned column -> n_local + position in the
+sorted list of needed remote columns. Because entries stay in global order,
+the local fold is the global fold: the distributed SpMV is bitwise equal to
+the single-GPU one.
+
+Per SpMV: pack the entries of x the neighbours need (wk_gather_f64), one
+grouped NCCL send/recv (torch.distributed.batch_isend_irecv) straight into
+the halo segment of x_ext, then the local SpMV kernel. Dot products: the
+local partial (written into a device state by the fused CG kernels) is
+all-reduced in place (NCCL returns bit-identical sums on every rank, so the
+device-side convergence decisions agree everywhere).
+
+For CPU testing, `LocalOps` can be swapped (tests inject a numpy/oracle
+implementation and run world-size-2 gloo groups); with the gloo backend,
+CUDA tensors are staged through host memory.
+"""
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as D
+from .errors import BreakdownError, DimensionMismatch
+
+ALIGN = 64
+
+
+# ---- communication -------------------------------------------------------------------------
+
+
+class Comm:
+    """Thin wrapper over a torch.distributed process group."""
+
+    def __init__(self, dist=None, group=None):
+        import torch.distributed as tdist
+
+        self.dist = dist if dist is not None else tdist
+        self.group = group
+        self.rank = self.dist.get_rank(group)
+        self.world = self.dist.get_world_size(group)
+        self.backend = str(self.dist.get_backend(group)).lower()
+
+    def _staged(self, t):
+        return self.backend == "gloo" and t.is_cuda
+
+    def allreduce_(self, t):
+        """In-place sum all-reduce."""
+        if self.world == 1:
+            return t
+        if self._staged(t):
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def max_scalar(self, v):
+        """Max of a host float over ranks (timing: max over ranks)."""
+        if self.world == 1:
+            return float(v)
+        dev = "cpu" if self.backend == "gloo" else "cuda"
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allgather_obj(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def exchange(self, sends, recvs):
+        """sends: [(peer, tensor)], recvs: [(peer, tensor view)] — one
+        grouped send/recv round (NCCL group / gloo P2P)."""
+        if not sends and not recvs:
+            return
+        if self.backend == "gloo":
+            ops, staged = [], []
+            for peer, t in sends:
+                ops.append(self.dist.P2POp(self.dist.isend, t.cpu() if t.is_cuda else t, peer, self.group))
+            for peer, t in recvs:
+                h = torch.empty(t.shape, dtype=t.dtype) if t.is_cuda else t
+                staged.append((h, t))
+                ops.append(self.dist.P2POp(self.dist.irecv, h, peer, self.group))
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+            for h, t in staged:
+                if h is not t:
+                    t.copy_(h)
+            return
+        ops = [self.dist.P2POp(self.dist.isend, t, peer, self.group) for peer, t in sends]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer, self.group) for peer, t in recvs]
+        for r in self.dist.batch_isend_irecv(ops):
+            r.wait()
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# ---- local compute backends -------------------------------------------------------------------
+
+
+class DeviceOps:
+    """Local kernels of libwk_sparse (the product path)."""
+
+    def __init__(self, device=None):
+        self.device = D._dev(device)
+        self.ws = D.workspace(self.device)
+
+    def stream(self):
+        return D.stream_handle(self.device)
+
+    def zeros(self, n):
+        return torch.zeros(n, dtype=torch.float64, device=self.device)
+
+    def index(self, arr):
+        return torch.as_tensor(np.asarray(arr, dtype=np.int32), device=self.device)
+
+    def gather(self, idx, src, dst):
+        _lib.call("wk_gather_f64", idx.numel(), D._ptr(idx), D._ptr(src), D._ptr(dst), self.stream())
+
+    def spmv(self, local, x_ext, y):
+        _lib.call("wk_spmv", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), self.stream())
+
+    def spmv_masked(self, local, x_ext, y, state):
+        done = ctypes.c_void_p(state.data_ptr() + _lib.WkCgState.done.offset)
+        _lib.call("wk_spmv_masked", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), done, self.stream())
+
+    # CG building blocks (state = 80-byte wk_cg_state in a uint8 tensor)
+    def new_state(self):
+        return torch.zeros(ctypes.sizeof(_lib.WkCgState), dtype=torch.uint8, device=self.device)
+
+    def cg(self, name, *args):
+        conv = [D._ptr(a) if isinstance(a, torch.Tensor) else a for a in args]
+        if name in ("wk_cg_init_local", "wk_cg_dot_pq", "wk_cg_update_xr", "wk_cg_replace_r"):
+            conv.append(D._ptr(self.ws.red))
+        _lib.call(name, *conv, self.stream())
+
+    def read_state(self, state):
+        h = _lib.WkCgState.from_buffer_copy(state.cpu().numpy().tobytes())
+        return h
+
+
+# ---- partition plans ----------------------------------------------------------------------------
+
+
+def row_blocks(nrows, world, align=ALIGN):
+    """Contiguous row ranges, boundaries multiples of `align`."""
+    units = (nrows + align - 1) // align
+    bounds = [min(nrows, (units * g // world) * align) for g in range(world + 1)]
+    bounds[-1] = nrows
+    return bounds
+
+
+class HaloPlan:
+    """Which entries of x go to / come from which rank."""
+
+    def __init__(self, n_local, halo_cols, send_idx, recv_ranges):
+        self.n_local = n_local
+        self.halo_cols = halo_cols          # sorted global ids of the halo (np.int64)
+        self.n_halo = len(halo_cols)
+        self.send_idx = send_idx            # {peer: local owned indices (np.int64)}
+        self.recv_ranges = recv_ranges      # {peer: (offset into halo, count)}
+
+    @property
+    def bytes_per_exchange(self):
+        return 8 * (sum(len(v) for v in self.send_idx.values()) + self.n_halo)
+
+
+def _plan_from_needs(rank, bounds, needed_by_rank):
+    """needed_by_rank[q] = sorted global columns rank q needs from others."""
+    lo, hi = bounds[rank], bounds[rank + 1]
+    mine = needed_by_rank[rank]
+    recv = {}
+    for q in range(len(bounds) - 1):
+        if q == rank:
+            continue
+        a = np.searchsorted(mine, bounds[q])
+        b = np.searchsorted(mine, bounds[q + 1])
+        if b > a:
+            recv[q] = (int(a), int(b - a))
+    send = {}
+    for q, need in enumerate(needed_by_rank):
+        if q == rank:
+            continue
+        a = np.searchsorted(need, lo)
+        b = np.searchsorted(need, hi)
+        if b > a:
+            send[q] = need[a:b] - lo
+    return HaloPlan(hi - lo, mine, send, recv)
+
+
+def localize_columns(cols, lo, hi, halo_cols):
+    """Global -> extended-local column ids (owned first, then halo)."""
+    cols = np.asarray(cols, dtype=np.int64)
+    out = cols - lo
+    remote = (cols < lo) | (cols >= hi)
+    out[remote] = (hi - lo) + np.searchsorted(halo_cols, cols[remote])
+    return out
+
+
+class DistOperator:
+    """Rank-local piece of a row-block partitioned matrix."""
+
+    def __init__(self, comm, bounds, plan, local, local_nnz, ops=None, nrows_global=None):
+        self.comm = comm
+        self.bounds = bounds
+        self.plan = plan
+        self.local = local
+        self.local_nnz = int(local_nnz)
+        self.ops = ops if ops is not None else DeviceOps()
+        self.n_local = plan.n_local
+        self.n_halo = plan.n_halo
+        self.nrows_global = nrows_global if nrows_global is not None else bounds[-1]
+        self.row_lo = bounds[comm.rank]
+        self._send_idx = {q: self.ops.index(v) for q, v in plan.send_idx.items()}
+        self._send_buf = {q: self.ops.zeros(len(v)) for q, v in plan.send_idx.items()}
+        self.launches_per_spmv = 1 + len(self._send_idx)
+
+    @property
+    def stored(self):
+        return getattr(self.local, "stored", self.local_nnz)
+
+    def new_vector(self):
+        """Zeroed vector with halo room: [n_local | n_halo]."""
+        return self.ops.zeros(self.n_local + self.n_halo)
+
+    def exchange(self, x_ext):
+        sends = []
+        for q, idx in self._send_idx.items():
+            buf = self._send_buf[q]
+            self.ops.gather(idx, x_ext, buf)
+            sends.append((q, buf))
+        recvs = [(q, x_ext[self.n_local + off: self.n_local + off + cnt])
+                 for q, (off, cnt) in self.plan.recv_ranges.items()]
+        self.comm.exchange(sends, recvs)
+
+    def spmv(self, x_ext, y):
+        """y[:n_local] = (A x)[rows of this rank]; x_ext's owned part must be
+        current, its halo part is refreshed here."""
+        self.exchange(x_ext)
+        self.ops.spmv(self.local, x_ext, y)
+        return y
+
+    def algorithmic_bytes(self):
+        return self.local.algorithmic_bytes()
+
+    def e2e(self, x, args, timed):
+        """End-to-end SpMV through this API with host buffers (pinned host x
+        slice in, host y out) — used by bench.py at N > 1."""
+        xh = x[: self.n_local].cpu().pin_memory()
+        yh = torch.empty(self.n_local, dtype=torch.float64, pin_memory=True)
+        x_ext = self.new_vector()
+        y = self.ops.zeros(self.n_local)
+
+        def step():
+            x_ext[: self.n_local].copy_(xh, non_blocking=True)
+            self.spmv(x_ext, y)
+            yh.copy_(y, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        steps = max(3, args.steps // 2)
+        ms, _ = timed(step, steps, 2, self.comm.dist)
+        ms = self.comm.max_scalar(ms)
+        return {"value": round(2.0 * self.local_nnz * self.comm.world * steps / (ms * 1e-3) / 1e9, 3),
+                "unit": "GFLOP/s", "h2d_bytes_per_step": int(8 * self.n_local * self.comm.world),
+                "d2h_bytes_per_step": int(8 * self.n_local * self.comm.world),
+                "ms_per_step": round(ms / steps, 4), "api": "distributed.DistOperator.spmv (pinned host x/y)"}
+
+
+def _convert_local(dcsr, fmt, slice_size):
+    if fmt == "csr":
+        return dcsr
+    if fmt == "sellp":
+        return D.csr_to_sellp(dcsr, slice_size)
+    if fmt == "ell":
+        return D.csr_to_ell(dcsr)
+    if fmt == "hybrid":
+        return D.csr_to_hybrid(dcsr)
+    if fmt == "coo":
+        return D.csr_to_coo(dcsr)
+    raise ValueError(f"unknown format {fmt!r}")
+
+
+def partition_csr(m, comm, fmt="sellp", slice_size=64, ops=None, bounds=None, upload=None):
+    """Partition a global CSR (host object with row_ptrs/col_idx/values, the
+    same on every rank) into row blocks. Returns this rank's DistOperator."""
+    n = m.nrows
+    if m.ncols != n:
+        raise DimensionMismatch("row-block partitioning needs a square matrix")
+    bounds = row_blocks(n, comm.world) if bounds is None else bounds
+    ptrs = np.asarray(m.row_ptrs, dtype=np.int64)
+    cols = np.asarray(m.col_idx, dtype=np.int64)
+    vals = np.asarray(m.values, dtype=np.float64)
+    needed = []
+    for q in range(comm.world):
+        lo, hi = bounds[q], bounds[q + 1]
+        c = cols[ptrs[lo]:ptrs[hi]]
+        needed.append(np.unique(c[(c < lo) | (c >= hi)]))
+    plan = _plan_from_needs(comm.rank, bounds, needed)
+    lo, hi = bounds[comm.rank], bounds[comm.rank + 1]
+    lp = ptrs[lo:hi + 1] - ptrs[lo]
+    lc = localize_columns(cols[ptrs[lo]:ptrs[hi]], lo, hi, plan.halo_cols)
+    lv = vals[ptrs[lo]:ptrs[hi]]
+    ncols_ext = (hi - lo) + plan.n_halo
+    if upload is not None:
+        local = upload(hi - lo, ncols_ext, lp, lc, lv)
+    else:
+        from types import SimpleNamespace
+
+        dcsr = D.upload(SimpleNamespace(nrows=hi - lo, ncols=ncols_ext, row_ptrs=lp, col_idx=lc, values=lv),
+                        (ops or DeviceOps()).device)
+        local = _convert_local(dcsr, fmt, slice_size)
+    return DistOperator(comm, bounds, plan, local, len(lv), ops, n)
+
+
+def stencil_slab_operator(nx, ny, nz_local, points, dist=None, fmt="sellp", slice_size=64, weak=True, nz=None):
+    """z-slab partition of a stencil matrix generated on the device.
+
+    weak=True: every rank owns nz_local planes of an nx*ny*(nz_local*P) grid
+    (weak scaling); weak=False: the global grid has `nz` planes split as
+    evenly as possible (strong scaling). Each rank generates only its planes
+    plus one halo plane on each side (the stencils here reach +-1 plane)."""
+    from . import corpus
+
+    comm = Comm(dist)
+    P, g = comm.world, comm.rank
+    plane = nx * ny
+    if weak:
+        nzg = nz_local * P
+        zb = [nz_local * q for q in range(P + 1)]
+    else:
+        nzg = nz
+        zb = [nzg * q // P for q in range(P + 1)]
+    z0, z1 = zb[g], zb[g + 1]
+    has_lo, has_hi = z0 > 0, z1 < nzg
+    e0, e1 = z0 - int(has_lo), z1 + int(has_hi)
+    ext = corpus.stencil(nx, ny, e1 - e0, points)          # device CSR of the extended slab
+    n_local = (z1 - z0) * plane
+    lo_rows = int(has_lo) * plane
+    ptrs = ext.row_ptrs[lo_rows: lo_rows + n_local + 1]
+    base = int(ptrs[0].item())
+    nnz = int(ptrs[-1].item()) - base
+    col = ext.col_idx[base: base + nnz].to(torch.int64)
+    val = ext.values[base: base + nnz]
+    # extended-slab column -> [owned | halo lo plane | halo hi plane]
+    owned_lo, owned_hi = lo_rows, lo_rows + n_local
+    lcol = col - owned_lo
+    if has_lo:
+        m = col < owned_lo
+        lcol = torch.where(m, n_local + col, lcol)
+    if has_hi:
+        m = col >= owned_hi
+        lcol = torch.where(m, n_local + lo_rows + (col - owned_hi), lcol)
+    n_halo = (int(has_lo) + int(has_hi)) * plane
+    dcsr = D.DeviceCsr(n_local, n_local + n_halo, (ptrs - base).contiguous(), lcol.to(torch.int32).contiguous(),
+                       val.contiguous())
+    del ext
+    local = _convert_local(dcsr, fmt, slice_size)
+    bounds = [z * plane for z in zb]
+    halo_cols = []
+    recv, send = {}, {}
+    if has_lo:
+        halo_cols.append(np.arange((z0 - 1) * plane, z0 * plane, dtype=np.int64))
+        recv[g - 1] = (0, plane)
+        send[g - 1] = np.arange(0, plane, dtype=np.int64)
+    if has_hi:
+        halo_cols.append(np.arange(z1 * plane, (z1 + 1) * plane, dtype=np.int64))
+        recv[g + 1] = (int(has_lo) * plane, plane)
+        send[g + 1] = np.arange(n_local - plane, n_local, dtype=np.int64)
+    hc = np.concatenate(halo_cols) if halo_cols else np.zeros(0, np.int64)
+    plan = HaloPlan(n_local, hc, send, recv)
+    return DistOperator(comm, bounds, plan, local, nnz, DeviceOps(), nzg * plane)
+
+
+# ---- distributed CG -------------------------------------------------------------------------------
+
+_RHO, _PQ, _RR = 0, 1, 2  # float64 slots of wk_cg_state
+
+
+REPLACE_EVERY = 50  # kernels.py:322, kReplaceEvery in krylov.cu
+
+
+def cg_solve(op: DistOperator, b_local, tol, max_iters):
+    """Row-block distributed CG with the reference's update order
+    (kernels.py:283-331), all scalars on the device. Returns (x_local, hist)
+    (device tensors). Iteration control is identical on all ranks because
+    the all-reduced scalars are bit-identical."""
+    ops, comm = op.ops, op.comm
+    n = op.n_local
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    b = b_local
+    x = op.new_vector()
+    r = ops.zeros(n)
+    p = op.new_vector()
+    q = ops.zeros(n)
+    hist = ops.zeros(int(max_iters) + 1)
+    st = ops.new_state()
+    f64 = st.view(torch.float64)
+    ops.cg("wk_cg_init_local", n, b, x, r, p, st)
+    comm.allreduce_(f64[_RHO:_RHO + 1])
+    ops.cg("wk_cg_init_finish", st, float(tol), int(max_iters), hist)
+    it = 0
+    while True:
+        h = ops.read_state(st)
+        if h.done:
+            break
+        for _ in range(REPLACE_EVERY):
+            it_next = it + 1
+            op.exchange(p)
+            ops.spmv_masked(op.local, p, q, st)
+            ops.cg("wk_cg_dot_pq", n, p, q, st)
+            comm.allreduce_(f64[_PQ:_PQ + 1])
+            ops.cg("wk_cg_step_alpha", st)
+            ops.cg("wk_cg_update_xr", n, p, q, x, r, st)
+            if it_next % REPLACE_EVERY == 0:
+                op.exchange(x)
+                ops.spmv_masked(op.local, x, q, st)
+                ops.cg("wk_cg_replace_r", n, b, q, r, st)
+            comm.allreduce_(f64[_RR:_RR + 1])
+            ops.cg("wk_cg_step_beta", st, hist)
+            ops.cg("wk_cg_update_p", n, r, p, st)
+            it = it_next
+    h = ops.read_state(st)
+    if h.breakdown:
+        raise BreakdownError(f"p.Ap <= 0 at iteration {h.iteration}; system is not SPD")
+    return x[:n], hist[: h.iteration + 1]
+
+
+def bench_cg(grid, iters, dist, timed):
+    """Strong-scaling CG on the 7-point Laplacian grid^3 (bench.py, N >= 1)."""
+    from . import corpus
+
+    op = stencil_slab_operator(grid, grid, None, corpus.points_7pt(), dist, fmt="sellp", weak=False, nz=grid)
+    b = op.ops.zeros(op.n_local) + 1.0
+    cg_solve(op, b, 1e-30, 50)
+    torch.cuda.synchronize()
+    op.comm.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    _, hist = cg_solve(op, b, 1e-30, iters)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = op.comm.max_scalar(t0.elapsed_time(t1))
+    it = len(hist) - 1
+    return {"workload": f"distributed CG, 7-point Laplacian {grid}^3 z-slab partitioned over {op.comm.world} GPUs, "
+                        f"SELL-P(64), tol 1e-30, {iters} iterations", "iterations": it, "ms": round(ms, 2),
+            "it_per_s": round(it / (ms * 1e-3), 1), "n_gpus": op.comm.world, "scaling": "strong",
+            "halo_bytes_per_spmv": op.plan.bytes_per_exchange}
