@@ -1,0 +1,91 @@
+"""Drop-in into the reference's own registry and harness.
+
+The reference package (`warpkit`) is importable from `baseline/_ref` (the
+offline install of /root/reference, git-ignored, shipped to the GPU box) or,
+in the build container, from /root/reference/pkg/src. Without either, these
+tests skip. CPU part: registration only. GPU part: warpkit's own public
+functions and its benchmark harness (`run_benchmark`, which checks every
+result against warpkit's sequential oracle) run on the b200 executor."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+for cand in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(cand, "warpkit")) and cand not in sys.path:
+        sys.path.append(cand)
+        break
+
+warpkit = pytest.importorskip("warpkit")
+
+
+@pytest.fixture(scope="module")
+def installed():
+    from paper_2006_14290_b200 import warpkit_plugin
+
+    return warpkit_plugin.install(warpkit)
+
+
+def test_registration(installed):
+    import importlib
+
+    wd = importlib.import_module("warpkit.dispatch")
+
+    assert "b200" in wd.EXEC_KINDS
+    ex = wd.make_executor("b200")
+    assert ex.kind == "b200"
+    for name in ("spmv_coo", "spmv_csr", "spmv_sellp", "cg", "reduce_microbench"):
+        assert wd.get_operation(name).impls["b200"] is not None
+    # the reference's own executors are untouched
+    assert wd.make_executor("ref").kind == "reference"
+    from warpkit.bench import BenchConfig
+
+    BenchConfig(corpus=".", execs=("ref", "b200"))  # accepted by the harness' validation
+
+
+@pytest.mark.gpu
+def test_reference_api_on_b200(installed):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from warpkit.corpus import poisson2d_matrix, random_sparse_matrix
+    from warpkit.kernels import cg_solve, spmv_coo, spmv_csr, spmv_sellp
+    from warpkit.sparse import coo_to_csr, coo_to_sellp, dense_spmv_reference
+
+    ex = warpkit.make_executor("b200")
+    ref = warpkit.make_executor("ref")
+    rng = np.random.default_rng(1234)
+    m = random_sparse_matrix(80, 80, 0.2, rng)
+    x = rng.random(80)
+    y = dense_spmv_reference(m, x)
+    assert np.array_equal(spmv_sellp(coo_to_sellp(m, 64), x, ex), y)
+    assert np.array_equal(spmv_csr(coo_to_csr(m), x, ex), y)
+    assert np.max(np.abs(spmv_coo(m, x, ex) - y)) <= 1e-12 * max(1.0, np.abs(y).max()) * 80
+    assert ex.counters.lane_steps == m.nnz
+    sp = coo_to_sellp(poisson2d_matrix(12), 64)
+    b = np.ones(sp.nrows)
+    xr, hr = cg_solve(sp, b, 1e-10, 500, ref)
+    xg, hg = warpkit.dispatch("cg", ex, sp, b, 1e-10, 500)
+    assert len(hg) == len(hr)
+    assert np.max(np.abs(hg - hr)) / np.linalg.norm(b) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_reference_harness_on_b200(installed, tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from warpkit.bench import BenchConfig, run_benchmark
+    from warpkit.corpus import generate_corpus
+
+    generate_corpus(tmp_path)
+    cfg = BenchConfig(corpus=tmp_path, kernels=("coo", "csr", "sellp", "cg"), execs=("ref", "b200"),
+                      warmup_iters=1, timed_iters=2)
+    res = run_benchmark(cfg)
+    rows = [r for r in res.records if r.exec == "b200"]
+    assert rows, "no b200 records"
+    bad = [(r.matrix, r.kernel, r.max_rel_err) for r in rows if not r.correct]
+    assert not bad, bad
