@@ -247,6 +247,11 @@ int wk_cg_init_finish(wk_cg_state* state, double tol, int64_t max_iters, double*
 /* state->pq = p.q (local) ; skipped when done */
 int wk_cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* state, void* workspace,
                  wk_stream_t stream);
+/* q = A p (masked by state->done) and state->pq = p.q (local) in one pass
+ * (fused into the SELL-P(64) TMA kernel; SpMV + reduction otherwise). p is
+ * the extended vector [owned | halo]; the dot covers the owned rows. */
+int wk_cg_spmv_dot(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
+                   wk_stream_t stream);
 /* after all-reduce of pq: breakdown check, alpha, iteration += 1 */
 int wk_cg_step_alpha(wk_cg_state* state, wk_stream_t stream);
 /* x += alpha p ; unless replacement (iteration % 50 == 0): r -= alpha q and

@@ -97,6 +97,7 @@ _SIGS = {
     "wk_cg_init_local": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
     "wk_cg_init_finish": (ctypes.c_int, [P, F64, I64, P, P]),
     "wk_cg_dot_pq": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_cg_spmv_dot": (ctypes.c_int, [P, P, P, P, P, P]),
     "wk_cg_step_alpha": (ctypes.c_int, [P, P]),
     "wk_cg_update_xr": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
     "wk_cg_replace_r": (ctypes.c_int, [I64, P, P, P, P, P, P]),

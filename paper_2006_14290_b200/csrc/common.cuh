@@ -50,6 +50,12 @@ void clear_error();
         }                                                                               \
     } while (0)
 
+#define WK_TRY(expr)          \
+    do {                      \
+        int _rc = (expr);     \
+        if (_rc) return _rc;  \
+    } while (0)
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Number of SMs of the current device (cached per device).
@@ -57,6 +63,11 @@ int sm_count();
 
 // Kernel-selection knob behind wk_config_set("sellp_kernel", ...).
 int set_sellp_kernel(int choice);
+
+// CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
+// if A cannot take the fused path.
+int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
+                   cudaStream_t st);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -20,11 +20,11 @@
 // Gram-Schmidt via batched dots and Givens rotations on one device thread).
 #include <vector>
 
+#include "cg_state.cuh"
 #include "reduce.cuh"
 
 namespace wk {
 
-constexpr int kReplaceEvery = 50;  // kernels.py:322
 
 template <typename F>
 __global__ void __launch_bounds__(256) masked_map_kernel(int64_t n, F f, const int* __restrict__ skip) {
@@ -55,33 +55,6 @@ static int launch_scalar(F f, cudaStream_t st) {
     WK_LAUNCH_CHECK();
     return 0;
 }
-
-// ---- CG scalar steps (shared by the epilogues and the 1-thread kernels) -----
-
-__device__ __forceinline__ void cg_alpha_step(wk_cg_state* s) {
-    if (s->done) return;
-    const double pq = s->pq;
-    if (pq <= 0.0) {  // kernels.py:317-318 (NaN falls through, as in Python)
-        s->breakdown = 1;
-        s->done = 1;
-        s->iteration += 1;
-        return;
-    }
-    s->alpha = s->rho / pq;
-    s->iteration += 1;
-}
-
-__device__ __forceinline__ void cg_beta_step(wk_cg_state* s, double* hist) {
-    if (s->done) return;
-    const double rr = s->rr;
-    const double rn = sqrt(rr);
-    hist[s->iteration] = rn;
-    s->beta = rr / s->rho;
-    s->rho = rr;
-    s->done = !(s->iteration < s->max_iters && rn > s->threshold);
-}
-
-__device__ __forceinline__ bool cg_replacing(const wk_cg_state* s) { return s->iteration % kReplaceEvery == 0; }
 
 // ---- CG building blocks -------------------------------------------------------
 
@@ -136,8 +109,139 @@ static int cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* s
         ws, &s->done, st);
 }
 
+// q = A p and state->pq = p.q: fused into the SELL-P(64) kernel when
+// possible, else SpMV then a separate reduction.
+static int cg_spmv_dot(const wk_matrix* A, int64_t n, const double* p, double* q, wk_cg_state* s, void* ws,
+                       bool finalize, cudaStream_t st) {
+    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st);
+    if (rc != 1) return rc;
+    WK_TRY(wk_spmv_masked(A, p, q, &s->done, st));
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!s->done) {
+                s->pq = 0.0;
+                if (finalize) cg_alpha_step(s);
+            }
+        }, st);
+    return cg_dot_pq(n, p, q, s, ws, finalize, st);
+}
+
+// Vectorised CG vector updates (double2, two independent pairs in flight per
+// thread, restrict-qualified so loads are issued ahead of the stores). Same
+// arithmetic as the scalar lambdas below (and as kernels.py:320-329).
+static bool vec_ok(const void* a, const void* b, const void* c, const void* d) {
+    auto al = [](const void* v) { return (reinterpret_cast<uintptr_t>(v) & 15) == 0; };
+    return al(a) && al(b) && al(c) && al(d);
+}
+
+static int vec_grid(int64_t n) {
+    int64_t g = ceil_div(ceil_div(n, 2), 256 * 2);
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (g > cap) g = cap;
+    if (g > kRedMaxBlocks) g = kRedMaxBlocks;
+    return int(g < 1 ? 1 : g);
+}
+
+__global__ void __launch_bounds__(256)
+cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
+                 double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize) {
+    if (s->done) return;
+    const double alpha = s->alpha;
+    const bool repl = cg_replacing(s);
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    double acc = 0.0;
+    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np; k += 2 * T) {
+        const int64_t k1 = k + T;
+        const bool h1 = k1 < np;
+        double2 pa = __ldcs(p2 + k), xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
+        if (h1) {
+            pb = __ldcs(p2 + k1);
+            xb = __ldcs(x2 + k1);
+        }
+        if (!repl) {
+            qa = __ldcs(q2 + k);
+            ra = __ldcs(r2 + k);
+            if (h1) {
+                qb = __ldcs(q2 + k1);
+                rb = __ldcs(r2 + k1);
+            }
+        }
+        xa.x = __dadd_rn(xa.x, __dmul_rn(alpha, pa.x));
+        xa.y = __dadd_rn(xa.y, __dmul_rn(alpha, pa.y));
+        __stcs(x2 + k, xa);
+        if (h1) {
+            xb.x = __dadd_rn(xb.x, __dmul_rn(alpha, pb.x));
+            xb.y = __dadd_rn(xb.y, __dmul_rn(alpha, pb.y));
+            __stcs(x2 + k1, xb);
+        }
+        if (!repl) {
+            ra.x = __dadd_rn(ra.x, -__dmul_rn(alpha, qa.x));
+            ra.y = __dadd_rn(ra.y, -__dmul_rn(alpha, qa.y));
+            r2[k] = ra;
+            acc += __dmul_rn(ra.x, ra.x);
+            acc += __dmul_rn(ra.y, ra.y);
+            if (h1) {
+                rb.x = __dadd_rn(rb.x, -__dmul_rn(alpha, qb.x));
+                rb.y = __dadd_rn(rb.y, -__dmul_rn(alpha, qb.y));
+                r2[k1] = rb;
+                acc += __dmul_rn(rb.x, rb.x);
+                acc += __dmul_rn(rb.y, rb.y);
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = n - 1;
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        if (!repl) {
+            r[i] = __dadd_rn(r[i], -__dmul_rn(alpha, q[i]));
+            acc += __dmul_rn(r[i], r[i]);
+        }
+    }
+    double total;
+    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0 && !repl) {
+        s->rr = total;
+        if (finalize) cg_beta_step(s, hist);
+    }
+}
+
+__global__ void __launch_bounds__(256)
+cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, const wk_cg_state* s) {
+    if (s->done) return;
+    const double beta = s->beta;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np; k += 2 * T) {
+        const int64_t k1 = k + T;
+        const bool h1 = k1 < np;
+        double2 ra = __ldcs(r2 + k), pa = p2[k], rb{0, 0}, pb{0, 0};
+        if (h1) {
+            rb = __ldcs(r2 + k1);
+            pb = p2[k1];
+        }
+        pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
+        pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
+        p2[k] = pa;
+        if (h1) {
+            pb.x = __dadd_rn(rb.x, __dmul_rn(beta, pb.x));
+            pb.y = __dadd_rn(rb.y, __dmul_rn(beta, pb.y));
+            p2[k1] = pb;
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
+}
+
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
                         double* hist, void* ws, bool finalize, cudaStream_t st) {
+    if (n > 0 && vec_ok(p, q, x, r)) {
+        cg_update_xr_vec<<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0);
+        WK_LAUNCH_CHECK();
+        return 0;
+    }
     return launch_map_reduce(
         n,
         [=] __device__(int64_t i) {
@@ -175,6 +279,11 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
 }
 
 static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st) {
+    if (n > 0 && vec_ok(r, p, r, p)) {
+        cg_update_p_vec<<<vec_grid(n), 256, 0, st>>>(n, r, p, s);
+        WK_LAUNCH_CHECK();
+        return 0;
+    }
     return launch_masked_map(
         n, [=] __device__(int64_t i) { p[i] = __dadd_rn(r[i], __dmul_rn(s->beta, p[i])); }, &s->done, st);
 }
@@ -225,12 +334,6 @@ static int capture(GraphRunner& g, Body body) {
 
 using namespace wk;
 
-#define WK_TRY(expr)              \
-    do {                          \
-        int _rc = (expr);         \
-        if (_rc) return _rc;      \
-    } while (0)
-
 extern "C" {
 
 // ---------------- CG building blocks (distributed path) -------------------------
@@ -252,6 +355,12 @@ int wk_cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* state
     if (n == 0)
         return launch_scalar([=] __device__() { if (!state->done) state->pq = 0.0; }, as_stream(stream));
     return cg_dot_pq(n, p, q, state, workspace, false, as_stream(stream));
+}
+
+int wk_cg_spmv_dot(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
+                   wk_stream_t stream) {
+    clear_error();
+    return cg_spmv_dot(A, A->nrows, p, q, state, workspace, false, as_stream(stream));
 }
 
 int wk_cg_step_alpha(wk_cg_state* state, wk_stream_t stream) {
@@ -324,8 +433,7 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     WK_TRY(cg_init_finish(s, tol, max_iters, hist, st));
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kReplaceEvery; ++i) {
-            WK_TRY(wk_spmv_masked(A, p, q, &s->done, cs));
-            WK_TRY(cg_dot_pq(n, p, q, s, red, true, cs));
+            WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs));
             WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs));
             if (i == kReplaceEvery - 1) {
                 WK_TRY(wk_spmv_masked(A, x, q, &s->done, cs));

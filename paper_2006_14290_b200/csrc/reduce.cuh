@@ -43,10 +43,11 @@ inline int red_grid(int64_t n) {
 
 // Block-level: reduce `v`, publish the partial, and return true in the (single)
 // last-arriving block, where `total` (thread 0) holds the grid total.
+template <int kThreads = kRedThreads>
 __device__ __forceinline__ bool grid_reduce_last(double v, RedWorkspace ws, double& total) {
-    __shared__ double red[kRedThreads / 32];
+    __shared__ double red[kThreads / 32];
     __shared__ bool is_last;
-    const double bsum = block_sum<kRedThreads>(v, red);
+    const double bsum = block_sum<kThreads>(v, red);
     if (threadIdx.x == 0) {
         ws.partials[blockIdx.x] = bsum;
         __threadfence();
@@ -57,9 +58,9 @@ __device__ __forceinline__ bool grid_reduce_last(double v, RedWorkspace ws, doub
     if (!is_last) return false;
     __threadfence();
     double acc = 0.0;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += kRedThreads) acc += __ldcg(ws.partials + b);
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) acc += __ldcg(ws.partials + b);
     __syncthreads();  // `red` reuse
-    total = block_sum<kRedThreads>(acc, red);
+    total = block_sum<kThreads>(acc, red);
     if (threadIdx.x == 0) *ws.ticket = 0;
     return true;
 }

@@ -13,7 +13,8 @@
 // flight while the current chunk's gathers resolve.
 #pragma once
 
-#include "common.cuh"
+#include "cg_state.cuh"
+#include "reduce.cuh"
 
 namespace wk {
 
@@ -49,11 +50,14 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
     }
 }
 
-template <class Cfg>
+// kDot: also accumulate sum_r x[r] * y[r] over the owned rows (CG's p.Ap with
+// x = p, y = q) and publish it through DotEpilogue (last-arriving CTA).
+template <class Cfg, bool kDot = false>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
 sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
                    const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
-                   const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip) {
+                   const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip,
+                   DotEpilogue dot) {
     constexpr int J = Cfg::kJ, S = Cfg::kS, WARPS = Cfg::kWarps, CH = Cfg::kChunk;
     if (skip != nullptr && *skip) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -105,6 +109,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     for (int st = 0; st < S && pvalid; ++st) issue(st);
 
     uint32_t i = 0;  // chunks consumed by this warp
+    double dacc = 0.0;
     for (int64_t s = gwarp; s < nslices; s += nwarps) {
         const int64_t s0 = __ldg(sets + s);
         const int w = int(__ldg(sets + s + 1) - s0);
@@ -134,21 +139,36 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         }
         if (r0 + 1 < nrows) {
             __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
+            if (kDot) {
+                const double2 p = *reinterpret_cast<const double2*>(x + r0);
+                dacc += __dmul_rn(p.x, a0);
+                dacc += __dmul_rn(p.y, a1);
+            }
         } else if (r0 < nrows) {
             st_stream(y + r0, a0);
+            if (kDot) dacc += __dmul_rn(x[r0], a0);
+        }
+    }
+    if (kDot) {
+        RedWorkspace ws{dot.partials, dot.ticket};
+        double total;
+        if (grid_reduce_last<WARPS * 32>(dacc, ws, total) && threadIdx.x == 0) {
+            dot.state->pq = total;
+            if (dot.finalize) cg_alpha_step(dot.state);
         }
     }
 }
 
 // Launch one configuration (persistent grid: one CTA per SM).
-template <class Cfg>
+template <class Cfg, bool kDot = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
-                       const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st) {
+                       const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
+                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0}) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
@@ -156,8 +176,8 @@ int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const 
     int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
     const int64_t need = ceil_div(nslices, Cfg::kWarps);
     if (grid > need) grid = need;
-    sellp64_tma_kernel<Cfg><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(nrows, ncols, nslices, sets, col,
-                                                                                val, row_lengths, x, y, skip);
+    sellp64_tma_kernel<Cfg, kDot><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
+        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot);
     WK_LAUNCH_CHECK();
     return 0;
 }

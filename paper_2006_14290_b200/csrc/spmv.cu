@@ -127,7 +127,7 @@ static bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(
 static int g_sellp_choice = -1;
 
 int set_sellp_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 8, WK_ERR_INVALID, "sellp kernel choice must be in [0, 8]");
+    WK_REQUIRE(choice >= 0 && choice <= 10, WK_ERR_INVALID, "sellp kernel choice must be in [0, 10]");
     g_sellp_choice = choice;
     return 0;
 }
@@ -164,6 +164,8 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
             case 5: WK_TMA(4, 4, 8, 2);
             case 6: WK_TMA(2, 6, 20, 1);
             case 8: WK_TMA(4, 5, 12, 1);
+            case 9: WK_TMA(8, 3, 12, 1);
+            case 10: WK_TMA(8, 2, 16, 1);
             case 7: WK_TMA(4, 3, 16, 1);  // best measured (profiles/r01/sellp_sweep.jsonl)
             default: WK_TMA(4, 4, 16, 1);
         }
@@ -180,6 +182,21 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
     }
     WK_LAUNCH_CHECK();
     return 0;
+}
+
+// CG's q = A p with p.q fused into the SpMV (SELL-P(64) TMA kernel only).
+// Returns 1 when the operand cannot take the fused path (caller falls back to
+// SpMV + separate dot), 0 on success, an error code otherwise.
+int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
+                   cudaStream_t st) {
+    if (A->format != WK_FMT_SELLP || A->slice_size != 64 || sellp_kernel_choice() == 0 || !aligned(A->values, 16) ||
+        !aligned(A->col_idx, 16) || !aligned(q, 16) || !aligned(p, 16) || A->nrows == 0)
+        return 1;
+    char* w = reinterpret_cast<char*>(red_ws);
+    DotEpilogue dot{reinterpret_cast<double*>(w),
+                    reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize};
+    return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
+                                                             A->values, A->row_lengths, p, q, &s->done, st, dot);
 }
 
 int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col,

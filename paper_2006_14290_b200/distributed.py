@@ -138,6 +138,11 @@ class DeviceOps:
         done = ctypes.c_void_p(state.data_ptr() + _lib.WkCgState.done.offset)
         _lib.call("wk_spmv_masked", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), done, self.stream())
 
+    def spmv_dot(self, local, p_ext, q, state):
+        """q = A p and state.pq = p.q (local part) in one fused pass."""
+        _lib.call("wk_cg_spmv_dot", local.wk_ptr(), D._ptr(p_ext), D._ptr(q), D._ptr(state), D._ptr(self.ws.red),
+                  self.stream())
+
     # CG building blocks (state = 80-byte wk_cg_state in a uint8 tensor)
     def new_state(self):
         return torch.zeros(ctypes.sizeof(_lib.WkCgState), dtype=torch.uint8, device=self.device)
@@ -421,8 +426,7 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters):
         for _ in range(REPLACE_EVERY):
             it_next = it + 1
             op.exchange(p)
-            ops.spmv_masked(op.local, p, q, st)
-            ops.cg("wk_cg_dot_pq", n, p, q, st)
+            ops.spmv_dot(op.local, p, q, st)
             comm.allreduce_(f64[_PQ:_PQ + 1])
             ops.cg("wk_cg_step_alpha", st)
             ops.cg("wk_cg_update_xr", n, p, q, x, r, st)

@@ -49,6 +49,10 @@ class NumpyOps:
         if not self._get(state, "done"):
             self.spmv(local, x_ext, y)
 
+    def spmv_dot(self, local, p_ext, q, state):
+        self.spmv_masked(local, p_ext, q, state)
+        self.cg("wk_cg_dot_pq", local.nrows, p_ext, q, state)
+
     def new_state(self):
         return torch.zeros(ctypes.sizeof(ST), dtype=torch.uint8)
 
