@@ -343,10 +343,12 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
 
     res = {}
     K, W = max(5, args.steps // 2), 3
-    flush_buf = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=x.device)
+    flush_buf = torch.ones(512 * 1024 * 1024 // 8, dtype=torch.float64, device=x.device)
 
     def flush():
-        flush_buf.fill_(1.0)
+        # read (not write) 512 MB: evicts the L2 without leaving dirty lines
+        # whose write-back would be charged to the timed kernel
+        flush_buf.sum()
 
     def rec(name, d, xx, flush_l2=False, nnz=None):
         yy = torch.empty(d.nrows, dtype=torch.float64, device=x.device)
@@ -358,14 +360,14 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
                      "GB/s": round(b / (ms * 1e-3) / 1e9, 1), "frac_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4),
                      "bytes": int(b), "nnz": int(nz)}
         if flush_l2:
-            res[name]["l2"] = "flushed (512 MB write) before every launch"
+            res[name]["l2"] = "flushed (512 MB read) before every launch"
         return yy
 
     rec("sellp_27pt_200", A_sellp, x)
-    rec("csr_27pt_200", A_csr, x)
-    A_csr.with_strategy("subwarp", 0)
-    rec("csr_subwarp_27pt_200", A_csr, x)
-    A_csr.with_strategy("stream", 0)
+    for strat in ("rowblock", "stream", "subwarp"):
+        A_csr.with_strategy(strat, 0)
+        rec(f"csr_{strat}_27pt_200", A_csr, x)
+    A_csr.with_strategy("auto", 0)
     ell = D.csr_to_ell(A_csr)
     rec("ell_27pt_200", ell, x)
     del ell
@@ -385,7 +387,9 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
     # config 1: CSR on the 2-D Poisson 1000^2 (80 MB: flush L2 before every launch)
     P = corpus.poisson2d_matrix(1000)
     xp = torch.rand(P.ncols, dtype=torch.float64, device=x.device)
-    rec("csr_poisson2d_1000", P, xp, flush_l2=True)
+    for strat in ("rowblock", "stream"):
+        P.with_strategy(strat, 0)
+        rec(f"csr_{strat}_poisson2d_1000", P, xp, flush_l2=True)
     del P
     # config 3: COO and Hybrid on R-MAT scale 24
     R = corpus.rmat(RMAT_SCALE)

@@ -49,18 +49,20 @@ enum {
 
 enum { WK_FMT_CSR = 0, WK_FMT_COO = 1, WK_FMT_ELL = 2, WK_FMT_SELLP = 3, WK_FMT_HYBRID = 4 };
 
-/* CSR SpMV strategies: STREAM = nnz-chunked, shared-memory staged,
- * load-balanced (bitwise for rows <= 1024 entries); SUBWARP = one
- * power-of-two tile of lanes per row (kernels.py:163-196). */
-enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1 };
+/* CSR SpMV strategies: STREAM = nnz-chunked, TMA-staged, load-balanced for
+ * any row-length distribution (bitwise for rows <= 256 entries); SUBWARP = one
+ * power-of-two tile of lanes per row (kernels.py:163-196); ROWBLOCK = blocks
+ * of 32k consecutive rows, TMA-staged, one lane folds one row (bitwise for
+ * rows <= 64 entries; the fastest for regular matrices). */
+enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1, WK_CSR_ROWBLOCK = 2 };
 
 const char* wk_last_error(void);
 int wk_version(void);
 /* number of SMs of the current device */
 int wk_device_sm_count(void);
-/* process-wide kernel selection knobs (A/B measurement): key "sellp_kernel":
- * 0 = register-only SELL-P kernel, 1..5 = TMA pipeline configurations
- * (J.S.W = 8.4.8, 8.2.16, 4.4.16, 16.2.8, 4.3.20) */
+/* process-wide kernel selection knobs (A/B measurement): "sellp_kernel":
+ * 0 = register-only SELL-P kernel, 1..10 = TMA pipeline configurations
+ * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr */
 int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */

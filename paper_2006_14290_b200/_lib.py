@@ -20,7 +20,7 @@ WK_ERR_BREAKDOWN = 1003
 WK_ERR_SLICE = 1004
 
 WK_FMT_CSR, WK_FMT_COO, WK_FMT_ELL, WK_FMT_SELLP, WK_FMT_HYBRID = range(5)
-WK_CSR_STREAM, WK_CSR_SUBWARP = 0, 1
+WK_CSR_STREAM, WK_CSR_SUBWARP, WK_CSR_ROWBLOCK = 0, 1, 2
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

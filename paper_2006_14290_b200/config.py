@@ -14,7 +14,7 @@ from typing import Mapping
 WARP_SIZE = 32
 MAX_TUNING_VALUE = 1024
 REQUIRED_TUNING_KEYS = ("block_size", "subwarps_per_block", "csr_subwarp_size")
-CSR_STRATEGIES = ("stream", "subwarp")
+CSR_STRATEGIES = ("auto", "stream", "rowblock", "subwarp")
 HYBRID_STRATEGIES = ("minimal_storage", "imbalance_limit")
 
 
@@ -29,7 +29,8 @@ DEFAULT_TUNING = {
     # 0 = auto: next power of two of the mean row length, <= 32
     "csr_subwarp_size": 0,
     # B200 additions
-    "csr_strategy": "stream",
+    # auto: rowblock for regular row lengths, stream (load-balanced) otherwise
+    "csr_strategy": "auto",
     "sellp_slice_size": 64,
     "hybrid_strategy": "minimal_storage",
     "hybrid_percent": 0.8,

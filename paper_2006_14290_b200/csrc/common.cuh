@@ -63,6 +63,7 @@ int sm_count();
 
 // Kernel-selection knob behind wk_config_set("sellp_kernel", ...).
 int set_sellp_kernel(int choice);
+int set_csr_kernel(int choice);
 
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.
@@ -116,14 +117,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of spinning on issue slots.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(smem_addr(bar)), "r"(parity)
+        : "r"(smem_addr(bar)), "r"(parity), "r"(0x100000u)
         : "memory");
     return ok != 0;
 }

@@ -17,6 +17,7 @@
 // x != 0, +0 + -0 == +0) as long as x[0] is finite; if it is not, the
 // kernels switch to the `row_lengths`-bounded loop of the oracle.
 #include "common.cuh"
+#include "csr_tma.cuh"
 #include "sellp_tma.cuh"
 
 namespace wk {
@@ -142,6 +143,27 @@ static int sellp_kernel_choice() {
     return choice;
 }
 
+// CSR kernel selection for A/B measurements (env WK_CSR_KERNEL or
+// wk_config_set("csr_kernel", i)). Stream strategy: 0 = one CTA per nnz chunk,
+// otherwise the persistent TMA pipeline. Row-block strategy: 2..7 force one
+// configuration, otherwise (default 1) the configuration follows the mean row
+// length.
+static int g_csr_choice = -1;
+
+int set_csr_kernel(int choice) {
+    WK_REQUIRE(choice >= 0 && choice <= 7, WK_ERR_INVALID, "csr kernel choice must be in [0, 7]");
+    g_csr_choice = choice;
+    return 0;
+}
+
+static int csr_kernel_choice() {
+    if (g_csr_choice < 0) {
+        const char* e = getenv("WK_CSR_KERNEL");
+        g_csr_choice = (e != nullptr) ? atoi(e) : 1;
+    }
+    return g_csr_choice;
+}
+
 static int log2i(int64_t v) {
     int l = 0;
     while ((int64_t(1) << l) < v) ++l;
@@ -229,8 +251,7 @@ int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
 // arrive (atomic ticket) adds the partials in chunk order — deterministic,
 // but reassociated, so long rows are checked with the 1e-12 tolerance.
 // ---------------------------------------------------------------------------
-constexpr int kCsrChunk = 1024;
-constexpr int kCsrCap = 2 * kCsrChunk;
+// kCsrChunk / kCsrCap: csr_tma.cuh (shared plan geometry)
 
 __global__ void csr_plan_kernel(int64_t nrows, int64_t nnz, int64_t nchunks, const int* __restrict__ ptrs,
                                 int* __restrict__ first) {
@@ -374,10 +395,31 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
                unsigned* tickets, const int* skip, cudaStream_t st) {
     (void)ncols;
     if (nrows == 0) return 0;
+    if (strategy == WK_CSR_ROWBLOCK) {
+        // 32*k-row blocks; the stage capacity is the smallest that keeps a
+        // 32-row block of mean-length rows "light" (more warps per SM when
+        // rows are short). Measured sweep: profiles/r01/csr_sweep.jsonl.
+        switch (csr_kernel_choice()) {
+            case 2: return launch_csr_rowblock<CsrRbCfg<8, 2, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            case 3: return launch_csr_rowblock<CsrRbCfg<16, 1, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            case 4: return launch_csr_rowblock<CsrRbCfg<16, 2, 512>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            case 5: return launch_csr_rowblock<CsrRbCfg<20, 1, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            case 6: return launch_csr_rowblock<CsrRbCfg<24, 1, 640>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            case 7: return launch_csr_rowblock<CsrRbCfg<12, 2, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+            default: break;
+        }
+        const double need = 32.0 * double(nnz) / double(nrows) * 1.25;
+        if (need <= 640.0) return launch_csr_rowblock<CsrRbCfg<24, 1, 640>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+        if (need <= 768.0) return launch_csr_rowblock<CsrRbCfg<20, 1, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+        return launch_csr_rowblock<CsrRbCfg<16, 1, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+    }
     if (strategy == WK_CSR_STREAM) {
         WK_REQUIRE(first != nullptr && partials != nullptr && tickets != nullptr, WK_ERR_INVALID,
                    "csr stream strategy needs a plan (wk_csr_plan_build)");
         const int64_t nchunks = csr_stream_chunks(nnz);
+        if (csr_kernel_choice() != 0)
+            return launch_csr_tma<CsrTmaCfg<16, 2>>(nrows, nnz, nchunks, ptrs, col, val, x, y, first, partials,
+                                                    tickets, skip, st);
         csr_stream_kernel<<<(unsigned)nchunks, kSpmvThreads, 0, st>>>(nrows, nnz, ptrs, col, val, x, y, first,
                                                                      partials, tickets, skip);
         WK_LAUNCH_CHECK();
@@ -537,8 +579,8 @@ int64_t wk_csr_plan_chunks(int64_t nnz) { return csr_stream_chunks(nnz); }
 
 int64_t wk_csr_plan_bytes(int64_t nnz) {
     const int64_t c = csr_stream_chunks(nnz);
-    // first[c+1] int32 | pad | partials[2c] f64 | tickets[c] u32
-    return ceil_div((c + 1) * 4, 16) * 16 + 2 * c * 8 + ceil_div(c * 4, 16) * 16;
+    // first[c+1] int32 (padded to 16 B) | item descriptors[c] int4 | partials[2c] f64 | tickets[c] u32
+    return csr_first_slots(c) * 4 + c * 16 + 2 * c * 8 + ceil_div(c * 4, 16) * 16;
 }
 
 int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream) {
@@ -546,8 +588,11 @@ int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void*
     const int64_t c = csr_stream_chunks(nnz);
     cudaStream_t st = as_stream(stream);
     WK_CUDA(cudaMemsetAsync(plan, 0, size_t(wk_csr_plan_bytes(nnz)), st));
-    csr_plan_kernel<<<(unsigned)ceil_div(nrows + 1, 256), 256, 0, st>>>(nrows, nnz, c, row_ptrs,
-                                                                      reinterpret_cast<int*>(plan));
+    int* first = reinterpret_cast<int*>(plan);
+    csr_plan_kernel<<<(unsigned)ceil_div(nrows + 1, 256), 256, 0, st>>>(nrows, nnz, c, row_ptrs, first);
+    WK_LAUNCH_CHECK();
+    csr_items_kernel<<<(unsigned)ceil_div(c, 256), 256, 0, st>>>(c, row_ptrs, first,
+                                                                reinterpret_cast<int4*>(first + csr_first_slots(c)));
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -556,7 +601,7 @@ static void csr_plan_views(void* plan, int64_t nnz, int** first, double** partia
     const int64_t c = csr_stream_chunks(nnz);
     char* p = reinterpret_cast<char*>(plan);
     *first = reinterpret_cast<int*>(p);
-    p += ceil_div((c + 1) * 4, 16) * 16;
+    p += csr_first_slots(c) * 4 + c * 16;
     *partials = reinterpret_cast<double*>(p);
     p += 2 * c * 8;
     *tickets = reinterpret_cast<unsigned*>(p);

@@ -125,6 +125,7 @@ class DeviceCsr(DeviceMatrix):
         self._wk = None
         self.strategy = _lib.WK_CSR_STREAM
         self.subwarp = 0
+        self._auto = None
 
     def plan(self):
         """nnz-chunk plan of the load-balanced stream kernel (built once)."""
@@ -135,8 +136,22 @@ class DeviceCsr(DeviceMatrix):
                       stream_handle(self.device))
         return self._plan
 
+    def auto_strategy(self):
+        """rowblock when every row is short and the mean is moderate (one lane
+        folds one row from a TMA-staged block), stream otherwise (nnz-balanced
+        for skewed row lengths). Decided once per matrix (one D2H read)."""
+        if getattr(self, "_auto", None) is None:
+            if self.nrows == 0:
+                self._auto = "stream"
+            else:
+                maxlen = max_row_length(self)
+                self._auto = "rowblock" if maxlen <= 64 and self.nnz <= 28 * self.nrows else "stream"
+        return self._auto
+
     def with_strategy(self, strategy, subwarp=0):
-        st = {"stream": _lib.WK_CSR_STREAM, "subwarp": _lib.WK_CSR_SUBWARP}[strategy]
+        if strategy == "auto":
+            strategy = self.auto_strategy()
+        st = {"stream": _lib.WK_CSR_STREAM, "subwarp": _lib.WK_CSR_SUBWARP, "rowblock": _lib.WK_CSR_ROWBLOCK}[strategy]
         if st != self.strategy or subwarp != self.subwarp:
             self.strategy, self.subwarp = st, int(subwarp)
             self._wk = None

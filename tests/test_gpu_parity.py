@@ -60,10 +60,21 @@ def test_sellp_golden_bitwise(wk, ex, case):
         assert y.tobytes() == case.y.tobytes(), f"slice {s}"
 
 
+CSR_LONG_ROW = 256  # kCsrChunk: longer rows are split across work items (tolerance)
+
+
+CSR_BITWISE_ROW = {"stream": 256, "rowblock": 64}  # rows up to this length fold bitwise
+
+
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
-def test_csr_stream_golden_bitwise(wk, ex, case):
-    y = wk.spmv_csr(_host(wk, case.csr, "csr"), case.x, ex)
-    assert y.tobytes() == case.y.tobytes()
+@pytest.mark.parametrize("strategy", ["stream", "rowblock", "auto"])
+def test_csr_stream_golden_bitwise(wk, case, strategy):
+    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
+    y = wk.spmv_csr(_host(wk, case.csr, "csr"), case.x, e)
+    lens = np.diff(case.csr.row_ptrs)
+    short = lens <= min(CSR_BITWISE_ROW.values())
+    assert y[short].tobytes() == case.y[short].tobytes()
+    assert sparse_ref.max_scaled_rel_err(y, case.y, lens) <= TOL
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -194,10 +205,15 @@ def test_long_rows_stream_kernel(wk, ex, rng):
     x = rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
     y = wk.spmv_csr(csr, x, ex)
-    short = lens <= 1024
+    short = lens <= CSR_LONG_ROW
     assert y[short].tobytes() == y_ref[short].tobytes()
     assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
     assert wk.spmv_csr(csr, x, ex).tobytes() == y.tobytes()  # deterministic
+    # forced row-block strategy: heavy blocks (long rows) take the warp-reduction path
+    eb = wk.make_executor("b200", device=0, tuning={"csr_strategy": "rowblock"})
+    yb = wk.spmv_csr(csr, x, eb)
+    assert yb[lens <= 64].tobytes() == y_ref[lens <= 64].tobytes()
+    assert sparse_ref.max_scaled_rel_err(yb, y_ref, lens) <= TOL
     coo = wk.csr_to_coo(csr, ex)
     assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
     hyb = wk.csr_to_hybrid(csr, exec=ex)

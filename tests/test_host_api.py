@@ -32,7 +32,7 @@ class TestLibrary:
         L = _lib.load()
         assert L.wk_version() >= 1
         assert L.wk_reduce_workspace_bytes() > 0
-        assert L.wk_csr_plan_chunks(0) == 1 and L.wk_csr_plan_chunks(1025) == 2
+        assert L.wk_csr_plan_chunks(0) == 1 and L.wk_csr_plan_chunks(257) == 2
         assert L.wk_cg_workspace_bytes(1000) > 3 * 8000
 
     def test_sm100a_cubin_only(self):
@@ -63,7 +63,7 @@ class TestExecutor:
     def test_custom_tuning(self):
         ex = wk.make_executor("b200", tuning={"block_size": 128, "subwarps_per_block": 32, "csr_subwarp_size": 4})
         assert ex.config.tuning["csr_subwarp_size"] == 4
-        assert ex.config.tuning["csr_strategy"] == "stream"
+        assert ex.config.tuning["csr_strategy"] == "auto"
 
     def test_tuning_validation(self):
         with pytest.raises(ValueError):
