@@ -263,6 +263,13 @@ int wk_cg_update_xr(int64_t n, const double* p, const double* q, double* x, doub
 /* replacement iteration only: r = b - q (q = A x) ; state->rr = r.r (local) */
 int wk_cg_replace_r(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state, void* workspace,
                     wk_stream_t stream);
+/* fused variants (one launch each instead of two): the alpha step evaluated
+ * from the all-reduced p.Ap inside the x/r update, and the beta step from the
+ * all-reduced r.r inside the p update */
+int wk_cg_update_xr_alpha(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* state,
+                          void* workspace, wk_stream_t stream);
+int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist, void* workspace,
+                        wk_stream_t stream);
 /* after all-reduce of rr: hist, beta, rho := rr, done */
 int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream);
 /* p = r + beta p ; skipped when done */

@@ -102,6 +102,8 @@ _SIGS = {
     "wk_cg_update_xr": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
     "wk_cg_replace_r": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_cg_step_beta": (ctypes.c_int, [P, P, P]),
+    "wk_cg_update_xr_alpha": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
+    "wk_cg_update_p_beta": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_cg_update_p": (ctypes.c_int, [I64, P, P, P, P]),
 }
 

@@ -142,19 +142,35 @@ static int vec_grid(int64_t n) {
     return int(g < 1 ? 1 : g);
 }
 
+// kAlphaIn: the alpha step (kernels.py:316-321) is evaluated here from the
+// all-reduced p.Ap (distributed path) instead of by a separate 1-thread kernel.
+template <bool kAlphaIn>
 __global__ void __launch_bounds__(256)
 cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
                  double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize) {
     if (s->done) return;
-    const double alpha = s->alpha;
-    const bool repl = cg_replacing(s);
+    double alpha;
+    bool repl, brk = false;
+    int64_t it_new = 0;
+    if (kAlphaIn) {
+        const double pq = s->pq;
+        it_new = s->iteration + 1;
+        brk = pq <= 0.0;  // kernels.py:317 (NaN falls through)
+        alpha = s->rho / pq;
+        repl = it_new % kReplaceEvery == 0;
+    } else {
+        alpha = s->alpha;
+        repl = cg_replacing(s);
+    }
+    const int64_t n_eff = brk ? 0 : n;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* q2 = reinterpret_cast<const double2*>(q);
     double2* x2 = reinterpret_cast<double2*>(x);
     double2* r2 = reinterpret_cast<double2*>(r);
     double acc = 0.0;
-    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np; k += 2 * T) {
+    const int64_t np_eff = n_eff >> 1;
+    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np_eff; k += 2 * T) {
         const int64_t k1 = k + T;
         const bool h1 = k1 < np;
         double2 pa = __ldcs(p2 + k), xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
@@ -193,7 +209,7 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
             }
         }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    if ((n_eff & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = n - 1;
         x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
         if (!repl) {
@@ -202,16 +218,31 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
         }
     }
     double total;
-    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0 && !repl) {
-        s->rr = total;
-        if (finalize) cg_beta_step(s, hist);
+    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0) {
+        if (kAlphaIn) {
+            s->iteration = it_new;
+            if (brk) {
+                s->breakdown = 1;
+                s->done = 1;
+                return;
+            }
+            s->alpha = alpha;
+        }
+        if (!repl) {
+            s->rr = total;
+            if (finalize) cg_beta_step(s, hist);
+        }
     }
 }
 
+// kBetaIn: beta = r.r / rho is evaluated here from the all-reduced r.r and the
+// last block performs the beta step (history, rho, convergence flag).
+template <bool kBetaIn>
 __global__ void __launch_bounds__(256)
-cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, const wk_cg_state* s) {
+cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, wk_cg_state* s, double* hist,
+                RedWorkspace ws) {
     if (s->done) return;
-    const double beta = s->beta;
+    const double beta = kBetaIn ? s->rr / s->rho : s->beta;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
@@ -233,12 +264,16 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
         }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
+    if (kBetaIn) {
+        double total;
+        if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) cg_beta_step(s, hist);
+    }
 }
 
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
                         double* hist, void* ws, bool finalize, cudaStream_t st) {
     if (n > 0 && vec_ok(p, q, x, r)) {
-        cg_update_xr_vec<<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0);
+        cg_update_xr_vec<false><<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0);
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -280,7 +315,8 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
 
 static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st) {
     if (n > 0 && vec_ok(r, p, r, p)) {
-        cg_update_p_vec<<<vec_grid(n), 256, 0, st>>>(n, r, p, s);
+        cg_update_p_vec<false><<<vec_grid(n), 256, 0, st>>>(n, r, p, const_cast<wk_cg_state*>(s), nullptr,
+                                                          RedWorkspace{nullptr, nullptr});
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -384,6 +420,26 @@ int wk_cg_replace_r(int64_t n, const double* b, const double* q, double* r, wk_c
         return launch_scalar([=] __device__() { if (!state->done && cg_replacing(state)) state->rr = 0.0; },
                              as_stream(stream));
     return cg_replace_r(n, b, q, r, state, nullptr, workspace, false, as_stream(stream));
+}
+
+int wk_cg_update_xr_alpha(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* state,
+                          void* workspace, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(vec_ok(p, q, x, r), WK_ERR_INVALID, "wk_cg_update_xr_alpha needs 16-byte aligned vectors");
+    cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, p, q, x, r, state, nullptr,
+                                                                                  red_ws(workspace), 0);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist, void* workspace,
+                        wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta needs 16-byte aligned vectors");
+    cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, r, p, state, hist,
+                                                                                 red_ws(workspace));
+    WK_LAUNCH_CHECK();
+    return 0;
 }
 
 int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream) {

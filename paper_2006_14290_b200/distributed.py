@@ -25,7 +25,7 @@ CUDA tensors are staged through host memory.
 """
 
 import ctypes
-import math
+import os
 
 import numpy as np
 import torch
@@ -56,8 +56,9 @@ class Comm:
         return self.backend == "gloo" and t.is_cuda
 
     def allreduce_(self, t):
-        """In-place sum all-reduce."""
-        if self.world == 1:
+        """In-place sum all-reduce (NCCL is called even for a single rank, so
+        the graph-captured path is the same code at every world size)."""
+        if self.world == 1 and self.backend != "nccl":
             return t
         if self._staged(t):
             h = t.cpu()
@@ -149,7 +150,8 @@ class DeviceOps:
 
     def cg(self, name, *args):
         conv = [D._ptr(a) if isinstance(a, torch.Tensor) else a for a in args]
-        if name in ("wk_cg_init_local", "wk_cg_dot_pq", "wk_cg_update_xr", "wk_cg_replace_r"):
+        if name in ("wk_cg_init_local", "wk_cg_dot_pq", "wk_cg_update_xr", "wk_cg_replace_r", "wk_cg_update_xr_alpha",
+                    "wk_cg_update_p_beta"):
             conv.append(D._ptr(self.ws.red))
         _lib.call(name, *conv, self.stream())
 
@@ -398,11 +400,20 @@ _RHO, _PQ, _RR = 0, 1, 2  # float64 slots of wk_cg_state
 REPLACE_EVERY = 50  # kernels.py:322, kReplaceEvery in krylov.cu
 
 
-def cg_solve(op: DistOperator, b_local, tol, max_iters):
+def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
     """Row-block distributed CG with the reference's update order
     (kernels.py:283-331), all scalars on the device. Returns (x_local, hist)
     (device tensors). Iteration control is identical on all ranks because
-    the all-reduced scalars are bit-identical."""
+    the all-reduced scalars are bit-identical.
+
+    Per iteration: halo exchange of p, q = A p with p.q fused (local), one
+    all-reduce, x/r update with the alpha step fused (local r.r), one
+    all-reduce, p update with the beta step fused; every 50th iteration the
+    true residual b - A x (exchange of x). With NCCL the 50-iteration period
+    is captured once as a CUDA graph (kernels + NCCL ops; host reads the
+    device `done` flag between replays); `graph=False` or WK_DIST_GRAPH=0
+    keeps the eager loop (always eager for gloo).
+    """
     ops, comm = op.ops, op.comm
     n = op.n_local
     if tol <= 0:
@@ -418,30 +429,58 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters):
     ops.cg("wk_cg_init_local", n, b, x, r, p, st)
     comm.allreduce_(f64[_RHO:_RHO + 1])
     ops.cg("wk_cg_init_finish", st, float(tol), int(max_iters), hist)
-    it = 0
-    while True:
-        h = ops.read_state(st)
-        if h.done:
-            break
-        for _ in range(REPLACE_EVERY):
-            it_next = it + 1
+
+    def period():
+        """One residual-replacement period: iterations 50k+1 .. 50k+50."""
+        for j in range(1, REPLACE_EVERY + 1):
             op.exchange(p)
             ops.spmv_dot(op.local, p, q, st)
             comm.allreduce_(f64[_PQ:_PQ + 1])
-            ops.cg("wk_cg_step_alpha", st)
-            ops.cg("wk_cg_update_xr", n, p, q, x, r, st)
-            if it_next % REPLACE_EVERY == 0:
+            ops.cg("wk_cg_update_xr_alpha", n, p, q, x, r, st)
+            if j == REPLACE_EVERY:
                 op.exchange(x)
                 ops.spmv_masked(op.local, x, q, st)
                 ops.cg("wk_cg_replace_r", n, b, q, r, st)
             comm.allreduce_(f64[_RR:_RR + 1])
-            ops.cg("wk_cg_step_beta", st, hist)
-            ops.cg("wk_cg_update_p", n, r, p, st)
-            it = it_next
+            ops.cg("wk_cg_update_p_beta", n, r, p, st, hist)
+
+    if graph is None:
+        graph = comm.backend == "nccl" and os.environ.get("WK_DIST_GRAPH", "1") != "0"
+    g = None
+    first = True
+    while not ops.read_state(st).done:
+        if g is None and graph and not first:
+            g = _capture(period)
+            if g is None:
+                graph = False
+        if g is not None:
+            g.replay()
+        else:
+            period()
+        first = False
     h = ops.read_state(st)
     if h.breakdown:
         raise BreakdownError(f"p.Ap <= 0 at iteration {h.iteration}; system is not SPD")
     return x[:n], hist[: h.iteration + 1]
+
+
+def _capture(fn):
+    """Capture fn() (kernels + NCCL collectives) into a CUDA graph; None if the
+    capture is refused (the caller then stays eager). The first period always
+    runs eagerly, so communicators and caches exist before the capture."""
+    try:
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            fn()
+        torch.cuda.synchronize()
+        return g
+    except Exception as exc:  # pragma: no cover - depends on the NCCL build
+        import warnings
+
+        warnings.warn(f"CUDA graph capture of the distributed CG period failed ({exc}); running eagerly")
+        torch.cuda.synchronize()
+        return None
 
 
 def bench_cg(grid, iters, dist, timed):

@@ -126,6 +126,16 @@ class NumpyOps:
             s(st, "beta", rr / g(st, "rho"))
             s(st, "rho", rr)
             s(st, "done", int(not (it < g(st, "max_iters") and math.sqrt(rr) > g(st, "threshold"))))
+        elif name == "wk_cg_update_xr_alpha":
+            self.cg("wk_cg_step_alpha", a[5])
+            self.cg("wk_cg_update_xr", *a)
+        elif name == "wk_cg_update_p_beta":
+            n, r, p, st, hist = a
+            if g(st, "done"):
+                return
+            beta = g(st, "rr") / g(st, "rho")
+            p[:n] = r + beta * p[:n]
+            self.cg("wk_cg_step_beta", st, hist)
         elif name == "wk_cg_update_p":
             n, r, p, st = a
             if not g(st, "done"):

@@ -97,6 +97,50 @@ def test_partitioned_formats(parts, fmt):
         assert y.tobytes() == ref.tobytes()
 
 
+def _nccl_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2006_14290_b200 import corpus
+        from paper_2006_14290_b200 import distributed as DI
+
+        opg = DI.stencil_slab_operator(24, 24, None, corpus.points_7pt(), dist, fmt="sellp", weak=False, nz=24)
+        b = torch.ones(opg.n_local, dtype=torch.float64, device="cuda")
+        res = {}
+        for graph in (False, True):
+            xs, hist = DI.cg_solve(opg, b, 1e-13, 500, graph=graph)
+            res[f"x_{graph}"] = xs.cpu().numpy()
+            res[f"hist_{graph}"] = hist.cpu().numpy()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_cg_nccl_graph_single_rank():
+    """The NCCL + CUDA-graph path of the distributed CG (one rank: the
+    all-reduces are real NCCL calls captured in the graph)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    res = out[0]
+    assert len(res["hist_True"]) > 51  # several graph replays
+    assert np.array_equal(res["hist_True"], res["hist_False"])
+    assert np.array_equal(res["x_True"], res["x_False"])
+    m = corpus_ref.stencil(24, 24, 24, corpus_ref.points_7pt())
+    sp = sparse_ref.csr_to_sellp(m, 64)
+    b = np.ones(m.nrows)
+    xr, hr = krylov_ref.cg_solve(lambda v: sparse_ref.spmv(sp, v), b, 1e-13, 500)
+    assert len(res["hist_True"]) == len(hr)
+    assert np.max(np.abs(res["hist_True"] - hr)) / np.linalg.norm(b) <= 1e-10
+
+
 def test_distributed_cg(parts):
     m = corpus_ref.stencil(12, 12, 12, corpus_ref.points_7pt())
     b = np.ones(m.nrows)
