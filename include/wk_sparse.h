@@ -275,6 +275,87 @@ int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream);
 /* p = r + beta p ; skipped when done */
 int wk_cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* state, wk_stream_t stream);
 
+/* ---- BiCGSTAB building blocks (oracle/krylov_ref.py bicgstab_solve order).
+ *      Vector steps reduce into the local slots of wk_bicg_state; the caller
+ *      all-reduces the named slot (distributed) and then runs the scalar step.
+ *      Every step is a no-op once `done` is set. ----------------------------- */
+typedef struct wk_bicg_state {
+    double rho, rho_new, alpha, omega, beta, threshold;
+    double rv, ss, tt, ts, rr; /* local partials: all-reduce rho_new, rv, ss, {tt,ts}, rr */
+    int64_t iteration, max_iters;
+    int32_t done, breakdown, apply_half, pad;
+} wk_bicg_state;
+
+/* x = 0, r = rh = b, p = v = 0 ; rr = b.b (local) */
+int wk_bicg_init(int64_t n, const double* b, double* x, double* r, double* rh, double* p, double* v,
+                 wk_bicg_state* st, void* workspace, wk_stream_t stream);
+/* after all-reduce of rr: hist[0] = ||b||, threshold, rho = alpha = omega = 1 */
+int wk_bicg_init_finish(wk_bicg_state* st, double tol, int64_t max_iters, double* hist, wk_stream_t stream);
+/* rho_new = rh.r (local) */
+int wk_bicg_rho(int64_t n, const double* rh, const double* r, wk_bicg_state* st, void* workspace, wk_stream_t stream);
+/* after all-reduce of rho_new: breakdown if 0, beta = (rho_new/rho)(alpha/omega) */
+int wk_bicg_step_beta(wk_bicg_state* st, wk_stream_t stream);
+/* p = r + beta (p - omega v) */
+int wk_bicg_update_p(int64_t n, const double* r, const double* v, double* p, wk_bicg_state* st, wk_stream_t stream);
+/* rv = rh.v (local) */
+int wk_bicg_rv(int64_t n, const double* rh, const double* v, wk_bicg_state* st, void* workspace, wk_stream_t stream);
+/* after all-reduce of rv: breakdown if 0, alpha = rho_new / rv */
+int wk_bicg_step_alpha(wk_bicg_state* st, wk_stream_t stream);
+/* s = r - alpha v ; ss = s.s (local) */
+int wk_bicg_update_s(int64_t n, const double* r, const double* v, double* s, wk_bicg_state* st, void* workspace,
+                     wk_stream_t stream);
+/* after all-reduce of ss: iteration += 1; half-step convergence test */
+int wk_bicg_step_s(wk_bicg_state* st, double* hist, wk_stream_t stream);
+/* on half-step convergence: x = x + alpha p (then clears the flag) */
+int wk_bicg_half_x(int64_t n, const double* p, double* x, wk_bicg_state* st, void* workspace, wk_stream_t stream);
+/* tt = t.t, ts = t.s (local) */
+int wk_bicg_tt_ts(int64_t n, const double* t, const double* s, wk_bicg_state* st, void* workspace,
+                  wk_stream_t stream);
+/* after all-reduce of {tt, ts}: breakdown if tt == 0, omega = ts / tt */
+int wk_bicg_step_omega(wk_bicg_state* st, wk_stream_t stream);
+/* x = x + alpha p + omega s ; r = s - omega t ; rr = r.r (local) */
+int wk_bicg_update_xr(int64_t n, const double* p, const double* s, const double* t, double* x, double* r,
+                      wk_bicg_state* st, void* workspace, wk_stream_t stream);
+/* after all-reduce of rr: hist, rho = rho_new, convergence */
+int wk_bicg_step_r(wk_bicg_state* st, double* hist, wk_stream_t stream);
+
+/* ---- GMRES(m) building blocks (classical Gram-Schmidt; oracle order).
+ *      H is (m+1) x m column-major; cs, sn: m; g: m+1; y: m. --------------- */
+typedef struct wk_gmres_state {
+    double beta, threshold, sq, hn; /* sq: local squared norm, all-reduced by the caller */
+    int64_t iteration, max_iters;
+    int32_t done, cycle_done, j_done, restart;
+} wk_gmres_state;
+
+/* x = 0, r = b ; sq = b.b (local) */
+int wk_gmres_init(int64_t n, const double* b, double* x, double* r, wk_gmres_state* st, void* workspace,
+                  wk_stream_t stream);
+/* after all-reduce of sq */
+int wk_gmres_init_finish(wk_gmres_state* st, double tol, int64_t max_iters, int32_t restart, double* hist,
+                         wk_stream_t stream);
+/* V0 = r / beta ; g = beta e1 ; opens a cycle */
+int wk_gmres_cycle_start(int64_t n, const double* r, double* V0, double* g, wk_gmres_state* st, wk_stream_t stream);
+/* Hj[i] = V_i . w for i <= j (local) */
+int wk_gmres_multidot(int64_t n, int32_t j, const double* V, int64_t ld, const double* w, double* Hj,
+                      wk_gmres_state* st, void* workspace, wk_stream_t stream);
+/* w = w - sum_i Hj[i] V_i (i order) ; sq = w.w (local) */
+int wk_gmres_orth(int64_t n, int32_t j, const double* V, int64_t ld, double* w, const double* Hj, wk_gmres_state* st,
+                  void* workspace, wk_stream_t stream);
+/* after all-reduce of sq: Givens rotations of column j, residual estimate,
+ * cycle termination test */
+int wk_gmres_givens(int32_t j, double* H, double* cs, double* sn, double* g, wk_gmres_state* st, double* hist,
+                    wk_stream_t stream);
+/* V_{j+1} = w / hn while the cycle continues */
+int wk_gmres_next_basis(int64_t n, const double* w, double* Vn, wk_gmres_state* st, wk_stream_t stream);
+/* y = H^-1 g (back substitution) ; x = x + sum y_i V_i */
+int wk_gmres_update_x(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y,
+                      double* x, wk_gmres_state* st, wk_stream_t stream);
+/* r = b - w (w = A x) ; sq = r.r (local) */
+int wk_gmres_residual(int64_t n, const double* b, const double* w, double* r, wk_gmres_state* st, void* workspace,
+                      wk_stream_t stream);
+/* after all-reduce of sq: beta, true residual replaces the last history entry, convergence */
+int wk_gmres_restart(wk_gmres_state* st, double* hist, wk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

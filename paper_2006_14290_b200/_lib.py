@@ -48,6 +48,17 @@ class WkCgState(ctypes.Structure):
                 ("iteration", I64), ("max_iters", I64), ("done", I32), ("breakdown", I32)]
 
 
+class WkBicgState(ctypes.Structure):
+    _fields_ = [(n, F64) for n in ("rho", "rho_new", "alpha", "omega", "beta", "threshold", "rv", "ss", "tt", "ts",
+                                   "rr")] + [("iteration", I64), ("max_iters", I64), ("done", I32),
+                                             ("breakdown", I32), ("apply_half", I32), ("pad", I32)]
+
+
+class WkGmresState(ctypes.Structure):
+    _fields_ = [("beta", F64), ("threshold", F64), ("sq", F64), ("hn", F64), ("iteration", I64), ("max_iters", I64),
+                ("done", I32), ("cycle_done", I32), ("j_done", I32), ("restart", I32)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "wk_last_error": (ctypes.c_char_p, []),
@@ -105,6 +116,30 @@ _SIGS = {
     "wk_cg_update_xr_alpha": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
     "wk_cg_update_p_beta": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_cg_update_p": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_bicg_init": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
+    "wk_bicg_init_finish": (ctypes.c_int, [P, F64, I64, P, P]),
+    "wk_bicg_rho": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_step_beta": (ctypes.c_int, [P, P]),
+    "wk_bicg_update_p": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_rv": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_step_alpha": (ctypes.c_int, [P, P]),
+    "wk_bicg_update_s": (ctypes.c_int, [I64, P, P, P, P, P, P]),
+    "wk_bicg_step_s": (ctypes.c_int, [P, P, P]),
+    "wk_bicg_half_x": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_tt_ts": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_step_omega": (ctypes.c_int, [P, P]),
+    "wk_bicg_update_xr": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
+    "wk_bicg_step_r": (ctypes.c_int, [P, P, P]),
+    "wk_gmres_init": (ctypes.c_int, [I64, P, P, P, P, P, P]),
+    "wk_gmres_init_finish": (ctypes.c_int, [P, F64, I64, I32, P, P]),
+    "wk_gmres_cycle_start": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_gmres_multidot": (ctypes.c_int, [I64, I32, P, I64, P, P, P, P, P]),
+    "wk_gmres_orth": (ctypes.c_int, [I64, I32, P, I64, P, P, P, P, P]),
+    "wk_gmres_givens": (ctypes.c_int, [I32, P, P, P, P, P, P, P]),
+    "wk_gmres_next_basis": (ctypes.c_int, [I64, P, P, P, P]),
+    "wk_gmres_update_x": (ctypes.c_int, [I64, P, I64, P, P, P, P, P, P]),
+    "wk_gmres_residual": (ctypes.c_int, [I64, P, P, P, P, P, P]),
+    "wk_gmres_restart": (ctypes.c_int, [P, P, P]),
 }
 
 EXPORTED = tuple(sorted(_SIGS))

@@ -1,0 +1,638 @@
+// BiCGSTAB and GMRES(m) as device step kernels (no reference implementation;
+// update order of oracle/krylov_ref.py: van der Vorst BiCGSTAB, restarted
+// GMRES with classical Gram-Schmidt via batched dots and Givens rotations on
+// one device thread).
+//
+// Every vector step reduces into a LOCAL slot of the solver state; between a
+// vector step and the scalar step that consumes it the row-block distributed
+// driver (distributed.py) all-reduces that slot over NCCL, the single-GPU
+// solvers below simply run the scalar step next. All steps are no-ops once
+// the device `done` flag is set, so a fixed period can be captured as a CUDA
+// graph and replayed until convergence.
+#include "krylov_common.cuh"
+
+namespace wk {
+
+using BS = wk_bicg_state;
+using GS = wk_gmres_state;
+
+// ---------------------------------- BiCGSTAB ---------------------------------------
+
+static int bicg_init(int64_t n, const double* b, double* x, double* r, double* rh, double* p, double* v, BS* s,
+                     void* ws, cudaStream_t st) {
+    if (n == 0) return launch_scalar([=] __device__() { s->rr = 0.0; }, st);
+    return launch_map_reduce(
+        n,
+        [=] __device__(int64_t i) {
+            const double bi = b[i];
+            x[i] = 0.0;
+            r[i] = bi;
+            rh[i] = bi;
+            p[i] = 0.0;
+            v[i] = 0.0;
+            return __dmul_rn(bi, bi);
+        },
+        [=] __device__(double t) { s->rr = t; }, ws, nullptr, st);
+}
+
+static int bicg_init_finish(BS* s, double tol, int64_t max_iters, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        const double bn = sqrt(s->rr);
+        hist[0] = bn;
+        s->rho = s->alpha = s->omega = 1.0;
+        s->threshold = tol * bn;
+        s->iteration = 0;
+        s->max_iters = max_iters;
+        s->breakdown = 0;
+        s->apply_half = 0;
+        s->done = !(bn != 0.0 && 0 < max_iters && bn > s->threshold);
+    }, st);
+}
+
+template <typename F, typename E>
+static int local_dot(int64_t n, F f, E epi, void* ws, const int* skip, cudaStream_t st) {
+    if (n == 0) return launch_scalar([=] __device__() { if (!*skip) epi(0.0); }, st);
+    return launch_map_reduce(n, f, epi, ws, skip, st);
+}
+
+static int bicg_rho(int64_t n, const double* rh, const double* r, BS* s, void* ws, cudaStream_t st) {
+    return local_dot(
+        n, [=] __device__(int64_t i) { return __dmul_rn(rh[i], r[i]); },
+        [=] __device__(double t) { s->rho_new = t; }, ws, &s->done, st);
+}
+
+static int bicg_step_beta(BS* s, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        if (s->rho_new == 0.0) {
+            s->breakdown = 1;
+            s->done = 1;
+            s->iteration += 1;
+            return;
+        }
+        s->beta = __dmul_rn(s->rho_new / s->rho, s->alpha / s->omega);
+    }, st);
+}
+
+static int bicg_update_p(int64_t n, const double* r, const double* v, double* p, BS* s, cudaStream_t st) {
+    return launch_masked_map(
+        n,
+        [=] __device__(int64_t i) {
+            p[i] = __dadd_rn(r[i], __dmul_rn(s->beta, __dadd_rn(p[i], -__dmul_rn(s->omega, v[i]))));
+        },
+        &s->done, st);
+}
+
+static int bicg_rv(int64_t n, const double* rh, const double* v, BS* s, void* ws, cudaStream_t st) {
+    return local_dot(
+        n, [=] __device__(int64_t i) { return __dmul_rn(rh[i], v[i]); }, [=] __device__(double t) { s->rv = t; },
+        ws, &s->done, st);
+}
+
+static int bicg_step_alpha(BS* s, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        if (s->rv == 0.0) {
+            s->breakdown = 1;
+            s->done = 1;
+            s->iteration += 1;
+            return;
+        }
+        s->alpha = s->rho_new / s->rv;
+    }, st);
+}
+
+static int bicg_update_s(int64_t n, const double* r, const double* v, double* sv, BS* s, void* ws, cudaStream_t st) {
+    return local_dot(
+        n,
+        [=] __device__(int64_t i) {
+            const double si = __dadd_rn(r[i], -__dmul_rn(s->alpha, v[i]));
+            sv[i] = si;
+            return __dmul_rn(si, si);
+        },
+        [=] __device__(double t) { s->ss = t; }, ws, &s->done, st);
+}
+
+static int bicg_step_s(BS* s, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        s->iteration += 1;
+        const double sn = sqrt(s->ss);
+        if (sn <= s->threshold) {
+            hist[s->iteration] = sn;
+            s->apply_half = 1;
+            s->done = 1;
+        }
+    }, st);
+}
+
+static int bicg_half_x(int64_t n, const double* p, double* x, BS* s, void* ws, cudaStream_t st) {
+    if (n == 0) return launch_scalar([=] __device__() { s->apply_half = 0; }, st);
+    return launch_map_reduce(
+        n,
+        [=] __device__(int64_t i) {
+            if (s->apply_half) x[i] = __dadd_rn(x[i], __dmul_rn(s->alpha, p[i]));
+            return 0.0;
+        },
+        [=] __device__(double) { s->apply_half = 0; }, ws, nullptr, st);
+}
+
+static int bicg_tt_ts(int64_t n, const double* t, const double* sv, BS* s, void* ws, cudaStream_t st) {
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!s->done) s->tt = s->ts = 0.0;
+        }, st);
+    return launch_map_reduce_n<2>(
+        n,
+        [=] __device__(int64_t i, double(&acc)[2]) {
+            const double ti = t[i];
+            acc[0] += __dmul_rn(ti, ti);
+            acc[1] += __dmul_rn(ti, sv[i]);
+        },
+        [=] __device__(double(&tot)[2]) {
+            s->tt = tot[0];
+            s->ts = tot[1];
+        },
+        ws, &s->done, st);
+}
+
+static int bicg_step_omega(BS* s, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        if (s->tt == 0.0) {
+            s->breakdown = 1;
+            s->done = 1;
+            return;
+        }
+        s->omega = s->ts / s->tt;
+    }, st);
+}
+
+static int bicg_update_xr(int64_t n, const double* p, const double* sv, const double* t, double* x, double* r, BS* s,
+                          void* ws, cudaStream_t st) {
+    return local_dot(
+        n,
+        [=] __device__(int64_t i) {
+            x[i] = __dadd_rn(__dadd_rn(x[i], __dmul_rn(s->alpha, p[i])), __dmul_rn(s->omega, sv[i]));
+            const double ri = __dadd_rn(sv[i], -__dmul_rn(s->omega, t[i]));
+            r[i] = ri;
+            return __dmul_rn(ri, ri);
+        },
+        [=] __device__(double tot) { s->rr = tot; }, ws, &s->done, st);
+}
+
+static int bicg_step_r(BS* s, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        const double rn = sqrt(s->rr);
+        hist[s->iteration] = rn;
+        s->rho = s->rho_new;
+        s->done = !(s->iteration < s->max_iters && rn > s->threshold);
+    }, st);
+}
+
+// ----------------------------------- GMRES ---------------------------------------------
+
+static int gmres_init(int64_t n, const double* b, double* x, double* r, GS* s, void* ws, cudaStream_t st) {
+    if (n == 0) return launch_scalar([=] __device__() { s->sq = 0.0; }, st);
+    return launch_map_reduce(
+        n,
+        [=] __device__(int64_t i) {
+            x[i] = 0.0;
+            r[i] = b[i];
+            return __dmul_rn(b[i], b[i]);
+        },
+        [=] __device__(double t) { s->sq = t; }, ws, nullptr, st);
+}
+
+static int gmres_init_finish(GS* s, double tol, int64_t max_iters, int restart, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        const double bn = sqrt(s->sq);
+        hist[0] = bn;
+        s->beta = bn;
+        s->threshold = tol * bn;
+        s->iteration = 0;
+        s->max_iters = max_iters;
+        s->restart = restart;
+        s->done = !(bn != 0.0 && 0 < max_iters && bn > s->threshold);
+        s->cycle_done = s->done;
+        s->j_done = 0;
+    }, st);
+}
+
+static int gmres_cycle_start(int64_t n, const double* r, double* V0, double* g, GS* s, cudaStream_t st) {
+    WK_TRY(launch_masked_map(n, [=] __device__(int64_t i) { V0[i] = r[i] / s->beta; }, &s->done, st));
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        for (int i = 0; i <= s->restart; ++i) g[i] = 0.0;
+        g[0] = s->beta;
+        s->j_done = 0;
+        s->cycle_done = 0;
+    }, st);
+}
+
+template <int K>
+static int gmres_multidot_k(int64_t n, int k, const double* V, int64_t ld, const double* w, double* Hj, GS* s,
+                            void* ws, cudaStream_t st) {
+    return launch_map_reduce_n<K>(
+        n,
+        [=] __device__(int64_t i, double(&acc)[K]) {
+            const double wi = w[i];
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                if (q < k) acc[q] += __dmul_rn(V[int64_t(q) * ld + i], wi);
+        },
+        [=] __device__(double(&tot)[K]) {
+            for (int q = 0; q < k; ++q) Hj[q] = tot[q];
+        },
+        ws, &s->cycle_done, st);
+}
+
+static int gmres_multidot(int64_t n, int j, const double* V, int64_t ld, const double* w, double* Hj, GS* s, void* ws,
+                          cudaStream_t st) {
+    const int k = j + 1;
+    WK_REQUIRE(k <= kRedMaxVec, WK_ERR_INVALID, "GMRES restart must be < %d", kRedMaxVec);
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!s->cycle_done)
+                for (int q = 0; q < k; ++q) Hj[q] = 0.0;
+        }, st);
+    if (k <= 8) return gmres_multidot_k<8>(n, k, V, ld, w, Hj, s, ws, st);
+    if (k <= 16) return gmres_multidot_k<16>(n, k, V, ld, w, Hj, s, ws, st);
+    return gmres_multidot_k<kRedMaxVec>(n, k, V, ld, w, Hj, s, ws, st);
+}
+
+static int gmres_orth(int64_t n, int j, const double* V, int64_t ld, double* w, const double* Hj, GS* s, void* ws,
+                      cudaStream_t st) {
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!s->cycle_done) s->sq = 0.0;
+        }, st);
+    return launch_map_reduce(
+        n,
+        [=] __device__(int64_t i) {
+            double wi = w[i];
+            for (int q = 0; q <= j; ++q) wi = __dadd_rn(wi, -__dmul_rn(Hj[q], V[int64_t(q) * ld + i]));
+            w[i] = wi;
+            return __dmul_rn(wi, wi);
+        },
+        [=] __device__(double t) { s->sq = t; }, ws, &s->cycle_done, st);
+}
+
+static int gmres_givens(int j, double* H, double* cs_, double* sn_, double* g, GS* s, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->cycle_done) return;
+        const int m = s->restart;
+        double* Hj = H + int64_t(j) * (m + 1);
+        const double hn = sqrt(s->sq);
+        s->hn = hn;
+        Hj[j + 1] = hn;
+        for (int i = 0; i < j; ++i) {
+            const double a = Hj[i], c = Hj[i + 1];
+            Hj[i] = __dadd_rn(__dmul_rn(cs_[i], a), __dmul_rn(sn_[i], c));
+            Hj[i + 1] = __dadd_rn(-__dmul_rn(sn_[i], a), __dmul_rn(cs_[i], c));
+        }
+        const double a = Hj[j], c = Hj[j + 1];
+        double cj = 1.0, sj = 0.0;
+        if (c != 0.0) {
+            const double h = hypot(a, c);
+            cj = a / h;
+            sj = c / h;
+        }
+        cs_[j] = cj;
+        sn_[j] = sj;
+        Hj[j] = __dadd_rn(__dmul_rn(cj, Hj[j]), __dmul_rn(sj, Hj[j + 1]));
+        Hj[j + 1] = 0.0;
+        g[j + 1] = -__dmul_rn(sj, g[j]);
+        g[j] = __dmul_rn(cj, g[j]);
+        s->iteration += 1;
+        s->j_done = j + 1;
+        const double res = fabs(g[j + 1]);
+        hist[s->iteration] = res;
+        if (res <= s->threshold || s->iteration >= s->max_iters || hn == 0.0 || j + 1 == m) s->cycle_done = 1;
+    }, st);
+}
+
+static int gmres_next_basis(int64_t n, const double* w, double* Vn, GS* s, cudaStream_t st) {
+    return launch_masked_map(n, [=] __device__(int64_t i) { Vn[i] = w[i] / s->hn; }, &s->cycle_done, st);
+}
+
+static int gmres_update_x(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y, double* x,
+                          GS* s, cudaStream_t st) {
+    WK_TRY(launch_scalar([=] __device__() {
+        if (s->done) return;
+        const int m = s->restart, jd = s->j_done;
+        for (int i = jd - 1; i >= 0; --i) {
+            double acc = g[i];
+            for (int k = i + 1; k < jd; ++k) acc = __dadd_rn(acc, -__dmul_rn(H[i + int64_t(k) * (m + 1)], y[k]));
+            y[i] = acc / H[i + int64_t(i) * (m + 1)];
+        }
+    }, st));
+    return launch_masked_map(
+        n,
+        [=] __device__(int64_t i) {
+            const int jd = s->j_done;
+            double xi = x[i];
+            for (int q = 0; q < jd; ++q) xi = __dadd_rn(xi, __dmul_rn(y[q], V[int64_t(q) * ld + i]));
+            x[i] = xi;
+        },
+        &s->done, st);
+}
+
+static int gmres_residual(int64_t n, const double* b, const double* w, double* r, GS* s, void* ws, cudaStream_t st) {
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!s->done) s->sq = 0.0;
+        }, st);
+    return launch_map_reduce(
+        n,
+        [=] __device__(int64_t i) {
+            const double ri = __dadd_rn(b[i], -w[i]);
+            r[i] = ri;
+            return __dmul_rn(ri, ri);
+        },
+        [=] __device__(double t) { s->sq = t; }, ws, &s->done, st);
+}
+
+static int gmres_restart(GS* s, double* hist, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (s->done) return;
+        const double bt = sqrt(s->sq);
+        s->beta = bt;
+        hist[s->iteration] = bt;
+        s->done = !(s->iteration < s->max_iters && bt > s->threshold);
+        s->cycle_done = s->done;
+    }, st);
+}
+
+}  // namespace wk
+
+using namespace wk;
+
+extern "C" {
+
+// ---- exported steps (distributed driver) --------------------------------------------
+
+int wk_bicg_init(int64_t n, const double* b, double* x, double* r, double* rh, double* p, double* v,
+                 wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_init(n, b, x, r, rh, p, v, s, ws, as_stream(stream));
+}
+int wk_bicg_init_finish(wk_bicg_state* s, double tol, int64_t max_iters, double* hist, wk_stream_t stream) {
+    clear_error();
+    return bicg_init_finish(s, tol, max_iters, hist, as_stream(stream));
+}
+int wk_bicg_rho(int64_t n, const double* rh, const double* r, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_rho(n, rh, r, s, ws, as_stream(stream));
+}
+int wk_bicg_step_beta(wk_bicg_state* s, wk_stream_t stream) {
+    clear_error();
+    return bicg_step_beta(s, as_stream(stream));
+}
+int wk_bicg_update_p(int64_t n, const double* r, const double* v, double* p, wk_bicg_state* s, wk_stream_t stream) {
+    clear_error();
+    return bicg_update_p(n, r, v, p, s, as_stream(stream));
+}
+int wk_bicg_rv(int64_t n, const double* rh, const double* v, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_rv(n, rh, v, s, ws, as_stream(stream));
+}
+int wk_bicg_step_alpha(wk_bicg_state* s, wk_stream_t stream) {
+    clear_error();
+    return bicg_step_alpha(s, as_stream(stream));
+}
+int wk_bicg_update_s(int64_t n, const double* r, const double* v, double* sv, wk_bicg_state* s, void* ws,
+                     wk_stream_t stream) {
+    clear_error();
+    return bicg_update_s(n, r, v, sv, s, ws, as_stream(stream));
+}
+int wk_bicg_step_s(wk_bicg_state* s, double* hist, wk_stream_t stream) {
+    clear_error();
+    return bicg_step_s(s, hist, as_stream(stream));
+}
+int wk_bicg_half_x(int64_t n, const double* p, double* x, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_half_x(n, p, x, s, ws, as_stream(stream));
+}
+int wk_bicg_tt_ts(int64_t n, const double* t, const double* sv, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_tt_ts(n, t, sv, s, ws, as_stream(stream));
+}
+int wk_bicg_step_omega(wk_bicg_state* s, wk_stream_t stream) {
+    clear_error();
+    return bicg_step_omega(s, as_stream(stream));
+}
+int wk_bicg_update_xr(int64_t n, const double* p, const double* sv, const double* t, double* x, double* r,
+                      wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return bicg_update_xr(n, p, sv, t, x, r, s, ws, as_stream(stream));
+}
+int wk_bicg_step_r(wk_bicg_state* s, double* hist, wk_stream_t stream) {
+    clear_error();
+    return bicg_step_r(s, hist, as_stream(stream));
+}
+
+int wk_gmres_init(int64_t n, const double* b, double* x, double* r, wk_gmres_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return gmres_init(n, b, x, r, s, ws, as_stream(stream));
+}
+int wk_gmres_init_finish(wk_gmres_state* s, double tol, int64_t max_iters, int32_t restart, double* hist,
+                         wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(restart >= 1 && restart <= kRedMaxVec - 1, WK_ERR_INVALID, "restart must be in [1, %d]",
+               kRedMaxVec - 1);
+    return gmres_init_finish(s, tol, max_iters, restart, hist, as_stream(stream));
+}
+int wk_gmres_cycle_start(int64_t n, const double* r, double* V0, double* g, wk_gmres_state* s, wk_stream_t stream) {
+    clear_error();
+    return gmres_cycle_start(n, r, V0, g, s, as_stream(stream));
+}
+int wk_gmres_multidot(int64_t n, int32_t j, const double* V, int64_t ld, const double* w, double* Hj,
+                      wk_gmres_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    return gmres_multidot(n, j, V, ld, w, Hj, s, ws, as_stream(stream));
+}
+int wk_gmres_orth(int64_t n, int32_t j, const double* V, int64_t ld, double* w, const double* Hj, wk_gmres_state* s,
+                  void* ws, wk_stream_t stream) {
+    clear_error();
+    return gmres_orth(n, j, V, ld, w, Hj, s, ws, as_stream(stream));
+}
+int wk_gmres_givens(int32_t j, double* H, double* cs, double* sn, double* g, wk_gmres_state* s, double* hist,
+                    wk_stream_t stream) {
+    clear_error();
+    return gmres_givens(j, H, cs, sn, g, s, hist, as_stream(stream));
+}
+int wk_gmres_next_basis(int64_t n, const double* w, double* Vn, wk_gmres_state* s, wk_stream_t stream) {
+    clear_error();
+    return gmres_next_basis(n, w, Vn, s, as_stream(stream));
+}
+int wk_gmres_update_x(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y, double* x,
+                      wk_gmres_state* s, wk_stream_t stream) {
+    clear_error();
+    return gmres_update_x(n, V, ld, H, g, y, x, s, as_stream(stream));
+}
+int wk_gmres_residual(int64_t n, const double* b, const double* w, double* r, wk_gmres_state* s, void* ws,
+                      wk_stream_t stream) {
+    clear_error();
+    return gmres_residual(n, b, w, r, s, ws, as_stream(stream));
+}
+int wk_gmres_restart(wk_gmres_state* s, double* hist, wk_stream_t stream) {
+    clear_error();
+    return gmres_restart(s, hist, as_stream(stream));
+}
+
+// ---- single-GPU solvers composed of the same steps (no all-reduce) -------------------
+
+int64_t wk_bicgstab_workspace_bytes(int64_t n) {
+    return 256 + red_ws_bytes() + 256 + 6 * (ceil_div(n * 8, 256) * 256) + 256;
+}
+
+int wk_bicgstab_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, double* x, double* hist,
+                      int64_t* iterations, void* workspace, wk_stream_t stream) {
+    clear_error();
+    WK_TRY(check_square(A));
+    WK_REQUIRE(tol > 0, WK_ERR_INVALID, "tol must be positive");
+    const int64_t n = A->nrows;
+    Carver cv{reinterpret_cast<char*>(workspace)};
+    BS* s = cv.take<BS>(1);
+    void* red = cv.take<char>(red_ws_bytes());
+    double* r = cv.take<double>(n);
+    double* rh = cv.take<double>(n);
+    double* p = cv.take<double>(n);
+    double* v = cv.take<double>(n);
+    double* sv = cv.take<double>(n);
+    double* t = cv.take<double>(n);
+    cudaStream_t user = as_stream(stream);
+    GraphRunner g;
+    WK_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
+    cudaEvent_t ev;
+    WK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    WK_CUDA(cudaEventRecord(ev, user));
+    WK_CUDA(cudaStreamWaitEvent(g.cs, ev, 0));
+    cudaStream_t st = g.cs;
+    WK_CUDA(cudaMemsetAsync(red, 0, size_t(red_ws_bytes()), st));
+    WK_TRY(bicg_init(n, b, x, r, rh, p, v, s, red, st));
+    WK_TRY(bicg_init_finish(s, tol, max_iters, hist, st));
+    const int* done = &s->done;
+    constexpr int kChunk = 10;
+    int rc = capture(g, [&](cudaStream_t cs) -> int {
+        for (int i = 0; i < kChunk; ++i) {
+            WK_TRY(bicg_rho(n, rh, r, s, red, cs));
+            WK_TRY(bicg_step_beta(s, cs));
+            WK_TRY(bicg_update_p(n, r, v, p, s, cs));
+            WK_TRY(wk_spmv_masked(A, p, v, done, cs));
+            WK_TRY(bicg_rv(n, rh, v, s, red, cs));
+            WK_TRY(bicg_step_alpha(s, cs));
+            WK_TRY(bicg_update_s(n, r, v, sv, s, red, cs));
+            WK_TRY(bicg_step_s(s, hist, cs));
+            WK_TRY(bicg_half_x(n, p, x, s, red, cs));
+            WK_TRY(wk_spmv_masked(A, sv, t, done, cs));
+            WK_TRY(bicg_tt_ts(n, t, sv, s, red, cs));
+            WK_TRY(bicg_step_omega(s, cs));
+            WK_TRY(bicg_update_xr(n, p, sv, t, x, r, s, red, cs));
+            WK_TRY(bicg_step_r(s, hist, cs));
+        }
+        return 0;
+    });
+    if (rc) {
+        cudaEventDestroy(ev);
+        return rc;
+    }
+    BS h{};
+    for (;;) {
+        WK_CUDA(cudaMemcpyAsync(&h, s, sizeof(h), cudaMemcpyDeviceToHost, st));
+        WK_CUDA(cudaStreamSynchronize(st));
+        if (h.done) break;
+        WK_CUDA(cudaGraphLaunch(g.exec, st));
+    }
+    WK_CUDA(cudaEventRecord(ev, st));
+    WK_CUDA(cudaStreamWaitEvent(user, ev, 0));
+    cudaEventDestroy(ev);
+    *iterations = h.iteration;
+    if (h.breakdown) {
+        set_error("BiCGSTAB breakdown at iteration %lld", (long long)h.iteration);
+        return WK_ERR_BREAKDOWN;
+    }
+    return 0;
+}
+
+int64_t wk_gmres_workspace_bytes(int64_t n, int32_t restart) {
+    const int64_t m = restart;
+    const int64_t vec = ceil_div(n * 8, 256) * 256;
+    return 256 + red_ws_bytes() + 256 + (m + 1) * vec + 2 * vec + ceil_div((m + 1) * m * 8 + 4 * (m + 1) * 8, 256) * 256 +
+           256;
+}
+
+int wk_gmres_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, int32_t restart, double* x,
+                   double* hist, int64_t* iterations, void* workspace, wk_stream_t stream) {
+    clear_error();
+    WK_TRY(check_square(A));
+    WK_REQUIRE(tol > 0, WK_ERR_INVALID, "tol must be positive");
+    WK_REQUIRE(restart >= 1 && restart <= kRedMaxVec - 1, WK_ERR_INVALID, "restart must be in [1, %d]",
+               kRedMaxVec - 1);
+    const int64_t n = A->nrows;
+    const int m = restart;
+    Carver cv{reinterpret_cast<char*>(workspace)};
+    GS* s = cv.take<GS>(1);
+    void* red = cv.take<char>(red_ws_bytes());
+    const int64_t ld = ceil_div(n * 8, 256) * 256 / 8;
+    double* V = cv.take<double>(ld * (m + 1));
+    double* w = cv.take<double>(n);
+    double* r = cv.take<double>(n);
+    double* small = cv.take<double>((m + 1) * m + 4 * (m + 1));
+    double* H = small;
+    double* cs_ = H + (m + 1) * m;
+    double* sn_ = cs_ + (m + 1);
+    double* g = sn_ + (m + 1);
+    double* y = g + (m + 1);
+    cudaStream_t user = as_stream(stream);
+    GraphRunner gr;
+    WK_CUDA(cudaStreamCreateWithFlags(&gr.cs, cudaStreamNonBlocking));
+    cudaEvent_t ev;
+    WK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    WK_CUDA(cudaEventRecord(ev, user));
+    WK_CUDA(cudaStreamWaitEvent(gr.cs, ev, 0));
+    cudaStream_t st = gr.cs;
+    WK_CUDA(cudaMemsetAsync(red, 0, size_t(red_ws_bytes()), st));
+    WK_TRY(gmres_init(n, b, x, r, s, red, st));
+    WK_TRY(gmres_init_finish(s, tol, max_iters, m, hist, st));
+    const int* done = &s->done;
+    const int* cdone = &s->cycle_done;
+    int rc = capture(gr, [&](cudaStream_t cs) -> int {
+        WK_TRY(gmres_cycle_start(n, r, V, g, s, cs));
+        for (int j = 0; j < m; ++j) {
+            double* Vj = V + int64_t(j) * ld;
+            double* Hj = H + int64_t(j) * (m + 1);
+            WK_TRY(wk_spmv_masked(A, Vj, w, cdone, cs));
+            WK_TRY(gmres_multidot(n, j, V, ld, w, Hj, s, red, cs));
+            WK_TRY(gmres_orth(n, j, V, ld, w, Hj, s, red, cs));
+            WK_TRY(gmres_givens(j, H, cs_, sn_, g, s, hist, cs));
+            if (j + 1 < m) WK_TRY(gmres_next_basis(n, w, V + int64_t(j + 1) * ld, s, cs));
+        }
+        WK_TRY(gmres_update_x(n, V, ld, H, g, y, x, s, cs));
+        WK_TRY(wk_spmv_masked(A, x, w, done, cs));
+        WK_TRY(gmres_residual(n, b, w, r, s, red, cs));
+        WK_TRY(gmres_restart(s, hist, cs));
+        return 0;
+    });
+    if (rc) {
+        cudaEventDestroy(ev);
+        return rc;
+    }
+    GS h{};
+    for (;;) {
+        WK_CUDA(cudaMemcpyAsync(&h, s, sizeof(h), cudaMemcpyDeviceToHost, st));
+        WK_CUDA(cudaStreamSynchronize(st));
+        if (h.done) break;
+        WK_CUDA(cudaGraphLaunch(gr.exec, st));
+    }
+    WK_CUDA(cudaEventRecord(ev, st));
+    WK_CUDA(cudaStreamWaitEvent(user, ev, 0));
+    cudaEventDestroy(ev);
+    *iterations = h.iteration;
+    (void)cdone;
+    return 0;
+}
+
+}  // extern "C"

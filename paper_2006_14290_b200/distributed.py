@@ -155,9 +155,23 @@ class DeviceOps:
             conv.append(D._ptr(self.ws.red))
         _lib.call(name, *conv, self.stream())
 
-    def read_state(self, state):
-        h = _lib.WkCgState.from_buffer_copy(state.cpu().numpy().tobytes())
-        return h
+    def read_state(self, state, cls=None):
+        return (cls or _lib.WkCgState).from_buffer_copy(state.cpu().numpy().tobytes())
+
+    # generic step call: tensors -> device pointers, workspace appended on request
+    def step(self, name, *args, ws=False):
+        conv = [D._ptr(a) if isinstance(a, torch.Tensor) else a for a in args]
+        if ws:
+            conv.append(D._ptr(self.ws.red))
+        _lib.call(name, *conv, self.stream())
+
+    def new_struct(self, cls):
+        return torch.zeros(ctypes.sizeof(cls), dtype=torch.uint8, device=self.device)
+
+    def spmv_flag(self, local, x_ext, y, state, offset):
+        """y = A x, skipped while the int32 flag at `state + offset` is set."""
+        flag = ctypes.c_void_p(state.data_ptr() + offset)
+        _lib.call("wk_spmv_masked", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), flag, self.stream())
 
 
 # ---- partition plans ----------------------------------------------------------------------------
@@ -481,6 +495,139 @@ def _capture(fn):
         warnings.warn(f"CUDA graph capture of the distributed CG period failed ({exc}); running eagerly")
         torch.cuda.synchronize()
         return None
+
+
+def _slot(cls, name):
+    return getattr(cls, name).offset // 8
+
+
+def _run_periods(ops, comm, st, cls, period, graph):
+    """Replay `period` until the device `done` flag of state `st` is set;
+    CUDA-graph captured after the first (eager) period when `graph`."""
+    if graph is None:
+        graph = comm.backend == "nccl" and os.environ.get("WK_DIST_GRAPH", "1") != "0"
+    g = None
+    first = True
+    while not ops.read_state(st, cls).done:
+        if g is None and graph and not first:
+            g = _capture(period)
+            if g is None:
+                graph = False
+        if g is not None:
+            g.replay()
+        else:
+            period()
+        first = False
+    return ops.read_state(st, cls)
+
+
+def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=10):
+    """Row-block distributed BiCGSTAB (oracle/krylov_ref.py order): five
+    all-reduces per iteration (rh.r, rh.v, s.s, {t.t, t.s}, r.r) and two halo
+    exchanges (p before v = A p, s before t = A s). Returns (x_local, hist)."""
+    ops, comm = op.ops, op.comm
+    n = op.n_local
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    C = _lib.WkBicgState
+    x = ops.zeros(n)
+    r, rh, v, t = ops.zeros(n), ops.zeros(n), ops.zeros(n), ops.zeros(n)
+    p, sv = op.new_vector(), op.new_vector()
+    hist = ops.zeros(int(max_iters) + 1)
+    st = ops.new_struct(C)
+    f = st.view(torch.float64)
+    done = C.done.offset
+
+    def red(*names):
+        lo = _slot(C, names[0])
+        comm.allreduce_(f[lo:lo + len(names)])
+
+    ops.step("wk_bicg_init", n, b_local, x, r, rh, p, v, st, ws=True)
+    red("rr")
+    ops.step("wk_bicg_init_finish", st, float(tol), int(max_iters), hist)
+
+    def period():
+        for _ in range(chunk):
+            ops.step("wk_bicg_rho", n, rh, r, st, ws=True)
+            red("rho_new")
+            ops.step("wk_bicg_step_beta", st)
+            ops.step("wk_bicg_update_p", n, r, v, p, st)
+            op.exchange(p)
+            ops.spmv_flag(op.local, p, v, st, done)
+            ops.step("wk_bicg_rv", n, rh, v, st, ws=True)
+            red("rv")
+            ops.step("wk_bicg_step_alpha", st)
+            ops.step("wk_bicg_update_s", n, r, v, sv, st, ws=True)
+            red("ss")
+            ops.step("wk_bicg_step_s", st, hist)
+            ops.step("wk_bicg_half_x", n, p, x, st, ws=True)
+            op.exchange(sv)
+            ops.spmv_flag(op.local, sv, t, st, done)
+            ops.step("wk_bicg_tt_ts", n, t, sv, st, ws=True)
+            red("tt", "ts")
+            ops.step("wk_bicg_step_omega", st)
+            ops.step("wk_bicg_update_xr", n, p, sv, t, x, r, st, ws=True)
+            red("rr")
+            ops.step("wk_bicg_step_r", st, hist)
+
+    h = _run_periods(ops, comm, st, C, period, graph)
+    if h.breakdown:
+        raise BreakdownError(f"BiCGSTAB breakdown at iteration {h.iteration}")
+    return x, hist[: h.iteration + 1]
+
+
+def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=None):
+    """Row-block distributed restarted GMRES(m) with classical Gram-Schmidt:
+    per Arnoldi step one halo exchange, one all-reduce of the j+1 batched dots
+    and one of ||w||^2; Givens rotations on one device thread (replicated on
+    every rank). One cycle per CUDA-graph period. Returns (x_local, hist)."""
+    ops, comm = op.ops, op.comm
+    n, n_ext = op.n_local, op.n_local + op.n_halo
+    m = int(restart)
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if not (1 <= m <= 31):
+        raise ValueError("restart must be in [1, 31]")
+    C = _lib.WkGmresState
+    ld = ((n_ext + 31) // 32) * 32
+    V = ops.zeros((m + 1) * ld)
+    x = op.new_vector()
+    w, r = ops.zeros(n), ops.zeros(n)
+    H = ops.zeros((m + 1) * m)
+    cs, sn, g, y = ops.zeros(m + 1), ops.zeros(m + 1), ops.zeros(m + 1), ops.zeros(m + 1)
+    hist = ops.zeros(int(max_iters) + 1)
+    st = ops.new_struct(C)
+    f = st.view(torch.float64)
+    sq = _slot(C, "sq")
+    done, cdone = C.done.offset, C.cycle_done.offset
+
+    ops.step("wk_gmres_init", n, b_local, x, r, st, ws=True)
+    comm.allreduce_(f[sq:sq + 1])
+    ops.step("wk_gmres_init_finish", st, float(tol), int(max_iters), m, hist)
+
+    def period():
+        ops.step("wk_gmres_cycle_start", n, r, V[:n_ext], g, st)
+        for j in range(m):
+            Vj = V[j * ld: j * ld + n_ext]
+            Hj = H[j * (m + 1): j * (m + 1) + m + 1]
+            op.exchange(Vj)
+            ops.spmv_flag(op.local, Vj, w, st, cdone)
+            ops.step("wk_gmres_multidot", n, j, V, ld, w, Hj, st, ws=True)
+            comm.allreduce_(Hj[: j + 1])
+            ops.step("wk_gmres_orth", n, j, V, ld, w, Hj, st, ws=True)
+            comm.allreduce_(f[sq:sq + 1])
+            ops.step("wk_gmres_givens", j, H, cs, sn, g, st, hist)
+            if j + 1 < m:
+                ops.step("wk_gmres_next_basis", n, w, V[(j + 1) * ld: (j + 1) * ld + n_ext], st)
+        ops.step("wk_gmres_update_x", n, V, ld, H, g, y, x, st)
+        op.exchange(x)
+        ops.spmv_flag(op.local, x, w, st, done)
+        ops.step("wk_gmres_residual", n, b_local, w, r, st, ws=True)
+        comm.allreduce_(f[sq:sq + 1])
+        ops.step("wk_gmres_restart", st, hist)
+
+    h = _run_periods(ops, comm, st, C, period, graph)
+    return x[:n], hist[: h.iteration + 1]
 
 
 def bench_cg(grid, iters, dist, timed):

@@ -61,6 +61,14 @@ def _worker(rank, world, port, out):
         xs, hist = DI.cg_solve(opg, b, 1e-10, 500)
         res["cg_x"] = xs.cpu().numpy()
         res["cg_hist"] = hist.cpu().numpy()
+        # nonsymmetric convection-diffusion: distributed BiCGSTAB and GMRES(30)
+        opn = DI.stencil_slab_operator(10, 10, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist,
+                                       fmt="csr", weak=False, nz=10)
+        bn = torch.ones(opn.n_local, dtype=torch.float64, device="cuda")
+        xs, hist = DI.bicgstab_solve(opn, bn, 1e-10, 500)
+        res["bicg_x"], res["bicg_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        xs, hist = DI.gmres_solve(opn, bn, 1e-10, 500, restart=30)
+        res["gmres_x"], res["gmres_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
         out[rank] = res
     finally:
         dist.destroy_process_group()
@@ -114,6 +122,13 @@ def _nccl_worker(rank, world, port, out):
             xs, hist = DI.cg_solve(opg, b, 1e-13, 500, graph=graph)
             res[f"x_{graph}"] = xs.cpu().numpy()
             res[f"hist_{graph}"] = hist.cpu().numpy()
+            opn = DI.stencil_slab_operator(16, 16, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist,
+                                           fmt="sellp", weak=False, nz=16)
+            bn = torch.ones(opn.n_local, dtype=torch.float64, device="cuda")
+            xs, hist = DI.bicgstab_solve(opn, bn, 1e-12, 500, graph=graph)
+            res[f"bicg_hist_{graph}"] = hist.cpu().numpy()
+            xs, hist = DI.gmres_solve(opn, bn, 1e-12, 500, restart=10, graph=graph)
+            res[f"gmres_hist_{graph}"] = hist.cpu().numpy()
         out[rank] = res
     finally:
         dist.destroy_process_group()
@@ -132,6 +147,9 @@ def test_distributed_cg_nccl_graph_single_rank():
     res = out[0]
     assert len(res["hist_True"]) > 51  # several graph replays
     assert np.array_equal(res["hist_True"], res["hist_False"])
+    for k in ("bicg", "gmres"):
+        assert len(res[f"{k}_hist_True"]) > 12
+        assert np.array_equal(res[f"{k}_hist_True"], res[f"{k}_hist_False"])
     assert np.array_equal(res["x_True"], res["x_False"])
     m = corpus_ref.stencil(24, 24, 24, corpus_ref.points_7pt())
     sp = sparse_ref.csr_to_sellp(m, 64)
@@ -151,4 +169,21 @@ def test_distributed_cg(parts):
     assert len(h0) == len(hr)
     assert np.max(np.abs(h0 - hr)) / np.linalg.norm(b) <= 1e-10
     x = np.concatenate([p["cg_x"] for p in parts])
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
+
+
+@pytest.mark.parametrize("solver", ["bicg", "gmres"])
+def test_distributed_nonsymmetric(parts, solver):
+    m = corpus_ref.stencil(10, 10, 10, corpus_ref.points_7pt(beta=(1.0, 0.5, 0.25)))
+    b = np.ones(m.nrows)
+    f = lambda v: sparse_ref.spmv(m, v)  # noqa: E731
+    if solver == "bicg":
+        xr, hr = krylov_ref.bicgstab_solve(f, b, 1e-10, 500)
+    else:
+        xr, hr = krylov_ref.gmres_solve(f, b, 1e-10, 500, restart=30)
+    h0, h1 = parts[0][f"{solver}_hist"], parts[1][f"{solver}_hist"]
+    assert np.array_equal(h0, h1)
+    assert len(h0) == len(hr)
+    assert np.max(np.abs(h0 - hr)) / np.linalg.norm(b) <= 1e-10
+    x = np.concatenate([p[f"{solver}_x"] for p in parts])
     assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
