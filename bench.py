@@ -329,10 +329,15 @@ def run_gpu(args, rank, world, dist):
         out["formats"] = bench_formats(args, wk, corpus, D, A_csr, A, x, peak)
         del A_csr
         torch.cuda.empty_cache()
-        out["cg"] = bench_cg(args, wk, corpus, D)
+        out["cg"] = _safe(lambda: bench_cg(args, wk, corpus, D))
+        torch.cuda.empty_cache()
+        out["nonsymmetric"] = _safe(lambda: bench_nonsym(args, wk, corpus, D))
+        torch.cuda.empty_cache()
         line["cpu_baseline"] = cpu_sample(budget_s=args.cpu_budget)[0] if not args.no_cpu else None
     elif world > 1 and not args.quick:
-        out["cg"] = part_cg(args, dist, world)
+        out["cg"] = _safe(lambda: part_cg(args, dist, world))
+        torch.cuda.empty_cache()
+        out["nonsymmetric"] = _safe(lambda: part_nonsym(args, dist, world))
     line.update(out)
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -428,6 +433,64 @@ def bench_cg(args, wk, corpus, D):
             "iterations": it, "ms": round(ms, 2), "it_per_s": round(it / (ms * 1e-3), 1),
             "GB/s_effective": round(per_it * it / (ms * 1e-3) / 1e9, 1), "bytes_per_iteration": int(per_it),
             "n_gpus": 1}
+
+
+def _safe(fn):
+    """Extra sections must never take the headline line down with them."""
+    try:
+        return fn()
+    except Exception as exc:  # pragma: no cover - reported in the JSON line
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+NONSYM_GRID = 512   # config 5: 7-point convection-diffusion 512^3
+NONSYM_ITERS = {"bicgstab": 50, "gmres": 60}
+
+
+def _nonsym_bytes(n, spmv_b, kind, iters, restart=30):
+    """Algorithmic bytes per iteration: BiCGSTAB = 2 SpMV + 19 vector passes;
+    GMRES(m) inner step j = SpMV + (2j + 6) vector passes (CGS dots, update,
+    norm, scale), averaged over the iterations run, + one SpMV and 4 passes per
+    restart."""
+    if kind == "bicgstab":
+        return 2 * spmv_b + 19 * 8 * n
+    steps = [(i % restart) for i in range(iters)]
+    cyc = max(1, -(-iters // restart))
+    tot = sum(spmv_b + (2 * j + 6) * 8 * n for j in steps) + cyc * (spmv_b + 4 * 8 * n)
+    return tot / max(iters, 1)
+
+
+def bench_nonsym(args, wk, corpus, D):
+    import torch
+
+    A = D.csr_to_sellp(corpus.convection_diffusion3d(NONSYM_GRID), SLICE)
+    torch.cuda.empty_cache()
+    b = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    ex = wk.make_executor("b200")
+    out = {"workload": f"7-point convection-diffusion {NONSYM_GRID}^3 (beta = (1, 0.5, 0.25)), SELL-P({SLICE}), "
+                       f"b = ones, tol 1e-30, fixed iteration counts", "n_gpus": 1}
+    for kind, fn in (("bicgstab", lambda it: wk.bicgstab_solve(A, b, 1e-30, it, ex)),
+                     ("gmres", lambda it: wk.gmres_solve(A, b, 1e-30, it, ex, restart=30))):
+        iters = NONSYM_ITERS[kind]
+        fn(4)
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        x, hist = fn(iters)
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        it = len(hist) - 1
+        per_it = _nonsym_bytes(A.nrows, A.algorithmic_bytes(), kind, it)
+        out[kind] = {"iterations": it, "ms": round(ms, 2), "it_per_s": round(it / (ms * 1e-3), 2),
+                     "GB/s_effective": round(per_it * it / (ms * 1e-3) / 1e9, 1), "bytes_per_iteration": int(per_it)}
+    return out
+
+
+def part_nonsym(args, dist, world):
+    from paper_2006_14290_b200 import distributed as DI
+
+    return DI.bench_nonsym(NONSYM_GRID, NONSYM_ITERS, dist)
 
 
 def part_cg(args, dist, world):

@@ -651,3 +651,30 @@ def bench_cg(grid, iters, dist, timed):
                         f"SELL-P(64), tol 1e-30, {iters} iterations", "iterations": it, "ms": round(ms, 2),
             "it_per_s": round(it / (ms * 1e-3), 1), "n_gpus": op.comm.world, "scaling": "strong",
             "halo_bytes_per_spmv": op.plan.bytes_per_exchange}
+
+
+def bench_nonsym(grid, iters, dist):
+    """Strong-scaling BiCGSTAB and GMRES(30) on the 7-point convection-
+    diffusion grid^3 (BASELINE config 5), fixed iteration counts."""
+    from . import corpus
+
+    op = stencil_slab_operator(grid, grid, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist, fmt="sellp",
+                               weak=False, nz=grid)
+    b = op.ops.zeros(op.n_local) + 1.0
+    out = {"workload": f"distributed BiCGSTAB / GMRES(30), 7-point convection-diffusion {grid}^3 z-slab partitioned "
+                       f"over {op.comm.world} GPUs, SELL-P(64), tol 1e-30, fixed iteration counts",
+           "n_gpus": op.comm.world, "scaling": "strong"}
+    for kind, fn in (("bicgstab", lambda it: bicgstab_solve(op, b, 1e-30, it)),
+                     ("gmres", lambda it: gmres_solve(op, b, 1e-30, it, restart=30))):
+        fn(4)
+        torch.cuda.synchronize()
+        op.comm.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        _, hist = fn(iters[kind])
+        t1.record()
+        torch.cuda.synchronize()
+        ms = op.comm.max_scalar(t0.elapsed_time(t1))
+        it = len(hist) - 1
+        out[kind] = {"iterations": it, "ms": round(ms, 2), "it_per_s": round(it / (ms * 1e-3), 2)}
+    return out
