@@ -44,7 +44,9 @@ enum {
     WK_ERR_INVALID = 1001,   /* bad argument (ValueError in the reference)             */
     WK_ERR_DIMENSION = 1002, /* errors.py:47-48 DimensionMismatch                      */
     WK_ERR_BREAKDOWN = 1003, /* errors.py:55-56 BreakdownError (p.Ap <= 0, rho == 0 …) */
-    WK_ERR_SLICE = 1004      /* errors.py:51-52 InvalidSliceSize                        */
+    WK_ERR_SLICE = 1004,     /* errors.py:51-52 InvalidSliceSize                        */
+    WK_ERR_PARSE = 1005,     /* errors.py:69-70 ParseError (MatrixMarket)               */
+    WK_ERR_UNSUPPORTED = 1006 /* errors.py:73-74 UnsupportedFormat (MatrixMarket)       */
 };
 
 enum { WK_FMT_CSR = 0, WK_FMT_COO = 1, WK_FMT_ELL = 2, WK_FMT_SELLP = 3, WK_FMT_HYBRID = 4 };
@@ -53,8 +55,14 @@ enum { WK_FMT_CSR = 0, WK_FMT_COO = 1, WK_FMT_ELL = 2, WK_FMT_SELLP = 3, WK_FMT_
  * any row-length distribution (bitwise for rows <= 256 entries); SUBWARP = one
  * power-of-two tile of lanes per row (kernels.py:163-196); ROWBLOCK = blocks
  * of 32k consecutive rows, TMA-staged, one lane folds one row (bitwise for
- * rows <= 64 entries; the fastest for regular matrices). */
-enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1, WK_CSR_ROWBLOCK = 2 };
+ * rows <= 64 entries; the fastest for regular matrices); MERGE = merge-path
+ * tiles of 2048 (row end | nonzero) items per CTA, equal work whatever the
+ * row-length skew (rows inside one thread's 8 items fold bitwise, others are
+ * joined by deterministic segmented scans); LOAD_BALANCE = Ginkgo's
+ * load_balance: 1024 nonzeros per warp, warp segmented scans with row ids
+ * expanded from row_ptrs on the fly, atomics for the rows shared between
+ * warps (the fastest for skewed matrices; not deterministic in the last bits). */
+enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1, WK_CSR_ROWBLOCK = 2, WK_CSR_MERGE = 3, WK_CSR_LOAD_BALANCE = 4 };
 
 const char* wk_last_error(void);
 int wk_version(void);
@@ -80,14 +88,23 @@ int wk_spmv_ell_f64(int64_t nrows, int64_t ncols, int64_t width, int64_t stride,
                     wk_stream_t stream);
 
 /* replaces spmv_csr (kernels.py:413-414 -> 163-203); csr_spmv fixture
- * (csr_kernels.cu:30-31). `plan` (wk_csr_plan_bytes) is required for
- * WK_CSR_STREAM; subwarp_size <= 0 picks next_pow2(nnz/nrows) <= 32. */
+ * (csr_kernels.cu:30-31). `plan` is required for WK_CSR_STREAM
+ * (wk_csr_plan_bytes / wk_csr_plan_build) and for WK_CSR_MERGE
+ * (wk_csr_merge_plan_bytes / wk_csr_merge_plan_build; also holds the
+ * per-tile carries, so one SpMV at a time per plan) and for
+ * WK_CSR_LOAD_BALANCE (wk_csr_load_balance_plan_*); subwarp_size <= 0 picks
+ * next_pow2(nnz/nrows) <= 32. */
 int wk_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idx,
                     const double* values, const double* x, double* y, int32_t strategy, int32_t subwarp_size,
                     void* plan, wk_stream_t stream);
 int64_t wk_csr_plan_chunks(int64_t nnz);
 int64_t wk_csr_plan_bytes(int64_t nnz);
 int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream);
+int64_t wk_csr_merge_plan_bytes(int64_t nrows, int64_t nnz);
+int wk_csr_merge_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream);
+int64_t wk_csr_load_balance_plan_bytes(int64_t nnz);
+int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
+                                   wk_stream_t stream);
 
 /* replaces spmv_coo (kernels.py:409-410 -> 209-264); coo_spmv fixture
  * (coo_kernels.cu:34-35). Entries sorted row-major. accumulate = 0 zero-fills y. */
@@ -355,6 +372,27 @@ int wk_gmres_residual(int64_t n, const double* b, const double* w, double* r, wk
                       wk_stream_t stream);
 /* after all-reduce of sq: beta, true residual replaces the last history entry, convergence */
 int wk_gmres_restart(wk_gmres_state* st, double* hist, wk_stream_t stream);
+
+/* ---- MatrixMarket coordinate I/O on the host (replaces read_matrix_market /
+ *      write_matrix_market, sparse.py:269-354; multi-threaded parse). ----- */
+enum { WK_MM_REAL = 0, WK_MM_INTEGER = 1, WK_MM_PATTERN = 2 };
+typedef struct wk_mm_header {
+    int64_t nrows, ncols, nnz; /* declared sizes (nnz = entry lines)                  */
+    int32_t field;             /* WK_MM_*                                             */
+    int32_t symmetric;         /* 1: entries are mirrored (output <= 2 nnz)           */
+    int64_t body_offset;       /* byte offset of the first entry line                 */
+    int64_t body_line;         /* line number of the size line                        */
+} wk_mm_header;
+/* banner + size line; WK_ERR_PARSE / WK_ERR_UNSUPPORTED with a message */
+int wk_mm_read_header(const char* data, int64_t len, wk_mm_header* header);
+/* 0-based (row, col, value) triplets in file order (symmetric: entry, then
+ * its mirror); duplicates are left for from_entries to sum. nthreads <= 0:
+ * all hardware threads. */
+int wk_mm_parse_entries(const char* data, int64_t len, const wk_mm_header* header, int32_t nthreads,
+                        int64_t* rows, int64_t* cols, double* vals, int64_t capacity, int64_t* count);
+/* 'coordinate real general', %.17g values; out == NULL: *written = bytes needed */
+int wk_mm_write(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                const double* vals, char* out, int64_t capacity, int64_t* written);
 
 #ifdef __cplusplus
 }

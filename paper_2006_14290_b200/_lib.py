@@ -8,7 +8,8 @@ is no CPU fallback anywhere in the package.
 import ctypes
 import os
 
-from .errors import BreakdownError, DeviceError, DimensionMismatch, InvalidSliceSize, NativeLibraryMissing
+from .errors import (BreakdownError, DeviceError, DimensionMismatch, InvalidSliceSize, NativeLibraryMissing,
+                     ParseError, UnsupportedFormat)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libwk_sparse.so")
@@ -18,15 +19,24 @@ WK_ERR_INVALID = 1001
 WK_ERR_DIMENSION = 1002
 WK_ERR_BREAKDOWN = 1003
 WK_ERR_SLICE = 1004
+WK_ERR_PARSE = 1005
+WK_ERR_UNSUPPORTED = 1006
 
 WK_FMT_CSR, WK_FMT_COO, WK_FMT_ELL, WK_FMT_SELLP, WK_FMT_HYBRID = range(5)
-WK_CSR_STREAM, WK_CSR_SUBWARP, WK_CSR_ROWBLOCK = 0, 1, 2
+WK_CSR_STREAM, WK_CSR_SUBWARP, WK_CSR_ROWBLOCK, WK_CSR_MERGE, WK_CSR_LOAD_BALANCE = 0, 1, 2, 3, 4
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
 I32 = ctypes.c_int32
 F64 = ctypes.c_double
 U64 = ctypes.c_uint64
+
+
+class WkMmHeader(ctypes.Structure):
+    """Mirror of `wk_mm_header` (include/wk_sparse.h)."""
+
+    _fields_ = [("nrows", I64), ("ncols", I64), ("nnz", I64), ("field", I32), ("symmetric", I32),
+                ("body_offset", I64), ("body_line", I64)]
 
 
 class WkMatrix(ctypes.Structure):
@@ -71,6 +81,13 @@ _SIGS = {
     "wk_csr_plan_chunks": (I64, [I64]),
     "wk_csr_plan_bytes": (I64, [I64]),
     "wk_csr_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
+    "wk_csr_merge_plan_bytes": (I64, [I64, I64]),
+    "wk_csr_merge_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
+    "wk_csr_load_balance_plan_bytes": (I64, [I64]),
+    "wk_csr_load_balance_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
+    "wk_mm_read_header": (ctypes.c_int, [P, I64, P]),
+    "wk_mm_parse_entries": (ctypes.c_int, [P, I64, P, I32, P, P, P, I64, P]),
+    "wk_mm_write": (ctypes.c_int, [I64, I64, I64, P, P, P, P, I64, P]),
     "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),
     "wk_spmv_hybrid_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P]),
     "wk_spmv": (ctypes.c_int, [P, P, P, P]),
@@ -188,6 +205,10 @@ def check(rc: int, what: str = ""):
         raise InvalidSliceSize(msg)
     if rc == WK_ERR_INVALID:
         raise ValueError(msg)
+    if rc == WK_ERR_PARSE:
+        raise ParseError(msg)
+    if rc == WK_ERR_UNSUPPORTED:
+        raise UnsupportedFormat(msg)
     raise DeviceError(rc, msg)
 
 

@@ -14,7 +14,7 @@ from typing import Mapping
 WARP_SIZE = 32
 MAX_TUNING_VALUE = 1024
 REQUIRED_TUNING_KEYS = ("block_size", "subwarps_per_block", "csr_subwarp_size")
-CSR_STRATEGIES = ("auto", "stream", "rowblock", "subwarp")
+CSR_STRATEGIES = ("auto", "stream", "rowblock", "subwarp", "merge", "load_balance")
 HYBRID_STRATEGIES = ("minimal_storage", "imbalance_limit")
 
 

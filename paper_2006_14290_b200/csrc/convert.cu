@@ -86,19 +86,24 @@ sellp_fill_kernel(int64_t nrows, int log2ss, const int* __restrict__ ptrs, const
     scatter_block(nrows, s * ss, ss, w, sets[s] * ss, ss, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
 }
 
+// `rpb` rows per block (a power of two <= kConvThreads chosen so that the
+// block's CSR range fits the shared-memory stage: width 27 -> 64 rows, 1728
+// entries), i.e. coalesced staged reads and 512-byte contiguous value stores.
 __global__ void __launch_bounds__(kConvThreads)
-ell_fill_kernel(int64_t nrows, int64_t width, int64_t stride, const int* __restrict__ ptrs,
+ell_fill_kernel(int64_t nrows, int64_t width, int64_t stride, int64_t rpb, const int* __restrict__ ptrs,
                 const int* __restrict__ col, const double* __restrict__ val, int* __restrict__ dcol,
                 double* __restrict__ dval, int* __restrict__ dlen) {
     __shared__ int s_col[kStageCap];
     __shared__ double s_val[kStageCap];
     __shared__ int s_ptr[kConvThreads * 4 + 1];
-    const int64_t r0 = int64_t(blockIdx.x) * kConvThreads;
-    const int64_t nslots = (r0 + kConvThreads <= stride) ? kConvThreads : stride - r0;
-    const int64_t r = r0 + threadIdx.x;
-    if (r < nrows) {
-        const int len = ptrs[r + 1] - ptrs[r];
-        dlen[r] = len < width ? len : int(width);
+    const int64_t r0 = int64_t(blockIdx.x) * rpb;
+    const int64_t nslots = (r0 + rpb <= stride) ? rpb : stride - r0;
+    if (threadIdx.x < rpb) {
+        const int64_t r = r0 + threadIdx.x;
+        if (r < nrows) {
+            const int len = ptrs[r + 1] - ptrs[r];
+            dlen[r] = len < width ? len : int(width);
+        }
     }
     scatter_block(nrows, r0, nslots, width, r0, stride, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
 }
@@ -256,8 +261,10 @@ int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32
     WK_REQUIRE(stride >= nrows, WK_ERR_INVALID, "ELL stride %lld < nrows %lld", (long long)stride,
                (long long)nrows);
     if (stride == 0) return 0;
-    ell_fill_kernel<<<(unsigned)ceil_div(stride, kConvThreads), kConvThreads, 0, as_stream(stream)>>>(
-        nrows, width, stride, row_ptrs, col_idx, values, e_col, e_val, e_row_lengths);
+    int64_t rpb = kConvThreads;
+    while (rpb > 32 && rpb * width > kStageCap) rpb >>= 1;
+    ell_fill_kernel<<<(unsigned)ceil_div(stride, rpb), kConvThreads, 0, as_stream(stream)>>>(
+        nrows, width, stride, rpb, row_ptrs, col_idx, values, e_col, e_val, e_row_lengths);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -248,6 +248,110 @@ static int gmres_multidot_k(int64_t n, int k, const double* V, int64_t ld, const
         ws, &s->cycle_done, st);
 }
 
+// Vectorised classical Gram-Schmidt kernels: double2 loads of w and of the
+// k <= K basis vectors (all issued before any use: k+1 independent 16-byte
+// loads in flight per thread), one pass over the basis per kernel. Same
+// per-element arithmetic as the scalar lambdas (kept for unaligned operands).
+constexpr int kCgsGroup = 8;  // basis vectors loaded together (16-byte loads in flight per thread)
+
+static int cgs_grid(int64_t n, int K) {
+    int64_t g = ceil_div(ceil_div(n, 2), 256);
+    const int64_t cap = int64_t(sm_count()) * (K > 8 ? 2 : 4);
+    if (g > cap) g = cap;
+    if (g > kRedMaxBlocks) g = kRedMaxBlocks;
+    return int(g < 1 ? 1 : g);
+}
+
+static bool cgs_vec_ok(const double* V, int64_t ld, const double* w) {
+    return ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(w)) & 15) == 0 && (ld & 1) == 0;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+gmres_multidot_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, const double* __restrict__ w,
+                   double* __restrict__ Hj, const int* __restrict__ skip, RedWorkspace ws) {
+    if (*skip) return;
+    double acc[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = 0.0;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < np; i += T) {
+        const double2 wv = reinterpret_cast<const double2*>(w)[i];
+#pragma unroll
+        for (int g = 0; g < K; g += kCgsGroup) {
+            double2 v[kCgsGroup];
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) v[u] = __ldcs(reinterpret_cast<const double2*>(V + int64_t(g + u) * ld) + i);
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) {
+                    acc[g + u] += __dmul_rn(v[u].x, wv.x);
+                    acc[g + u] += __dmul_rn(v[u].y, wv.y);
+                }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (q < k) acc[q] += __dmul_rn(V[int64_t(q) * ld + n - 1], w[n - 1]);
+    }
+    double tot[K];
+    if (grid_reduce_last_n<K>(acc, ws, tot) && threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (q < k) Hj[q] = tot[q];
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256)
+gmres_orth_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, double* __restrict__ w,
+               const double* __restrict__ Hj, GS* s, RedWorkspace ws) {
+    if (s->cycle_done) return;
+    double h[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) h[q] = q < k ? Hj[q] : 0.0;
+    double acc = 0.0;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < np; i += T) {
+        double2 wv = reinterpret_cast<const double2*>(w)[i];
+#pragma unroll
+        for (int g = 0; g < K; g += kCgsGroup) {
+            double2 v[kCgsGroup];
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) v[u] = __ldcs(reinterpret_cast<const double2*>(V + int64_t(g + u) * ld) + i);
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) {
+                    wv.x = __dadd_rn(wv.x, -__dmul_rn(h[g + u], v[u].x));
+                    wv.y = __dadd_rn(wv.y, -__dmul_rn(h[g + u], v[u].y));
+                }
+        }
+        reinterpret_cast<double2*>(w)[i] = wv;
+        acc += __dmul_rn(wv.x, wv.x);
+        acc += __dmul_rn(wv.y, wv.y);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        double wi = w[n - 1];
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (q < k) wi = __dadd_rn(wi, -__dmul_rn(h[q], V[int64_t(q) * ld + n - 1]));
+        w[n - 1] = wi;
+        acc += __dmul_rn(wi, wi);
+    }
+    double total;
+    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0) s->sq = total;
+}
+
+#define WK_CGS_LAUNCH(KERN, KK, ...)                                                         \
+    do {                                                                                   \
+        KERN<KK><<<cgs_grid(n, KK), 256, 0, st>>>(__VA_ARGS__);                            \
+        WK_LAUNCH_CHECK();                                                                 \
+        return 0;                                                                          \
+    } while (0)
+
 static int gmres_multidot(int64_t n, int j, const double* V, int64_t ld, const double* w, double* Hj, GS* s, void* ws,
                           cudaStream_t st) {
     const int k = j + 1;
@@ -257,6 +361,15 @@ static int gmres_multidot(int64_t n, int j, const double* V, int64_t ld, const d
             if (!s->cycle_done)
                 for (int q = 0; q < k; ++q) Hj[q] = 0.0;
         }, st);
+    if (cgs_vec_ok(V, ld, w)) {
+        const RedWorkspace rw = red_ws(ws);
+        const int* skip = &s->cycle_done;
+        if (k <= 2) WK_CGS_LAUNCH(gmres_multidot_vec, 2, n, k, V, ld, w, Hj, skip, rw);
+        if (k <= 4) WK_CGS_LAUNCH(gmres_multidot_vec, 4, n, k, V, ld, w, Hj, skip, rw);
+        if (k <= 8) WK_CGS_LAUNCH(gmres_multidot_vec, 8, n, k, V, ld, w, Hj, skip, rw);
+        if (k <= 16) WK_CGS_LAUNCH(gmres_multidot_vec, 16, n, k, V, ld, w, Hj, skip, rw);
+        WK_CGS_LAUNCH(gmres_multidot_vec, kRedMaxVec, n, k, V, ld, w, Hj, skip, rw);
+    }
     if (k <= 8) return gmres_multidot_k<8>(n, k, V, ld, w, Hj, s, ws, st);
     if (k <= 16) return gmres_multidot_k<16>(n, k, V, ld, w, Hj, s, ws, st);
     return gmres_multidot_k<kRedMaxVec>(n, k, V, ld, w, Hj, s, ws, st);
@@ -268,6 +381,15 @@ static int gmres_orth(int64_t n, int j, const double* V, int64_t ld, double* w, 
         return launch_scalar([=] __device__() {
             if (!s->cycle_done) s->sq = 0.0;
         }, st);
+    const int k = j + 1;
+    if (cgs_vec_ok(V, ld, w) && k <= kRedMaxVec) {
+        const RedWorkspace rw = red_ws(ws);
+        if (k <= 2) WK_CGS_LAUNCH(gmres_orth_vec, 2, n, k, V, ld, w, Hj, s, rw);
+        if (k <= 4) WK_CGS_LAUNCH(gmres_orth_vec, 4, n, k, V, ld, w, Hj, s, rw);
+        if (k <= 8) WK_CGS_LAUNCH(gmres_orth_vec, 8, n, k, V, ld, w, Hj, s, rw);
+        if (k <= 16) WK_CGS_LAUNCH(gmres_orth_vec, 16, n, k, V, ld, w, Hj, s, rw);
+        WK_CGS_LAUNCH(gmres_orth_vec, kRedMaxVec, n, k, V, ld, w, Hj, s, rw);
+    }
     return launch_map_reduce(
         n,
         [=] __device__(int64_t i) {

@@ -26,10 +26,12 @@ struct SellpTmaCfg {
 };
 
 // Consume one landed chunk: nj <= J columns for this lane's two rows.
-template <int J, bool kLen>
+// kGuard (ELL's last, partial 64-row block): rows past nrows hold stale
+// shared memory and must not gather.
+template <int J, bool kLen, bool kGuard = false>
 __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const int* __restrict__ c, int nj,
                                             int j0, int len0, int len1, const double* __restrict__ x, double& a0,
-                                            double& a1) {
+                                            double& a1, bool ok0 = true, bool ok1 = true) {
     double2 vv[J];
     double x0[J], x1[J];
 #pragma unroll
@@ -37,8 +39,8 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
         if (jj < nj) {
             vv[jj] = *reinterpret_cast<const double2*>(v + jj * 64);
             const int2 cc = *reinterpret_cast<const int2*>(c + jj * 64);
-            x0[jj] = ld_x(x, cc.x);
-            x1[jj] = ld_x(x, cc.y);
+            x0[jj] = (!kGuard || ok0) ? ld_x(x, cc.x) : 0.0;
+            x1[jj] = (!kGuard || ok1) ? ld_x(x, cc.y) : 0.0;
         }
     }
 #pragma unroll
@@ -52,12 +54,14 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
 
 // kDot: also accumulate sum_r x[r] * y[r] over the owned rows (CG's p.Ap with
 // x = p, y = q) and publish it through DotEpilogue (last-arriving CTA).
-template <class Cfg, bool kDot = false>
+// kEll: ELL(width, stride) — one "slice" per 64-row block, column j of block
+// b at j*stride + 64b (stride % 4 == 0): J bulk copies per chunk instead of 2.
+template <class Cfg, bool kDot = false, bool kEll = false>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
 sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
                    const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
                    const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip,
-                   DotEpilogue dot) {
+                   DotEpilogue dot, int64_t ell_width = 0, int64_t ell_stride = 0) {
     constexpr int J = Cfg::kJ, S = Cfg::kS, WARPS = Cfg::kWarps, CH = Cfg::kChunk;
     if (skip != nullptr && *skip) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -82,6 +86,17 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     auto seek = [&]() {
         pvalid = false;
         while (ps < nslices) {
+            if (kEll) {
+                pw = int(ell_width);
+                if (pj < pw) {
+                    pbase = ps * 64;
+                    pvalid = true;
+                    return;
+                }
+                ps += nwarps;
+                pj = 0;
+                continue;
+            }
             const int64_t s0 = __ldg(sets + ps);
             pw = int(__ldg(sets + ps + 1) - s0);
             if (pj < pw) {
@@ -96,11 +111,22 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     auto issue = [&](int st) {
         if (lane == 0) {
             const int nj = (pw - pj < J) ? pw - pj : J;
-            const uint32_t bv = uint32_t(nj) * 64 * sizeof(double), bc = uint32_t(nj) * 64 * sizeof(int);
-            mbar_arrive_expect_tx(bars + st, bv + bc);
-            const int64_t off = pbase + int64_t(pj) * 64;
-            bulk_g2s_evict_first(sval + st * CH, val + off, bv, bars + st, pol);
-            bulk_g2s_evict_first(scol + st * CH, col + off, bc, bars + st, pol);
+            if (kEll) {
+                const int64_t cnt = (ell_stride - pbase < 64) ? ell_stride - pbase : 64;
+                const uint32_t bv = uint32_t(cnt) * sizeof(double), bc = uint32_t(cnt) * sizeof(int);
+                mbar_arrive_expect_tx(bars + st, uint32_t(nj) * (bv + bc));
+                for (int jj = 0; jj < nj; ++jj) {
+                    const int64_t off = int64_t(pj + jj) * ell_stride + pbase;
+                    bulk_g2s_evict_first(sval + st * CH + jj * 64, val + off, bv, bars + st, pol);
+                    bulk_g2s_evict_first(scol + st * CH + jj * 64, col + off, bc, bars + st, pol);
+                }
+            } else {
+                const uint32_t bv = uint32_t(nj) * 64 * sizeof(double), bc = uint32_t(nj) * 64 * sizeof(int);
+                mbar_arrive_expect_tx(bars + st, bv + bc);
+                const int64_t off = pbase + int64_t(pj) * 64;
+                bulk_g2s_evict_first(sval + st * CH, val + off, bv, bars + st, pol);
+                bulk_g2s_evict_first(scol + st * CH, col + off, bc, bars + st, pol);
+            }
         }
         pj += J;
         seek();
@@ -111,9 +137,9 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     uint32_t i = 0;  // chunks consumed by this warp
     double dacc = 0.0;
     for (int64_t s = gwarp; s < nslices; s += nwarps) {
-        const int64_t s0 = __ldg(sets + s);
-        const int w = int(__ldg(sets + s + 1) - s0);
+        const int w = kEll ? int(ell_width) : int(__ldg(sets + s + 1) - __ldg(sets + s));
         const int64_t r0 = s * 64 + 2 * lane;
+        const bool partial = kEll && (s + 1) * 64 > nrows;
         int len0 = w, len1 = w;
         if (!finite0) {
             len0 = r0 < nrows ? row_lengths[r0] : 0;
@@ -126,7 +152,9 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             const int nj = (w - j0 < J) ? w - j0 : J;
             const double* v = sval + st * CH + 2 * lane;
             const int* c = scol + st * CH + 2 * lane;
-            if (finite0)
+            if (kEll && partial)
+                sellp_chunk<J, true, true>(v, c, nj, j0, len0, len1, x, a0, a1, r0 < nrows, r0 + 1 < nrows);
+            else if (finite0)
                 sellp_chunk<J, false>(v, c, nj, j0, len0, len1, x, a0, a1);
             else
                 sellp_chunk<J, true>(v, c, nj, j0, len0, len1, x, a0, a1);
@@ -159,25 +187,27 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     }
 }
 
-// Launch one configuration (persistent grid: one CTA per SM).
-template <class Cfg, bool kDot = false>
+// Launch one configuration (persistent grid: one CTA per SM). kEll: sets is
+// unused, the operand is ELL(ell_width, ell_stride).
+template <class Cfg, bool kDot = false, bool kEll = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
-                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0}) {
+                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0}, int64_t ell_width = 0,
+                       int64_t ell_stride = 0) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(Cfg::kSmem)));
+        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot, kEll>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
     const int64_t nslices = ceil_div(nrows, 64);
     int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
     const int64_t need = ceil_div(nslices, Cfg::kWarps);
     if (grid > need) grid = need;
-    sellp64_tma_kernel<Cfg, kDot><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
-        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot);
+    sellp64_tma_kernel<Cfg, kDot, kEll><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
+        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, ell_width, ell_stride);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -17,6 +17,8 @@
 // x != 0, +0 + -0 == +0) as long as x[0] is finite; if it is not, the
 // kernels switch to the `row_lengths`-bounded loop of the oracle.
 #include "common.cuh"
+#include "csr_merge.cuh"
+#include "segwarp.cuh"
 #include "csr_tma.cuh"
 #include "sellp_tma.cuh"
 
@@ -164,6 +166,27 @@ static int csr_kernel_choice() {
     return g_csr_choice;
 }
 
+// COO kernel selection (env WK_COO_KERNEL or wk_config_set("coo_kernel", i)):
+// 0 = warp-range kernel without load pipelining, 1 = the pipelined warp-range
+// kernel (segwarp.cuh seg_warp_kernel), 2 = persistent TMA tile kernel with
+// block-wide scans (csr_merge.cuh coo_tile_kernel), 3 (default) = 8 entries
+// per lane, one warp scan per 256 entries (segwarp.cuh seg8_kernel).
+static int g_coo_choice = -1;
+
+int set_coo_kernel(int choice) {
+    WK_REQUIRE(choice >= 0 && choice <= 3, WK_ERR_INVALID, "coo kernel choice must be in [0, 3]");
+    g_coo_choice = choice;
+    return 0;
+}
+
+static int coo_kernel_choice() {
+    if (g_coo_choice < 0) {
+        const char* e = getenv("WK_COO_KERNEL");
+        g_coo_choice = (e != nullptr) ? atoi(e) : 3;
+    }
+    return g_coo_choice;
+}
+
 static int log2i(int64_t v) {
     int l = 0;
     while ((int64_t(1) << l) < v) ++l;
@@ -225,6 +248,14 @@ int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
                const double* val, const int* row_lengths, const double* x, double* y, const int* skip,
                cudaStream_t st) {
     if (nrows == 0) return 0;
+    // TMA pipeline (the SELL-P(64) kernel with ELL addressing) unless the
+    // register-only kernel is selected (sellp_kernel 0) or the layout cannot
+    // be bulk-copied (16-byte aligned columns need stride % 4 == 0)
+    if (sellp_kernel_choice() != 0 && stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) &&
+        aligned(y, 16) && width > 0)
+        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, false, true>(
+            nrows, ncols, nullptr, col, val, row_lengths, x, y, skip, st, DotEpilogue{nullptr, nullptr, nullptr, 0},
+            width, stride);
     const bool vec = (stride % 2 == 0) && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {
         const int64_t threads = ceil_div(nrows, 2);
@@ -390,11 +421,45 @@ csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __res
     }
 }
 
+__global__ void zero_masked_kernel(double* __restrict__ y, int64_t n, const int* __restrict__ skip) {
+    if (*skip) return;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) y[i] = 0.0;
+}
+
+static int launch_zero_masked(double* y, int64_t n, const int* skip, cudaStream_t st) {
+    if (n == 0) return 0;
+    int64_t blocks = ceil_div(n, 256);
+    if (blocks > int64_t(sm_count()) * 8) blocks = int64_t(sm_count()) * 8;
+    zero_masked_kernel<<<(unsigned)blocks, 256, 0, st>>>(y, n, skip);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
 int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const int* col, const double* val,
                const double* x, double* y, int strategy, int subwarp, const int* first, double* partials,
-               unsigned* tickets, const int* skip, cudaStream_t st) {
+               unsigned* tickets, const int* skip, cudaStream_t st, void* merge_plan = nullptr) {
     (void)ncols;
     if (nrows == 0) return 0;
+    if (strategy == WK_CSR_MERGE) {
+        WK_REQUIRE(merge_plan != nullptr, WK_ERR_INVALID, "csr merge strategy needs a plan (wk_csr_merge_plan_build)");
+        return launch_csr_merge(nrows, nnz, ptrs, col, val, x, y, merge_plan, skip, st);
+    }
+    if (strategy == WK_CSR_LOAD_BALANCE) {
+        WK_REQUIRE(merge_plan != nullptr, WK_ERR_INVALID,
+                   "csr load_balance strategy needs a plan (wk_csr_load_balance_plan_build)");
+        // skip-aware zero fill: the boundary rows are added atomically
+        if (skip == nullptr) {
+            WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
+        } else {
+            WK_TRY(launch_zero_masked(y, nrows, skip, st));
+        }
+        if (nnz == 0) return 0;
+        WK_REQUIRE(aligned(col, 16) && aligned(val, 16), WK_ERR_INVALID,
+                   "csr load_balance needs 16-byte aligned col_idx / values");
+        return launch_seg8(true, nnz, nrows, 0, ptrs, reinterpret_cast<const int*>(merge_plan), col, val, x, y, skip,
+                           st);
+    }
     if (strategy == WK_CSR_ROWBLOCK) {
         // 32*k-row blocks; the stage capacity is the smallest that keeps a
         // 32-row block of mean-length rows "light" (more warps per SM when
@@ -542,6 +607,12 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const
         WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
     }
     if (nnz == 0) return 0;
+    const int cc = coo_kernel_choice();
+    if (cc == 3 && aligned(row, 16) && aligned(col, 16) && aligned(val, 16))
+        return launch_seg8(false, nnz, nrows, accumulate, row, nullptr, col, val, x, y, skip, st);
+    if (cc == 1 || cc == 3)
+        return launch_seg_warp(false, nnz, nrows, accumulate, row, nullptr, col, val, x, y, skip, st);
+    if (coo_kernel_choice() == 2) return launch_coo_tile(nnz, accumulate, row, col, val, x, y, skip, st);
     const int64_t warps = ceil_div(nnz, kCooPerWarp);
     const int64_t blocks = ceil_div(warps * 32, kSpmvThreads);
     coo_kernel<<<(unsigned)blocks, kSpmvThreads, 0, st>>>(nnz, accumulate, row, col, val, x, y, skip);
@@ -597,6 +668,27 @@ int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void*
     return 0;
 }
 
+int64_t wk_csr_merge_plan_bytes(int64_t nrows, int64_t nnz) { return csr_merge_plan_bytes(nrows, nnz); }
+
+int64_t wk_csr_load_balance_plan_bytes(int64_t nnz) { return seg8_plan_bytes(nnz); }
+
+int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
+                                   wk_stream_t stream) {
+    clear_error();
+    const int64_t nw = seg8_warps(nnz);
+    seg8_plan_kernel<<<(unsigned)ceil_div(nw + 1, 256), 256, 0, as_stream(stream)>>>(
+        nrows, nnz, nw, row_ptrs, reinterpret_cast<int*>(plan));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_csr_merge_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream) {
+    clear_error();
+    cudaStream_t st = as_stream(stream);
+    WK_CUDA(cudaMemsetAsync(plan, 0, size_t(csr_merge_plan_bytes(nrows, nnz)), st));
+    return build_csr_merge_plan(nrows, nnz, row_ptrs, plan, st);
+}
+
 static void csr_plan_views(void* plan, int64_t nnz, int** first, double** partials, unsigned** tickets) {
     const int64_t c = csr_stream_chunks(nnz);
     char* p = reinterpret_cast<char*>(plan);
@@ -614,9 +706,9 @@ int wk_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* ro
     int* first = nullptr;
     double* partials = nullptr;
     unsigned* tickets = nullptr;
-    if (plan != nullptr) csr_plan_views(plan, nnz, &first, &partials, &tickets);
+    if (plan != nullptr && strategy == WK_CSR_STREAM) csr_plan_views(plan, nnz, &first, &partials, &tickets);
     return launch_csr(nrows, ncols, nnz, row_ptrs, col_idx, values, x, y, strategy, subwarp_size, first, partials,
-                      tickets, nullptr, as_stream(stream));
+                      tickets, nullptr, as_stream(stream), (strategy == WK_CSR_MERGE || strategy == WK_CSR_LOAD_BALANCE) ? plan : nullptr);
 }
 
 int wk_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_idx, const int32_t* col_idx,
@@ -649,9 +741,11 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
             int* first = nullptr;
             double* partials = nullptr;
             unsigned* tickets = nullptr;
-            if (A->plan != nullptr) csr_plan_views(A->plan, A->nnz, &first, &partials, &tickets);
+            if (A->plan != nullptr && A->csr_strategy == WK_CSR_STREAM)
+                csr_plan_views(A->plan, A->nnz, &first, &partials, &tickets);
             return launch_csr(A->nrows, A->ncols, A->nnz, A->row_ptrs, A->col_idx, A->values, x, y,
-                              A->csr_strategy, A->subwarp_size, first, partials, tickets, skip, st);
+                              A->csr_strategy, A->subwarp_size, first, partials, tickets, skip, st,
+                              (A->csr_strategy == WK_CSR_MERGE || A->csr_strategy == WK_CSR_LOAD_BALANCE) ? A->plan : nullptr);
         }
         case WK_FMT_COO:
             WK_REQUIRE(skip == nullptr, WK_ERR_INVALID, "masked COO SpMV is not supported");
@@ -667,11 +761,8 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
                                 y, skip, st);
             if (rc) return rc;
             if (A->coo_nnz == 0) return 0;
-            const int64_t warps = ceil_div(A->coo_nnz, kCooPerWarp);
-            coo_kernel<<<(unsigned)ceil_div(warps * 32, kSpmvThreads), kSpmvThreads, 0, st>>>(
-                A->coo_nnz, 1, A->coo_row, A->coo_col, A->coo_val, x, y, skip);
-            WK_LAUNCH_CHECK();
-            return 0;
+            return launch_coo(A->nrows, A->coo_nnz, A->coo_row, A->coo_col, A->coo_val, x, y, /*accumulate=*/1,
+                              skip, st);
         }
         default:
             WK_REQUIRE(false, WK_ERR_INVALID, "unknown matrix format %d", A->format);

@@ -136,22 +136,44 @@ class DeviceCsr(DeviceMatrix):
                       stream_handle(self.device))
         return self._plan
 
+    def merge_plan(self):
+        """merge-path tile coordinates + per-tile carry slots (built once)."""
+        if getattr(self, "_merge_plan", None) is None:
+            L = _lib.load()
+            nb = int(L.wk_csr_merge_plan_bytes(self.nrows, self.nnz))
+            self._merge_plan = torch.empty(nb, dtype=torch.uint8, device=self.device)
+            _lib.call("wk_csr_merge_plan_build", self.nrows, self.nnz, _ptr(self.row_ptrs), _ptr(self._merge_plan),
+                      stream_handle(self.device))
+        return self._merge_plan
+
+    def load_balance_plan(self):
+        """row containing the first entry of every 1024-entry warp range (built once)."""
+        if getattr(self, "_lb_plan", None) is None:
+            L = _lib.load()
+            self._lb_plan = torch.empty(int(L.wk_csr_load_balance_plan_bytes(self.nnz)), dtype=torch.uint8,
+                                        device=self.device)
+            _lib.call("wk_csr_load_balance_plan_build", self.nrows, self.nnz, _ptr(self.row_ptrs),
+                      _ptr(self._lb_plan), stream_handle(self.device))
+        return self._lb_plan
+
     def auto_strategy(self):
         """rowblock when every row is short and the mean is moderate (one lane
-        folds one row from a TMA-staged block), stream otherwise (nnz-balanced
-        for skewed row lengths). Decided once per matrix (one D2H read)."""
+        folds one row from a TMA-staged block; bitwise), merge otherwise
+        (merge-path tiles: equal work per CTA for skewed row lengths).
+        Decided once per matrix (one D2H read)."""
         if getattr(self, "_auto", None) is None:
             if self.nrows == 0:
-                self._auto = "stream"
+                self._auto = "merge"
             else:
                 maxlen = max_row_length(self)
-                self._auto = "rowblock" if maxlen <= 64 and self.nnz <= 28 * self.nrows else "stream"
+                self._auto = "rowblock" if maxlen <= 64 and self.nnz <= 28 * self.nrows else "merge"
         return self._auto
 
     def with_strategy(self, strategy, subwarp=0):
         if strategy == "auto":
             strategy = self.auto_strategy()
-        st = {"stream": _lib.WK_CSR_STREAM, "subwarp": _lib.WK_CSR_SUBWARP, "rowblock": _lib.WK_CSR_ROWBLOCK}[strategy]
+        st = {"stream": _lib.WK_CSR_STREAM, "subwarp": _lib.WK_CSR_SUBWARP, "rowblock": _lib.WK_CSR_ROWBLOCK,
+              "merge": _lib.WK_CSR_MERGE, "load_balance": _lib.WK_CSR_LOAD_BALANCE}[strategy]
         if st != self.strategy or subwarp != self.subwarp:
             self.strategy, self.subwarp = st, int(subwarp)
             self._wk = None
@@ -166,6 +188,10 @@ class DeviceCsr(DeviceMatrix):
         m.row_ptrs, m.col_idx, m.values = _ptr(self.row_ptrs), _ptr(self.col_idx), _ptr(self.values)
         if self.strategy == _lib.WK_CSR_STREAM:
             m.plan = _ptr(self.plan())
+        elif self.strategy == _lib.WK_CSR_MERGE:
+            m.plan = _ptr(self.merge_plan())
+        elif self.strategy == _lib.WK_CSR_LOAD_BALANCE:
+            m.plan = _ptr(self.load_balance_plan())
         return m
 
     def row_lengths(self):

@@ -12,6 +12,7 @@ The GPU box has no /root/reference, so the committed `.npz` files are what
 the oracle and the CUDA path are pinned against there.
 """
 
+import io
 import json
 import os
 import sys
@@ -144,9 +145,116 @@ def write_cg():
     return names
 
 
+def mm_texts():
+    """MatrixMarket inputs: the reference's own test texts (test_sparse.py:149-266)
+    plus whitespace / line-ending / literal / symmetry / size edge cases."""
+    rng = np.random.default_rng(99)
+    H = "%%MatrixMarket matrix coordinate"
+    t = {}
+    t["diag"] = "\n".join([H + " real general", "3 3 3", "1 1 1.0", "2 2 2.0", "3 3 3.0"])
+    t["symmetric"] = "\n".join([H + " real symmetric", "3 3 3", "1 1 2.0", "2 1 5.0", "3 3 1.0"])
+    t["pattern"] = "\n".join([H + " pattern general", "2 2 2", "1 1", "2 2"])
+    t["integer"] = "\n".join([H + " integer general", "2 2 1", "2 1 7"])
+    t["duplicates"] = "\n".join([H + " real general", "2 2 2", "1 1 1.5", "1 1 2.5"])
+    t["comments_blank"] = "\n".join([H + " real general", "% a comment", "", "2 2 1", "% another", "1 2 3.0"])
+    t["crlf_tabs"] = "\r\n".join([H + " real general", "  3\t3  2 ", "\t1 3\t-4.25  ", "3 1 1e-3", ""])
+    t["upper_banner"] = "\n".join(["%%MATRIXMARKET Matrix Coordinate REAL General", "2 3 2", "1 3 2.0", "2 1 -1.0"])
+    t["literals"] = "\n".join([H + " real general", "4 4 10", "1 1 +1.5", "1 2 1E5", "1 3 .5", "1 4 5.",
+                                "2 1 -0.0", "2 2 4.9e-324", "2 3 1.7976931348623157e308", "2 4 inf",
+                                "3 3 -Infinity", "4 4 0.1000000000000000055511151231257827"])
+    t["int_literals"] = "\n".join([H + " integer general", "3 3 3", "+1 1 +7", "002 3 -0", "3 002 12345678901"])
+    t["empty_matrix"] = H + " real general\n0 0 0\n"
+    t["no_final_newline"] = H + " real general\n1 1 1\n1 1 2.5"
+    t["cr_only"] = "\r".join([H + " pattern symmetric", "3 3 3", "2 1", "3 3", "3 2"])
+    t["sym_diag_dups"] = "\n".join([H + " real symmetric", "3 3 5", "1 1 1.0", "2 1 2.0", "2 1 3.0", "1 1 4.0",
+                                     "3 2 0.5"])
+    # random general matrix with duplicates, values in repr form
+    n, m, k = 300, 200, 3000
+    r = rng.integers(1, n + 1, k)
+    c = rng.integers(1, m + 1, k)
+    v = rng.standard_normal(k) * 10.0 ** rng.integers(-30, 30, k)
+    t["random_general"] = H + " real general\n% generated\n" + f"{n} {m} {k}\n" + "".join(
+        f"{a} {b} {repr(float(x))}\n" for a, b, x in zip(r, c, v))
+    r2 = rng.integers(1, 121, 900)
+    c2 = np.minimum(r2, rng.integers(1, 121, 900))
+    t["random_symmetric"] = H + " real symmetric\n" + "120 120 900\n" + "".join(
+        f"{a} {b} {x!r}\n" for a, b, x in zip(r2, c2, rng.random(900).tolist()))
+    errors = {
+        "err_complex": H + " complex general\n1 1 1\n1 1 1.0 2.0",
+        "err_array": "%%MatrixMarket matrix array real general\n2 2\n1.0\n2.0\n3.0\n4.0",
+        "err_skew": H + " real skew-symmetric\n2 2 1\n2 1 1.0",
+        "err_hermitian": H + " real hermitian\n2 2 1\n2 1 1.0",
+        "err_banner": "%%NotMatrixMarket whatever\n1 1 1\n1 1 1.0",
+        "err_banner_short": "%%MatrixMarket matrix coordinate real\n1 1 1\n1 1 1.0",
+        "err_count_low": H + " real general\n2 2 2\n1 1 1.0",
+        "err_count_high": H + " real general\n2 2 1\n1 1 1.0\n2 2 1.0",
+        "err_fields": H + " real general\n2 2 1\n1 x 1.0",
+        "err_fields_count": H + " real general\n2 2 1\n1 1",
+        "err_pattern_extra": H + " pattern general\n2 2 1\n1 1 1.0",
+        "err_bounds": H + " real general\n3 3 1\n4 1 1.0",
+        "err_zero_index": H + " real general\n3 3 1\n0 1 1.0",
+        "err_size_fields": H + " real general\n3 3\n1 1 1.0",
+        "err_negative": H + " real general\n-3 3 0",
+        "err_missing_size": H + " real general\n% only a comment\n",
+        "err_empty": "",
+        "err_float_index": H + " real general\n3 3 1\n1.0 1 1.0",
+        "err_bad_value": H + " real general\n3 3 1\n1 1 abc",
+        "err_hex_value": H + " real general\n3 3 1\n1 1 0x1p3",
+    }
+    t.update(errors)
+    return t
+
+
+def write_mm():
+    """Record the reference reader's results (or error type) for every text,
+    and the reference writer's output for a few matrices."""
+    from warpkit.errors import ParseError, UnsupportedFormat
+    from warpkit.sparse import read_matrix_market, write_matrix_market
+
+    texts = mm_texts()
+    cases = {}
+    arrays = {}
+    for name, text in texts.items():
+        try:
+            m = read_matrix_market(text if text else io.BytesIO(b""))
+        except (ParseError, UnsupportedFormat) as exc:
+            cases[name] = {"text": text, "error": type(exc).__name__}
+            continue
+        cases[name] = {"text": text, "shape": [m.nrows, m.ncols]}
+        arrays[name + "__row_idx"] = np.asarray(m.row_idx, dtype=np.int64)
+        arrays[name + "__col_idx"] = np.asarray(m.col_idx, dtype=np.int64)
+        arrays[name + "__values"] = np.asarray(m.values, dtype=np.float64)
+    # non-ASCII bytes
+    try:
+        read_matrix_market(io.BytesIO(b"%%MatrixMarket matrix coordinate real general\n1 1 1\n1 1 1.0\xff"))
+    except ParseError:
+        cases["err_non_ascii"] = {"text_bytes_hex": (b"%%MatrixMarket matrix coordinate real general\n1 1 1\n"
+                                                     b"1 1 1.0\xff").hex(), "error": "ParseError"}
+    rng = np.random.default_rng(7)
+    writes = {}
+    for name, (n, m_, dens) in {"w_small": (8, 8, 0.5), "w_rect": (23, 31, 0.2)}.items():
+        mm = random_sparse_matrix(n, m_, dens, rng)
+        vals = mm.values * np.logspace(-120, 100, mm.nnz) * np.where(np.arange(mm.nnz) % 2, -1, 1)
+        mm = CooMatrix(mm.nrows, mm.ncols, mm.row_idx, mm.col_idx, vals)
+        writes[name] = write_matrix_market(mm)
+        arrays[name + "__row_idx"] = np.asarray(mm.row_idx, dtype=np.int64)
+        arrays[name + "__col_idx"] = np.asarray(mm.col_idx, dtype=np.int64)
+        arrays[name + "__values"] = np.asarray(mm.values, dtype=np.float64)
+        arrays[name + "__shape"] = np.array([mm.nrows, mm.ncols])
+    with open(os.path.join(HERE, "mm_cases.json"), "w") as fh:
+        json.dump({"generator": "tests/golden/make_golden.py (mm)", "reads": cases, "writes": writes}, fh, indent=1)
+        fh.write("\n")
+    np.savez_compressed(os.path.join(HERE, "mm_cases.npz"), **arrays)
+    print(f"mm: {len(cases)} read cases, {len(writes)} write cases")
+
+
 def main():
+    if "--only-mm" in sys.argv:
+        write_mm()
+        return
     spmv_names = write_spmv()
     cg_names = write_cg()
+    write_mm()
     manifest = {
         "generator": "tests/golden/make_golden.py",
         "reference": "warpkit " + warpkit.__version__ + " from /root/reference/pkg/src",

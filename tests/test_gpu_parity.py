@@ -1,7 +1,7 @@
 """Parity of the CUDA path (through the C ABI) against the CPU oracle and the
 reference's golden vectors. Bars:
-  * SELL-P, ELL, CSR-stream SpMV and every conversion: bitwise;
-  * CSR-subwarp, COO, Hybrid SpMV: max_scaled_rel_err <= 1e-12
+  * SELL-P, ELL, CSR-stream / -rowblock SpMV and every conversion: bitwise;
+  * CSR-subwarp, CSR-merge, COO, Hybrid SpMV: max_scaled_rel_err <= 1e-12
     (integer-valued data: exact);
   * CG: equal iteration count, max |res_k - res_ref_k| / ||b|| <= 1e-10,
     max_scaled_rel_err(x) <= 1e-10.
@@ -67,14 +67,26 @@ CSR_BITWISE_ROW = {"stream": 256, "rowblock": 64}  # rows up to this length fold
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
-@pytest.mark.parametrize("strategy", ["stream", "rowblock", "auto"])
-def test_csr_stream_golden_bitwise(wk, case, strategy):
+@pytest.mark.parametrize("strategy", ["stream", "rowblock", "merge", "load_balance", "auto"])
+def test_csr_golden(wk, case, strategy):
+    """stream / rowblock fold short rows bitwise; merge (merge-path tiles)
+    reassociates rows cut by thread boundaries: 1e-12 scaled, exact on
+    integer data, deterministic. auto resolves to rowblock or merge."""
+    from paper_2006_14290_b200 import device as D
+
     e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
-    y = wk.spmv_csr(_host(wk, case.csr, "csr"), case.x, e)
+    m = _host(wk, case.csr, "csr")
+    y = wk.spmv_csr(m, case.x, e)
     lens = np.diff(case.csr.row_ptrs)
-    short = lens <= min(CSR_BITWISE_ROW.values())
-    assert y[short].tobytes() == case.y[short].tobytes()
     assert sparse_ref.max_scaled_rel_err(y, case.y, lens) <= TOL
+    if _is_int(case):
+        assert np.array_equal(y, case.y)
+    resolved = D.as_device(m, 0).auto_strategy() if strategy == "auto" else strategy
+    if resolved in CSR_BITWISE_ROW:
+        short = lens <= CSR_BITWISE_ROW[resolved]
+        assert y[short].tobytes() == case.y[short].tobytes()
+    elif resolved == "merge":
+        assert wk.spmv_csr(m, case.x, e).tobytes() == y.tobytes()  # deterministic
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -90,13 +102,47 @@ def test_csr_subwarp_golden(wk, case):
             assert sparse_ref.max_scaled_rel_err(y, case.y, nnz) <= TOL, tile
 
 
+COO_KERNELS = (0, 1, 2, 3)  # spmv.cu coo_kernel_choice: warp range, pipelined warp range, TMA tiles, seg8 (default)
+
+
+@pytest.fixture
+def coo_kernel(wk, request):
+    from paper_2006_14290_b200 import _lib
+
+    _lib.call("wk_config_set", b"coo_kernel", request.param)
+    yield request.param
+    _lib.call("wk_config_set", b"coo_kernel", 3)
+
+
+@pytest.mark.parametrize("coo_kernel", COO_KERNELS, indirect=True)
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
-def test_coo_golden(wk, ex, case):
+def test_coo_golden(wk, ex, case, coo_kernel):
     y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, ex)
     if _is_int(case):
         assert np.array_equal(y, case.y)
     else:
         assert sparse_ref.max_scaled_rel_err(y, case.y, sparse_ref.row_nnz(case.csr)) <= TOL
+
+
+@pytest.mark.parametrize("coo_kernel", COO_KERNELS, indirect=True)
+@pytest.mark.parametrize("shape", ["skewed", "many_tiles", "one_row"])
+def test_coo_hybrid_skewed(wk, ex, rng, shape, coo_kernel):
+    """COO and Hybrid (ELL + COO accumulate) on skewed / multi-tile inputs."""
+    ncols = 70000
+    if shape == "one_row":
+        lens = np.array([0, 60000, 0, 3])
+    else:
+        n = 400000 if shape == "many_tiles" else 30000
+        lens = np.minimum((rng.pareto(1.3, size=n) * 5).astype(np.int64), 20000)
+        lens[rng.random(n) < 0.4] = 0
+    ptrs, cols, vals = _banded_case(rng, lens, ncols)
+    csr = wk.CsrMatrix(len(lens), ncols, ptrs, cols, vals)
+    x = rng.standard_normal(ncols)
+    y_ref = sparse_ref.spmv(csr, x)
+    coo = wk.csr_to_coo(csr, ex)
+    assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
+    hyb = wk.csr_to_hybrid(csr, width=3, exec=ex)
+    assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -112,6 +158,28 @@ def test_conversions_golden_bitwise(wk, ex, case):
         assert np.array_equal(got.row_lengths, ref.row_lengths), s
         assert np.array_equal(got.col_idx, ref.col_idx), s
         assert got.values.tobytes() == ref.values.tobytes(), s
+
+
+@pytest.mark.parametrize("nrows,stride", [(1000, 1000), (4096, 4096), (4100, 4100), (130, 132), (999, 1004),
+                                          (1001, 1001), (2000, 2050)])
+def test_ell_strides_bitwise(wk, ex, rng, nrows, stride):
+    """ELL through the TMA pipeline (stride % 4 == 0, partial last 64-row
+    block) and the register kernel (other strides): bitwise vs the oracle,
+    also with non-finite x[0] (padding must then be skipped via row_lengths)."""
+    ncols = 3000
+    lens = rng.integers(0, 30, size=nrows)
+    lens[rng.random(nrows) < 0.1] = 0
+    ptrs = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(ncols, size=int(L), replace=False)) for L in lens])
+    csr = wk.CsrMatrix(nrows, ncols, ptrs, cols, rng.standard_normal(len(cols)))
+    ell = wk.csr_to_ell(csr, stride=stride, exec=ex)
+    ref = sparse_ref.csr_to_ell(csr, stride=stride)
+    assert np.array_equal(ell.col_idx, ref.col_idx) and ell.values.tobytes() == ref.values.tobytes()
+    for x0 in (0.5, np.inf):
+        x = rng.standard_normal(ncols)
+        x[0] = x0
+        y_ref = sparse_ref.spmv(csr, x)
+        assert wk.spmv_ell(ell, x, ex).tobytes() == y_ref.tobytes()
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -204,11 +272,14 @@ def test_long_rows_stream_kernel(wk, ex, rng):
     csr = wk.CsrMatrix(n, ncols, ptrs, cols, vals)
     x = rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
-    y = wk.spmv_csr(csr, x, ex)
+    es = wk.make_executor("b200", device=0, tuning={"csr_strategy": "stream"})
+    y = wk.spmv_csr(csr, x, es)
     short = lens <= CSR_LONG_ROW
     assert y[short].tobytes() == y_ref[short].tobytes()
     assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
-    assert wk.spmv_csr(csr, x, ex).tobytes() == y.tobytes()  # deterministic
+    assert wk.spmv_csr(csr, x, es).tobytes() == y.tobytes()  # deterministic
+    ym = wk.spmv_csr(csr, x, ex)  # auto -> merge
+    assert sparse_ref.max_scaled_rel_err(ym, y_ref, lens) <= TOL
     # forced row-block strategy: heavy blocks (long rows) take the warp-reduction path
     eb = wk.make_executor("b200", device=0, tuning={"csr_strategy": "rowblock"})
     yb = wk.spmv_csr(csr, x, eb)
@@ -218,6 +289,89 @@ def test_long_rows_stream_kernel(wk, ex, rng):
     assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
     hyb = wk.csr_to_hybrid(csr, exec=ex)
     assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
+
+
+def _merge_case(rng, lens, ncols, ints=False):
+    ptrs = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(ncols, size=int(L), replace=False)) for L in lens]) if len(lens) else \
+        np.zeros(0, np.int64)
+    vals = rng.integers(1, 10, size=len(cols)).astype(np.float64) if ints else rng.standard_normal(len(cols))
+    return ptrs, cols.astype(np.int64), vals
+
+
+MERGE_TILE = 2048  # csr_merge.cuh kMgTile: merge items (row ends + nonzeros) per CTA
+
+
+def _banded_case(rng, lens, ncols):
+    """rows of consecutive columns at random offsets (vectorised; big cases)."""
+    ptrs = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    start = rng.integers(0, ncols - lens.max(initial=0) + 1, size=len(lens))
+    rows = np.repeat(np.arange(len(lens)), lens)
+    cols = start[rows] + (np.arange(ptrs[-1]) - ptrs[rows])
+    return ptrs, cols.astype(np.int64), rng.standard_normal(int(ptrs[-1]))
+
+
+@pytest.mark.parametrize("strategy", ["merge", "load_balance"])
+@pytest.mark.parametrize("shape", ["tile_spanning_row", "empty_runs", "tile_aligned", "all_empty", "one_row",
+                                   "skewed", "ints", "many_tiles"])
+def test_csr_balanced_edge_cases(wk, rng, shape, strategy):
+    """merge-path and load-balance CSR: rows spanning many tiles / warp
+    ranges, long runs of empty rows crossing them, rows ending exactly on tile /
+    thread boundaries, empty matrices; tolerance 1e-12, exact on integer data;
+    merge is deterministic."""
+    ncols = 70000
+    if shape == "tile_spanning_row":
+        lens = np.array([3, 50000, 2, 0, 7000, 1] + [5] * 900)
+    elif shape == "empty_runs":
+        lens = np.zeros(20000, np.int64)
+        lens[[5, 6000, 6001, 19999]] = [4000, 3, 2100, 9]
+    elif shape == "tile_aligned":
+        # every row is 2047 entries: row end + entries = one tile exactly; plus 7-item rows (thread boundaries)
+        lens = np.array([MERGE_TILE - 1] * 6 + [7] * 3000)
+    elif shape == "all_empty":
+        lens = np.zeros(5000, np.int64)
+    elif shape == "one_row":
+        lens = np.array([60000])
+    else:
+        lens = np.minimum((rng.pareto(1.2, size=30000) * 3).astype(np.int64), ncols)
+        lens[rng.random(30000) < 0.5] = 0
+    if shape == "many_tiles":
+        # > 2 tiles per CTA of the persistent grid: every pipeline stage is reused
+        lens = np.minimum((rng.pareto(1.5, size=400000) * 6).astype(np.int64), 20000)
+        lens[rng.random(400000) < 0.3] = 0
+        ptrs, cols, vals = _banded_case(rng, lens, ncols)
+    else:
+        ptrs, cols, vals = _merge_case(rng, lens, ncols, ints=(shape == "ints"))
+    if shape == "ints":
+        lens = np.minimum((rng.pareto(1.2, size=20000) * 3).astype(np.int64), 3000)
+        ptrs, cols, vals = _merge_case(rng, lens, ncols, ints=True)
+    csr = wk.CsrMatrix(len(lens), ncols, ptrs, cols, vals)
+    x = rng.integers(-5, 6, size=ncols).astype(np.float64) if shape == "ints" else rng.standard_normal(ncols)
+    y_ref = sparse_ref.spmv(csr, x)
+    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
+    y = wk.spmv_csr(csr, x, e)
+    assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
+    if shape == "ints":
+        assert np.array_equal(y, y_ref)
+    assert np.all(y[lens == 0] == 0.0)
+    if strategy == "merge":
+        assert wk.spmv_csr(csr, x, e).tobytes() == y.tobytes()
+        # rows folded inside one thread's 8 items are the reference fold exactly
+        one = lens <= 1
+        assert y[one].tobytes() == y_ref[one].tobytes()
+    # masked SpMV through the solver entry point: skip flag set -> y untouched
+    from paper_2006_14290_b200 import device as D
+    from paper_2006_14290_b200 import _lib
+
+    d = D.as_device(csr, 0).with_strategy(strategy)
+    xt = torch.as_tensor(x, device="cuda")
+    yt = torch.full((csr.nrows,), 7.0, dtype=torch.float64, device="cuda")
+    flag = torch.ones(1, dtype=torch.int32, device="cuda")
+    _lib.call("wk_spmv_masked", d.wk_ptr(), D._ptr(xt), D._ptr(yt), D._ptr(flag), D.stream_handle(d.device))
+    assert torch.all(yt == 7.0)
+    flag.zero_()
+    _lib.call("wk_spmv_masked", d.wk_ptr(), D._ptr(xt), D._ptr(yt), D._ptr(flag), D.stream_handle(d.device))
+    assert sparse_ref.max_scaled_rel_err(yt.cpu().numpy(), y_ref, lens) <= TOL
 
 
 # ---- generators ---------------------------------------------------------------------------

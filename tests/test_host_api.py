@@ -73,7 +73,7 @@ class TestExecutor:
         with pytest.raises(ValueError):
             wk.B200Config({"csr_subwarp_size": 64})
         with pytest.raises(ValueError):
-            wk.B200Config({"csr_strategy": "merge"})
+            wk.B200Config({"csr_strategy": "balanced"})
         with pytest.raises(ValueError):
             wk.make_executor("ref", tuning={"block_size": 256})
 

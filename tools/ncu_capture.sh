@@ -1,0 +1,28 @@
+#!/bin/bash
+# Run on the GPU box (gpurun): one `ncu --set full` capture per hot kernel and
+# the launch list of a short bench run. Outputs go to gpurun_out/ncu/; read
+# them here with tools/ncu_summarize.py, which writes profiles/ncu_summary.json.
+#   gpurun -- 'bash tools/ncu_capture.sh [tag]'
+set -u
+TAG=${1:-cur}
+OUT=gpurun_out/ncu
+mkdir -p "$OUT"
+NCU="ncu --set full --clock-control none --import-source on"
+cap() {  # name kernel-regex skip count cmd...
+    local name=$1 rx=$2 skip=$3 cnt=$4
+    shift 4
+    timeout 600 $NCU -k "regex:$rx" -s "$skip" -c "$cnt" -f -o "$OUT/${TAG}_$name" "$@" > "$OUT/${TAG}_$name.log" 2>&1
+    echo "$name rc=$?" >> "$OUT/${TAG}_status.txt"
+}
+cap sellp_spmv sellp64_tma 2 1 python tools/profile_spmv.py sellp 27 200
+cap ell_spmv sliced_spmv 2 1 python tools/profile_spmv.py ell 27 200
+cap csr_rowblock csr_rowblock 2 1 python tools/profile_spmv.py csr 27 200 rowblock
+cap csr_stream "csr_(stream|tma)" 2 1 python tools/profile_spmv.py csr 27 200 stream
+cap csr_rmat "csr_" 2 3 python tools/profile_spmv.py csr_rmat 0 24
+cap coo_rmat coo_kernel 2 1 python tools/profile_spmv.py coo 0 24
+cap csr_poisson2d csr_ 2 1 python tools/profile_spmv.py csr 5 1000 auto
+if [ -n "${WK_NCU_LAUNCHES:-1}" ]; then
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+        --log-file "$OUT/${TAG}_launches.csv" python bench.py --steps 4 --warmup 3 > "$OUT/${TAG}_launches_bench.log" 2>&1
+    echo "launches rc=$?" >> "$OUT/${TAG}_status.txt"
+fi

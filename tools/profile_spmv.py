@@ -1,4 +1,4 @@
-"""One format's SpMV a few times, for ncu: python tools/profile_spmv.py FMT [points] [n]
+"""One format's SpMV a few times, for ncu: python tools/profile_spmv.py FMT [points] [n] [csr strategy]
 FMT in csr, sellp, ell, coo(R-MAT scale n), hybrid(R-MAT)."""
 import sys
 sys.path.insert(0, '.')
@@ -20,6 +20,9 @@ else:
         A = D.csr_to_sellp(A, 64)
     elif fmt == "ell":
         A = D.csr_to_ell(A)
+strategy = sys.argv[4] if len(sys.argv) > 4 else None
+if strategy and getattr(A, "fmt", None) == "csr":
+    A.with_strategy(strategy)
 x = torch.rand(A.ncols, dtype=torch.float64, device='cuda')
 y = torch.empty(A.nrows, dtype=torch.float64, device='cuda')
 for _ in range(5):
