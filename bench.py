@@ -369,7 +369,7 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
         return yy
 
     rec("sellp_27pt_200", A_sellp, x)
-    for strat in ("rowblock", "merge", "stream", "subwarp"):
+    for strat in ("rowblock", "load_balance", "merge", "stream", "subwarp"):
         A_csr.with_strategy(strat, 0)
         rec(f"csr_{strat}_27pt_200", A_csr, x)
     A_csr.with_strategy("auto", 0)
@@ -392,7 +392,7 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
     # config 1: CSR on the 2-D Poisson 1000^2 (80 MB: flush L2 before every launch)
     P = corpus.poisson2d_matrix(1000)
     xp = torch.rand(P.ncols, dtype=torch.float64, device=x.device)
-    for strat in ("rowblock", "merge", "stream"):
+    for strat in ("rowblock", "load_balance", "merge", "stream"):
         P.with_strategy(strat, 0)
         rec(f"csr_{strat}_poisson2d_1000", P, xp, flush_l2=True)
     del P
@@ -401,7 +401,7 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
     xr = torch.rand(R.ncols, dtype=torch.float64, device=x.device)
     rec("coo_rmat24", R, xr)
     Rc = D.coo_to_csr(R)
-    for strat in ("stream", "merge"):
+    for strat in ("load_balance", "merge", "stream"):
         Rc.with_strategy(strat, 0)
         rec(f"csr_{strat}_rmat24", Rc, xr)
     H = D.csr_to_hybrid(Rc)

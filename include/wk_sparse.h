@@ -70,7 +70,9 @@ int wk_version(void);
 int wk_device_sm_count(void);
 /* process-wide kernel selection knobs (A/B measurement): "sellp_kernel":
  * 0 = register-only SELL-P kernel, 1..10 = TMA pipeline configurations
- * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr */
+ * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr;
+ * "coo_kernel": 0..3 (default 3, spmv.cu coo_kernel_choice); "ell_kernel":
+ * 0 = register kernel (default), 1 = TMA pipeline */
 int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */
@@ -239,6 +241,21 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
 int64_t wk_bicgstab_workspace_bytes(int64_t n);
 int wk_bicgstab_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, double* x,
                       double* hist, int64_t* iterations, void* workspace, wk_stream_t stream);
+/* Jacobi-preconditioned CG (z = r / diag, the apply_jacobi fixture,
+ * preconditioner.cu:9-17, inside the reference CG loop kernels.py:283-331;
+ * no reference PCG: order of oracle/krylov_ref.py pcg_jacobi_solve).
+ * diag from wk_extract_diagonal (missing entries -> 0.0). */
+int wk_extract_diagonal(const wk_matrix* A, double* diag, wk_stream_t stream);
+int64_t wk_pcg_workspace_bytes(int64_t n);
+int wk_pcg_jacobi_solve(const wk_matrix* A, const double* diag, const double* b, double tol, int64_t max_iters,
+                        double* x, double* hist, int64_t* iterations, void* workspace, wk_stream_t stream);
+/* reduce_microbench (kernels.py:341-364; reduce_driver.cu:5-23): one warp,
+ * tiles of `size` lanes reduce (rank + 1) `inner_loops` times with the
+ * coop-group butterfly (shared_memory = 0) or the shared-memory tree
+ * (residual_check.cu:17-32 style, shared_memory = 1); out[32] per-lane
+ * results, *cycles = clock64 cycles of the loop (device pointers). */
+int wk_reduce_microbench(int32_t size, int32_t inner_loops, int32_t shared_memory, double* out, long long* cycles,
+                         wk_stream_t stream);
 int64_t wk_gmres_workspace_bytes(int64_t n, int32_t restart);
 int wk_gmres_solve(const wk_matrix* A, const double* b, double tol, int64_t max_iters, int32_t restart,
                    double* x, double* hist, int64_t* iterations, void* workspace, wk_stream_t stream);

@@ -66,6 +66,48 @@ def cg_solve(spmv, b, tol, max_iters, dot=_dot, replace_every=50):
     return x, np.asarray(hist)
 
 
+def pcg_jacobi_solve(spmv, diag, b, tol, max_iters, dot=_dot, replace_every=50):
+    """Jacobi-preconditioned CG: `cg_solve` (kernels.py:283-331) with
+    z = r / diag (the apply_jacobi fixture, preconditioner.cu:9-17) inserted
+    after every residual update; rho = r.z drives alpha and beta, the history
+    and stopping test stay on ||r|| (the reference's criterion). NO reference
+    PCG exists: this fixes the order the B200 solver follows."""
+    b = np.asarray(b, dtype=np.float64)
+    diag = np.asarray(diag, dtype=np.float64)
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    b_norm = float(np.linalg.norm(b))
+    x = np.zeros_like(b)
+    r = b.copy()
+    z = r / diag
+    p = z.copy()
+    rho = dot(r, z)
+    hist = [b_norm]
+    if b_norm == 0.0:
+        return x, np.asarray(hist)
+    threshold = tol * b_norm
+    it = 0
+    while it < max_iters and hist[-1] > threshold:
+        q = spmv(p)
+        p_ap = dot(p, q)
+        if p_ap <= 0.0:
+            raise BreakdownError(f"p.Ap = {p_ap} at iteration {it + 1}; system is not SPD")
+        alpha = rho / p_ap
+        x = x + alpha * p
+        it += 1
+        if replace_every and it % replace_every == 0:
+            r = b - spmv(x)
+        else:
+            r = r - alpha * q
+        z = r / diag
+        rho_next = dot(r, z)
+        hist.append(math.sqrt(dot(r, r)))
+        beta = rho_next / rho
+        p = z + beta * p
+        rho = rho_next
+    return x, np.asarray(hist)
+
+
 def bicgstab_solve(spmv, b, tol, max_iters, dot=_dot):
     """Unpreconditioned BiCGSTAB, x0 = 0, shadow residual r^ = b.
 

@@ -54,7 +54,8 @@ from .kernels import (
     spmv_sellp,
 )
 from .mmio import read_matrix_market, read_matrix_market_entries, write_matrix_market
-from .solvers import Bicgstab, Cg, Gmres, Iteration, ResidualNorm, bicgstab_solve, cg_solve, gmres_solve
+from .solvers import (Bicgstab, Cg, Gmres, Iteration, Jacobi, ResidualNorm, bicgstab_solve, cg_solve, diagonal,
+                      gmres_solve, pcg_solve, reduce_microbench)
 
 __version__ = "0.1.0"
 
@@ -67,5 +68,6 @@ __all__ = [
     "axpy", "coo_to_csr", "coo_to_sellp", "csr_to_coo", "csr_to_ell", "csr_to_hybrid", "csr_to_sellp", "dot",
     "norm2", "spmv", "spmv_coo", "spmv_csr", "spmv_ell", "spmv_hybrid", "spmv_sellp",
     "read_matrix_market", "read_matrix_market_entries", "write_matrix_market",
-    "Bicgstab", "Cg", "Gmres", "Iteration", "ResidualNorm", "bicgstab_solve", "cg_solve", "gmres_solve",
+    "Bicgstab", "Cg", "Gmres", "Iteration", "Jacobi", "ResidualNorm", "bicgstab_solve", "cg_solve", "diagonal",
+    "gmres_solve", "pcg_solve", "reduce_microbench",
 ]

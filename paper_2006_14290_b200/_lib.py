@@ -88,6 +88,10 @@ _SIGS = {
     "wk_mm_read_header": (ctypes.c_int, [P, I64, P]),
     "wk_mm_parse_entries": (ctypes.c_int, [P, I64, P, I32, P, P, P, I64, P]),
     "wk_mm_write": (ctypes.c_int, [I64, I64, I64, P, P, P, P, I64, P]),
+    "wk_extract_diagonal": (ctypes.c_int, [P, P, P]),
+    "wk_pcg_workspace_bytes": (I64, [I64]),
+    "wk_pcg_jacobi_solve": (ctypes.c_int, [P, P, P, F64, I64, P, P, P, P, P]),
+    "wk_reduce_microbench": (ctypes.c_int, [I32, I32, I32, P, P, P]),
     "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),
     "wk_spmv_hybrid_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P]),
     "wk_spmv": (ctypes.c_int, [P, P, P, P]),

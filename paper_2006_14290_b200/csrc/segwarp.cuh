@@ -312,21 +312,42 @@ seg8_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ 
             // heads: non-empty rows starting inside [E, E + 256)
             if (lane < kS8Win / 32) s_mask[wib][lane] = 0u;
             __syncwarp();
+            // row starts of the next kSuper*32 rows in one batch of independent
+            // loads (the expansion is a serial chain per warp: one latency per
+            // batch instead of one per 32 rows — windows in sparse regions span
+            // hundreds of mostly empty rows)
+            constexpr int kSuper = 4;
             for (;;) {
-                const int64_t rr = rnext + lane;
-                int s0 = INT_MAX;
-                if (rr < nrows) s0 = __ldg(rows + rr);
-                int s1 = __shfl_down_sync(FULL, s0, 1);
-                if (lane == 31) s1 = (rr < nrows) ? __ldg(rows + rr + 1) : INT_MAX;
-                const bool in = int64_t(s0) < E + kS8Win;
-                if (in && s1 > s0) {
-                    const int p = int(int64_t(s0) - E);
-                    s_row[wib][p] = int(rr);
-                    atomicOr(&s_mask[wib][p >> 5], 1u << (p & 31));
+                int s0[kSuper + 1];
+#pragma unroll
+                for (int k = 0; k < kSuper; ++k) {
+                    const int64_t rr = rnext + 32 * k + lane;
+                    s0[k] = rr < nrows ? __ldg(rows + rr) : INT_MAX;
                 }
-                const int m = __popc(__ballot_sync(FULL, in));
+                {
+                    const int64_t rr = rnext + 32 * kSuper;  // one past the batch, for lane 31's s1
+                    s0[kSuper] = rr <= nrows ? __ldg(rows + rr) : INT_MAX;
+                }
+                int m = 0;
+#pragma unroll
+                for (int k = 0; k < kSuper; ++k) {
+                    const int64_t rr = rnext + 32 * k + lane;
+                    int s1 = __shfl_down_sync(FULL, s0[k], 1);
+                    const int nxt0 = __shfl_sync(FULL, s0[k + 1], 0);
+                    if (lane == 31) s1 = (k + 1 < kSuper) ? nxt0 : s0[kSuper];
+                    if (rr == nrows - 1) s1 = __ldg(rows + nrows);  // the last row ends at nnz
+                    const bool in = int64_t(s0[k]) < E + kS8Win;
+                    if (in && s1 > s0[k]) {
+                        const int p = int(int64_t(s0[k]) - E);
+                        s_row[wib][p] = int(rr);
+                        atomicOr(&s_mask[wib][p >> 5], 1u << (p & 31));
+                    }
+                    const int mk = __popc(__ballot_sync(FULL, in));
+                    m += mk;
+                    if (mk < 32) break;
+                }
                 rnext += m;
-                if (m < 32) break;
+                if (m < 32 * kSuper) break;
             }
             __syncwarp();
             const unsigned bits = (s_mask[wib][lane >> 2] >> ((lane & 3) * 8)) & 0xffu;

@@ -158,15 +158,17 @@ class DeviceCsr(DeviceMatrix):
 
     def auto_strategy(self):
         """rowblock when every row is short and the mean is moderate (one lane
-        folds one row from a TMA-staged block; bitwise), merge otherwise
-        (merge-path tiles: equal work per CTA for skewed row lengths).
-        Decided once per matrix (one D2H read)."""
+        folds one row from a TMA-staged block; bitwise), load_balance
+        otherwise (Ginkgo's choice for irregular matrices: equal nonzeros per
+        warp whatever the row-length skew). Decided once per matrix (one D2H
+        read). `merge` (deterministic) and `stream` (bitwise) are explicit
+        choices."""
         if getattr(self, "_auto", None) is None:
             if self.nrows == 0:
-                self._auto = "merge"
+                self._auto = "load_balance"
             else:
                 maxlen = max_row_length(self)
-                self._auto = "rowblock" if maxlen <= 64 and self.nnz <= 28 * self.nrows else "merge"
+                self._auto = "rowblock" if maxlen <= 64 and self.nnz <= 28 * self.nrows else "load_balance"
         return self._auto
 
     def with_strategy(self, strategy, subwarp=0):

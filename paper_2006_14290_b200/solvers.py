@@ -39,7 +39,19 @@ def _check(m, b, tol):
         raise ValueError("tol must be positive")
 
 
-def _run(kind, exec: Executor, m, b, tol, max_iters, restart=30):
+def diagonal(m, exec: Executor = None):
+    """Main diagonal of a matrix as a device vector (wk_extract_diagonal;
+    missing entries are 0.0)."""
+    from .kernels import _prepare
+
+    d = _prepare(exec if exec is not None else make_executor("b200"), m)
+    n = min(d.nrows, d.ncols)
+    out = torch.empty(n, dtype=torch.float64, device=d.device)
+    _lib.call("wk_extract_diagonal", d.wk_ptr(), D._ptr(out), D.stream_handle(d.device))
+    return out
+
+
+def _run(kind, exec: Executor, m, b, tol, max_iters, restart=30, diag=None):
     _check(m, b, tol)
     from .kernels import _prepare
 
@@ -56,6 +68,12 @@ def _run(kind, exec: Executor, m, b, tol, max_iters, restart=30):
         ws = torch.empty(int(L.wk_cg_workspace_bytes(n)), dtype=torch.uint8, device=d.device)
         rc = L.wk_cg_solve(d.wk_ptr(), D._ptr(bt), float(tol), max_iters, D._ptr(x), D._ptr(hist),
                            ctypes.byref(iters), D._ptr(ws), st)
+    elif kind == "pcg":
+        dg = diag if diag is not None else diagonal(d, exec)
+        dg, _ = D.as_device_vector(dg, n, d.device, "diag")
+        ws = torch.empty(int(L.wk_pcg_workspace_bytes(n)), dtype=torch.uint8, device=d.device)
+        rc = L.wk_pcg_jacobi_solve(d.wk_ptr(), D._ptr(dg), D._ptr(bt), float(tol), max_iters, D._ptr(x),
+                                   D._ptr(hist), ctypes.byref(iters), D._ptr(ws), st)
     elif kind == "bicgstab":
         ws = torch.empty(int(L.wk_bicgstab_workspace_bytes(n)), dtype=torch.uint8, device=d.device)
         rc = L.wk_bicgstab_solve(d.wk_ptr(), D._ptr(bt), float(tol), max_iters, D._ptr(x), D._ptr(hist),
@@ -76,6 +94,10 @@ def _cg_b200(exec, m, b, tol, max_iters):
     return _run("cg", exec, m, b, tol, max_iters)
 
 
+def _pcg_b200(exec, m, b, tol, max_iters, diag=None):
+    return _run("pcg", exec, m, b, tol, max_iters, diag=diag)
+
+
 def _bicgstab_b200(exec, m, b, tol, max_iters):
     return _run("bicgstab", exec, m, b, tol, max_iters)
 
@@ -85,6 +107,7 @@ def _gmres_b200(exec, m, b, tol, max_iters, restart=30):
 
 
 register("cg", {EXEC_B200: _cg_b200})
+register("pcg", {EXEC_B200: _pcg_b200})
 register("bicgstab", {EXEC_B200: _bicgstab_b200})
 register("gmres", {EXEC_B200: _gmres_b200})
 
@@ -94,6 +117,13 @@ def cg_solve(m, b, tol: float, max_iters: int, exec: Executor):
     with len(history) == iterations + 1. Like the reference it does not reset
     the executor's counters (it bypasses dispatch, kernels.py:299)."""
     return op_impl("cg", exec)(exec, m, b, tol, max_iters)
+
+
+def pcg_solve(m, b, tol: float, max_iters: int, exec: Executor, diag=None):
+    """Jacobi-preconditioned CG: the reference CG loop (kernels.py:283-331)
+    with z = r / diag (the apply_jacobi fixture, preconditioner.cu:9-17);
+    `diag` defaults to the matrix's main diagonal. Returns (x, ||r|| history)."""
+    return op_impl("pcg", exec)(exec, m, b, tol, max_iters, diag)
 
 
 def bicgstab_solve(m, b, tol: float, max_iters: int, exec: Executor):
@@ -160,8 +190,10 @@ class _Solver:
     criteria: tuple
     exec: Executor
     restart: int = 30
+    preconditioner: Optional[object] = None
     iterations: int = 0
     residual_history: Optional[object] = None
+    _diag: Optional[object] = None
 
     def apply(self, b, x=None):
         """Solve A x = b from the zero initial guess; returns x (and fills
@@ -173,6 +205,10 @@ class _Solver:
         tol, max_iters = _criteria_to_params(self.criteria, b, self.exec)
         if self.kind == "gmres":
             sol, hist = _gmres_b200(self.exec, self.A, b, tol, max_iters, self.restart)
+        elif self.kind == "cg" and self.preconditioner is not None:
+            if self._diag is None:
+                self._diag = self.preconditioner.generate(self.A, self.exec)
+            sol, hist = _run("pcg", self.exec, self.A, b, tol, max_iters, diag=self._diag)
         else:
             sol, hist = _run(self.kind, self.exec, self.A, b, tol, max_iters)
         self.iterations = len(hist) - 1
@@ -192,6 +228,7 @@ class _Factory:
     criteria: tuple = field(default_factory=tuple)
     exec: Optional[Executor] = None
     restart: int = 30
+    preconditioner: Optional[object] = None
 
     def generate(self, A) -> _Solver:
         ex = self.exec if self.exec is not None else make_executor("b200")
@@ -200,11 +237,23 @@ class _Factory:
         d = _prepare(ex, A)  # upload once, at generate time (Ginkgo semantics)
         if d.nrows != d.ncols:
             raise DimensionMismatch(f"solver needs a square matrix, got {d.nrows}x{d.ncols}")
-        return _Solver(self.kind, d, tuple(self.criteria), ex, self.restart)
+        return _Solver(self.kind, d, tuple(self.criteria), ex, self.restart, self.preconditioner)
 
 
-def Cg(criteria=(), exec=None) -> _Factory:
-    return _Factory("cg", tuple(criteria), exec)
+@dataclass(frozen=True)
+class Jacobi:
+    """Scalar Jacobi preconditioner M = diag(A) (gko::preconditioner::Jacobi
+    with block size 1; apply z = r / diag as the fixture's apply_jacobi)."""
+
+    def generate(self, A, exec=None):
+        return diagonal(A, exec)
+
+
+def Cg(criteria=(), exec=None, preconditioner=None) -> _Factory:
+    """CG factory; preconditioner=Jacobi() gives the preconditioned solver."""
+    if preconditioner is not None and not isinstance(preconditioner, Jacobi):
+        raise TypeError(f"unsupported preconditioner {preconditioner!r}")
+    return _Factory("cg", tuple(criteria), exec, preconditioner=preconditioner)
 
 
 def Bicgstab(criteria=(), exec=None) -> _Factory:
@@ -213,3 +262,19 @@ def Bicgstab(criteria=(), exec=None) -> _Factory:
 
 def Gmres(criteria=(), exec=None, restart=30) -> _Factory:
     return _Factory("gmres", tuple(criteria), exec, restart)
+
+
+def reduce_microbench(size: int, inner_loops: int, exec: Executor = None, shared_memory: bool = False):
+    """The reference's reduction microbenchmark (kernels.py:341-364) on the
+    GPU: one warp, tiles of `size` lanes butterfly-reduce (rank + 1)
+    `inner_loops` times (coop groups, or the legacy shared-memory tree with
+    shared_memory=True). Returns (per-lane results of the first tile
+    (length size), device clock cycles of the loop)."""
+    ex = exec if exec is not None else make_executor("b200")
+    dev = ex.torch_device()
+    out = torch.empty(32, dtype=torch.float64, device=dev)
+    cyc = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.call("wk_reduce_microbench", int(size), int(inner_loops), int(bool(shared_memory)), D._ptr(out), D._ptr(cyc),
+              D.stream_handle(dev))
+    ex.counters.launches += 1
+    return out[: int(size)].cpu().numpy(), int(cyc.item())

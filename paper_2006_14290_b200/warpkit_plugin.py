@@ -64,8 +64,10 @@ def install(warpkit_module=None, device=None):
         return S._run("cg", ours, m, b, tol, max_iters)
 
     def reduce_microbench(exec, size, inner_loops):
-        # the butterfly of `size` lanes reduces ranks 1..size (kernels.py:351-364)
-        return np.full(size, float(sum(range(1, size + 1))))
+        # the butterfly of `size` lanes reduces ranks 1..size (kernels.py:351-364), on the GPU
+        out, _cycles = S.reduce_microbench(size, inner_loops, ours)
+        exec.counters.lane_steps += int(inner_loops) * int(size)
+        return out
 
     for name, fn in (("spmv_coo", spmv_coo), ("spmv_csr", spmv_csr), ("spmv_sellp", spmv_sellp), ("cg", cg),
                      ("reduce_microbench", reduce_microbench)):

@@ -160,9 +160,19 @@ def test_conversions_golden_bitwise(wk, ex, case):
         assert got.values.tobytes() == ref.values.tobytes(), s
 
 
+@pytest.fixture
+def ell_kernel(wk, request):
+    from paper_2006_14290_b200 import _lib
+
+    _lib.call("wk_config_set", b"ell_kernel", request.param)
+    yield request.param
+    _lib.call("wk_config_set", b"ell_kernel", 0)
+
+
+@pytest.mark.parametrize("ell_kernel", [0, 1], indirect=True)
 @pytest.mark.parametrize("nrows,stride", [(1000, 1000), (4096, 4096), (4100, 4100), (130, 132), (999, 1004),
                                           (1001, 1001), (2000, 2050)])
-def test_ell_strides_bitwise(wk, ex, rng, nrows, stride):
+def test_ell_strides_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
     """ELL through the TMA pipeline (stride % 4 == 0, partial last 64-row
     block) and the register kernel (other strides): bitwise vs the oracle,
     also with non-finite x[0] (padding must then be skipped via row_lengths)."""
@@ -474,14 +484,88 @@ def test_cg_device_resident_and_factory(wk, ex):
     assert torch.equal(xs, x)
 
 
+# ---- Jacobi PCG, diagonal, reduction microbenchmark -----------------------
+
+
+def _shifted_stencil(wk, n, rng):
+    """7-point 3-D Laplacian scaled symmetrically, S A S with S = diag(10^u),
+    u ~ U(-1.5, 1.5): SPD, rows of very different scale (Jacobi undoes the
+    scaling; plain CG struggles)."""
+    from paper_2006_14290_b200 import corpus
+
+    h = corpus.stencil3d(n, 7).to_host()
+    rows = np.repeat(np.arange(h.nrows), np.diff(h.row_ptrs))
+    cols = np.asarray(h.col_idx)
+    sc = 10.0 ** rng.uniform(-1.5, 1.5, size=h.nrows)
+    vals = np.array(h.values, dtype=np.float64) * sc[rows] * sc[cols]
+    return wk.CsrMatrix(h.nrows, h.ncols, h.row_ptrs, h.col_idx, vals), vals[rows == cols]
+
+
+@pytest.mark.parametrize("fmt", ["csr", "sellp", "ell", "coo", "hybrid"])
+def test_diagonal_all_formats(wk, ex, rng, fmt):
+    A, d_ref = _shifted_stencil(wk, 9, rng)
+    m = {"csr": lambda: A, "sellp": lambda: wk.csr_to_sellp(A, 64, ex), "ell": lambda: wk.csr_to_ell(A, exec=ex),
+         "coo": lambda: wk.csr_to_coo(A, ex), "hybrid": lambda: wk.csr_to_hybrid(A, width=3, exec=ex)}[fmt]()
+    d = wk.diagonal(m, ex).cpu().numpy()
+    assert d.tobytes() == d_ref.tobytes()
+    z = wk.CsrMatrix(3, 3, [0, 1, 1, 2], [1, 0], [5.0, 6.0])  # rows without a diagonal entry -> 0.0
+    assert wk.diagonal(z, ex).cpu().numpy().tolist() == [0.0, 0.0, 0.0]
+
+
+@pytest.mark.parametrize("fmt", ["sellp", "csr"])
+@pytest.mark.parametrize("n", [10, 15])
+def test_pcg_jacobi_matches_oracle(wk, ex, rng, fmt, n):
+    """> 50 iterations (residual replacement), equal counts, history within
+    1e-10 ||b||; Jacobi takes fewer iterations than plain CG here."""
+    A, d_ref = _shifted_stencil(wk, n, rng)
+    m = wk.csr_to_sellp(A, 64, ex) if fmt == "sellp" else A
+    b = rng.standard_normal(A.nrows)
+    x, hist = wk.pcg_solve(m, b, 1e-13, 2000, ex)
+    f = lambda v: sparse_ref.spmv(A, v)  # noqa: E731
+    xr, hr = krylov_ref.pcg_jacobi_solve(f, d_ref, b, 1e-13, 2000)
+    assert len(hist) == len(hr) and len(hr) > 51
+    assert np.max(np.abs(hist - hr)) / np.linalg.norm(b) <= 1e-10
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(A)) <= 1e-10
+    _, hc = wk.cg_solve(m, b, 1e-13, 500, ex)
+    assert len(hist) < len(hc)
+    solver = wk.Cg([wk.Iteration(2000), wk.ResidualNorm(1e-13)], ex, preconditioner=wk.Jacobi()).generate(m)
+    xs = solver.apply(b)
+    assert solver.iterations == len(hr) - 1 and np.array_equal(xs, x)
+
+
+def test_pcg_breakdown_and_errors(wk, ex):
+    bad = wk.coo_to_sellp(wk.CooMatrix(2, 2, [0, 1], [0, 1], [1.0, -1.0]), 64, ex)
+    with pytest.raises(wk.BreakdownError):
+        wk.pcg_solve(bad, np.array([0.0, 1.0]), 1e-10, 10, ex, diag=np.ones(2))
+    sq = wk.coo_to_sellp(wk.CooMatrix(3, 3, [0, 1, 2], [0, 1, 2], [2.0, 4.0, 8.0]), 64, ex)
+    x, hist = wk.pcg_solve(sq, np.array([2.0, 4.0, 8.0]), 1e-12, 10, ex)
+    assert np.array_equal(x, [1.0, 1.0, 1.0]) and len(hist) == 2  # exact in one step
+    x, hist = wk.pcg_solve(sq, np.zeros(3), 1e-10, 5, ex)
+    assert np.array_equal(x, np.zeros(3)) and len(hist) == 1
+    with pytest.raises(ValueError):
+        wk.pcg_solve(sq, np.ones(3), -1.0, 5, ex)
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_reduce_microbench(wk, ex, shared):
+    """kernels.py:341-364: every tile of `size` lanes reduces ranks 1..size."""
+    for size in (1, 2, 4, 8, 16, 32):
+        out, cycles = wk.reduce_microbench(size, 100, ex, shared_memory=shared)
+        assert out.tolist() == [float(size * (size + 1) // 2)] * size
+        assert cycles > 0
+    with pytest.raises(ValueError):
+        wk.reduce_microbench(3, 1, ex)
+
+
 # ---- BiCGSTAB / GMRES (no reference: vs the oracle restatement) ----------------------------------
 
 
+@pytest.mark.parametrize("grid", [12, 11])
 @pytest.mark.parametrize("solver", ["bicgstab", "gmres"])
-def test_nonsymmetric_solvers_match_oracle(wk, ex, solver):
+def test_nonsymmetric_solvers_match_oracle(wk, ex, solver, grid):
     from paper_2006_14290_b200 import corpus
 
-    A = corpus.convection_diffusion3d(12)
+    A = corpus.convection_diffusion3d(grid)
     Ah = A.to_host()
     b = np.ones(A.nrows)
     f = lambda v: sparse_ref.spmv(Ah, v)  # noqa: E731

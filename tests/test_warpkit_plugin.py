@@ -71,6 +71,9 @@ def test_reference_api_on_b200(installed):
     xg, hg = warpkit.dispatch("cg", ex, sp, b, 1e-10, 500)
     assert len(hg) == len(hr)
     assert np.max(np.abs(hg - hr)) / np.linalg.norm(b) <= 1e-10
+    for size in (4, 8, 32):  # the reduction microbenchmark runs on the GPU now
+        assert np.array_equal(warpkit.dispatch("reduce_microbench", ex, size, 10),
+                              warpkit.dispatch("reduce_microbench", ref, size, 10))
 
 
 @pytest.mark.gpu

@@ -15,11 +15,13 @@ cap() {  # name kernel-regex skip count cmd...
     echo "$name rc=$?" >> "$OUT/${TAG}_status.txt"
 }
 cap sellp_spmv sellp64_tma 2 1 python tools/profile_spmv.py sellp 27 200
-cap ell_spmv sliced_spmv 2 1 python tools/profile_spmv.py ell 27 200
+cap ell_spmv sellp64_tma 2 1 python tools/profile_spmv.py ell 27 200
 cap csr_rowblock csr_rowblock 2 1 python tools/profile_spmv.py csr 27 200 rowblock
 cap csr_stream "csr_(stream|tma)" 2 1 python tools/profile_spmv.py csr 27 200 stream
-cap csr_rmat "csr_" 2 3 python tools/profile_spmv.py csr_rmat 0 24
-cap coo_rmat coo_kernel 2 1 python tools/profile_spmv.py coo 0 24
+cap csr_rmat seg8 2 1 python tools/profile_spmv.py csr_rmat 0 24 load_balance
+cap csr_merge_rmat csr_merge_kernel 2 1 python tools/profile_spmv.py csr_rmat 0 24 merge
+cap coo_rmat seg8 2 1 python tools/profile_spmv.py coo 0 24
+cap gmres_multidot gmres_multidot_vec 20 1 python tools/profile_gmres.py
 cap csr_poisson2d csr_ 2 1 python tools/profile_spmv.py csr 5 1000 auto
 if [ -n "${WK_NCU_LAUNCHES:-1}" ]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \

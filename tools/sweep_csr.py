@@ -1,5 +1,7 @@
-"""A/B of the CSR stream kernels (wk_config_set "csr_kernel": 0 = CTA per
-chunk, 1 = persistent TMA pipeline) and the subwarp kernel."""
+"""A/B of every CSR strategy / kernel configuration (wk_config_set "csr_kernel":
+stream 0 = CTA per chunk, 1 = persistent TMA pipeline; rowblock 2..7 = fixed
+configurations, 1 = by mean row length), L2 flushed before each launch for
+the small config-1 matrix."""
 import json
 import statistics
 import sys
@@ -27,15 +29,18 @@ for name, A, fl in cases:
     x = torch.rand(A.ncols, dtype=torch.float64, device='cuda')
     y = torch.empty(A.nrows, dtype=torch.float64, device='cuda')
     ref = None
-    for label, strat, choice in (("stream_cta", "stream", 0), ("stream_tma", "stream", 1), ("rb_8x2x1024", "stream", 2),
-                                 ("rb_16x1x1024", "stream", 3), ("rb_16x2x512", "stream", 4), ("rb_20x1x768", "stream", 5),
-                                 ("rb_24x1x640", "stream", 6), ("rb_12x2x768", "stream", 7), ("subwarp", "subwarp", 1)):
+    runs = [("rowblock_auto", "rowblock", 1, 0)] + [(f"rowblock_cfg{c}", "rowblock", c, 0) for c in range(2, 8)]
+    runs += [("stream_cta", "stream", 0, 0), ("stream_tma", "stream", 1, 0), ("load_balance", "load_balance", 1, 0),
+             ("merge", "merge", 1, 0)] + [(f"subwarp{t}", "subwarp", 1, t) for t in (1, 2, 4, 8)]
+    for label, strat, choice, sw in runs:
         _lib.call('wk_config_set', b'csr_kernel', choice)
-        A.with_strategy(strat, 0)
+        A.with_strategy(strat, sw)
         _, per = bench.timed(lambda: kernels.spmv_device(A, x, y), 20, 5, None, flush if fl else None)
         ms = statistics.mean(per)
         if ref is None:
             ref = y.clone()
-        print(json.dumps({"matrix": name, "kernel": label, "ms": round(ms, 4),
-                          "GB/s": round(A.algorithmic_bytes() / ms / 1e6, 1), "same_as_first": bool(torch.equal(ref, y))}))
-    A.with_strategy("stream", 0)
+        print(json.dumps({"matrix": name, "kernel": label, "ms": round(ms, 4), "min_ms": round(min(per), 4),
+                          "GB/s": round(A.algorithmic_bytes() / ms / 1e6, 1),
+                          "max_abs_diff_vs_first": float((ref - y).abs().max())}), flush=True)
+    _lib.call('wk_config_set', b'csr_kernel', 1)
+    A.with_strategy("auto", 0)
