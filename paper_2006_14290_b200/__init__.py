@@ -53,6 +53,7 @@ from .kernels import (
     spmv_hybrid,
     spmv_sellp,
 )
+from .pipeline import SpmvPipeline
 from .mmio import read_matrix_market, read_matrix_market_entries, write_matrix_market
 from .solvers import (Bicgstab, Cg, Gmres, Iteration, Jacobi, ResidualNorm, bicgstab_solve, cg_solve, diagonal,
                       gmres_solve, pcg_solve, reduce_microbench)
@@ -67,7 +68,7 @@ __all__ = [
     "CooMatrix", "CsrMatrix", "EllMatrix", "HybridMatrix", "SellpMatrix",
     "axpy", "coo_to_csr", "coo_to_sellp", "csr_to_coo", "csr_to_ell", "csr_to_hybrid", "csr_to_sellp", "dot",
     "norm2", "spmv", "spmv_coo", "spmv_csr", "spmv_ell", "spmv_hybrid", "spmv_sellp",
-    "read_matrix_market", "read_matrix_market_entries", "write_matrix_market",
+    "read_matrix_market", "read_matrix_market_entries", "write_matrix_market", "SpmvPipeline",
     "Bicgstab", "Cg", "Gmres", "Iteration", "Jacobi", "ResidualNorm", "bicgstab_solve", "cg_solve", "diagonal",
     "gmres_solve", "pcg_solve", "reduce_microbench",
 ]

@@ -12,7 +12,8 @@ from .errors import (BreakdownError, DeviceError, DimensionMismatch, InvalidSlic
                      ParseError, UnsupportedFormat)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libwk_sparse.so")
+# WK_LIB_PATH: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("WK_LIB_PATH") or os.path.join(_HERE, "_lib", "libwk_sparse.so")
 
 WK_OK = 0
 WK_ERR_INVALID = 1001

@@ -217,6 +217,10 @@ namespace wk {
 constexpr int kS8Win = 256;                  // entries per window (8 per lane)
 constexpr int kS8PerWarp = 8 * kS8Win;       // entries per warp range
 constexpr int kS8Warps = 8;                  // warps per block
+#ifndef WK_S8_MIN_BLOCKS
+#define WK_S8_MIN_BLOCKS 1
+#endif
+constexpr int kS8MinBlocks = WK_S8_MIN_BLOCKS;  // resident blocks per SM the register budget targets
 
 inline int64_t seg8_warps(int64_t nnz) { return ceil_div(nnz, kS8PerWarp); }
 inline int64_t seg8_plan_bytes(int64_t nnz) { return ceil_div((seg8_warps(nnz) + 1) * 4, 16) * 16; }
@@ -242,7 +246,7 @@ __global__ void seg8_plan_kernel(int64_t nrows, int64_t nnz, int64_t nwarps, con
 }
 
 template <bool kCsr>
-__global__ void __launch_bounds__(kS8Warps * 32)
+__global__ void __launch_bounds__(kS8Warps * 32, kS8MinBlocks)
 seg8_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ rows, const int* __restrict__ wrow,
             const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
             double* __restrict__ y, const int* __restrict__ skip) {

@@ -384,6 +384,36 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy):
     assert sparse_ref.max_scaled_rel_err(yt.cpu().numpy(), y_ref, lens) <= TOL
 
 
+@pytest.mark.parametrize("shape", ["stencil", "random", "tiny"])
+def test_spmv_pipeline_bitwise(wk, ex, rng, shape):
+    """Host-to-host pipeline (chunked copy-in / sub-range SpMV launches /
+    chunked copy-out on three streams, two alternating buffer sets) ==
+    the one-launch SpMV, bit for bit, over several in-flight submissions."""
+    from paper_2006_14290_b200 import corpus
+
+    if shape == "stencil":
+        m = corpus.stencil3d(20, 27).to_host()
+    elif shape == "random":
+        lens = rng.integers(0, 40, size=3000)
+        ptrs, cols, vals = _banded_case(rng, lens, 5000)
+        m = wk.CsrMatrix(3000, 5000, ptrs, cols, vals)
+    else:
+        m = wk.CsrMatrix(3, 2, [0, 1, 1, 3], [1, 0, 1], [2.0, 3.0, 4.0])
+    sp = wk.csr_to_sellp(m, 64, ex)
+    pipe = wk.SpmvPipeline(sp, chunks=7, pieces=5)
+    xs = [torch.from_numpy(rng.standard_normal(m.ncols)).pin_memory() for _ in range(5)]
+    ys = [torch.empty(m.nrows, dtype=torch.float64, pin_memory=True) for _ in range(5)]
+    for xh, yh in zip(xs, ys):
+        pipe.submit(xh, yh)
+    pipe.synchronize()
+    for xh, yh in zip(xs, ys):
+        ref = sparse_ref.spmv(m, xh.numpy())
+        assert yh.numpy().tobytes() == ref.tobytes()
+    assert pipe(xs[0].numpy()).tobytes() == sparse_ref.spmv(m, xs[0].numpy()).tobytes()
+    with pytest.raises(wk.DimensionMismatch):
+        pipe.submit(torch.zeros(m.ncols + 1, dtype=torch.float64), ys[0])
+
+
 # ---- generators ---------------------------------------------------------------------------
 
 
