@@ -298,8 +298,8 @@ def run_gpu(args, rank, world, dist):
             # consecutive steps in flight on two buffer sets
             pipe = wk.SpmvPipeline(A)
             yhs = [torch.empty(n_local, dtype=torch.float64, pin_memory=True) for _ in range(2)]
-            e_steps = max(3, args.steps // 2)
-            for k in range(2):
+            e_steps = max(10, args.steps)
+            for k in range(3):
                 pipe.submit(xh, yhs[k % 2])
             pipe.synchronize()
             torch.cuda.synchronize()

@@ -72,7 +72,8 @@ int wk_device_sm_count(void);
  * 0 = register-only SELL-P kernel, 1..10 = TMA pipeline configurations
  * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr;
  * "coo_kernel": 0..3 (default 3, spmv.cu coo_kernel_choice); "ell_kernel":
- * 0 = register kernel (default), 1 = TMA pipeline */
+ * 0 = register kernel (default), 1 = TMA pipeline; "seg8_kernel" (COO /
+ * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring */
 int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */
@@ -104,7 +105,7 @@ int64_t wk_csr_plan_bytes(int64_t nnz);
 int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream);
 int64_t wk_csr_merge_plan_bytes(int64_t nrows, int64_t nnz);
 int wk_csr_merge_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream);
-int64_t wk_csr_load_balance_plan_bytes(int64_t nnz);
+int64_t wk_csr_load_balance_plan_bytes(int64_t nrows, int64_t nnz);
 int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
                                    wk_stream_t stream);
 

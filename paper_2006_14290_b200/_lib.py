@@ -84,7 +84,7 @@ _SIGS = {
     "wk_csr_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_csr_merge_plan_bytes": (I64, [I64, I64]),
     "wk_csr_merge_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
-    "wk_csr_load_balance_plan_bytes": (I64, [I64]),
+    "wk_csr_load_balance_plan_bytes": (I64, [I64, I64]),
     "wk_csr_load_balance_plan_build": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_mm_read_header": (ctypes.c_int, [P, I64, P]),
     "wk_mm_parse_entries": (ctypes.c_int, [P, I64, P, I32, P, P, P, I64, P]),

@@ -66,6 +66,7 @@ int set_sellp_kernel(int choice);
 int set_csr_kernel(int choice);
 int set_coo_kernel(int choice);
 int set_ell_kernel(int choice);
+int set_seg8_kernel(int choice);
 
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.

@@ -13,19 +13,15 @@
 // range can share with its neighbours (its first and last) go through
 // atomicAdd on a zero-filled y (or on y itself when accumulating, Hybrid).
 //
-// CSR variant ("balanced"): equal nonzeros per warp whatever the row-length
-// skew, reading 12 B per entry instead of COO's 16. Row ids are expanded on
-// the fly from row_ptrs: per batch window [e, e+32) the lanes load 32 row
-// starts from the next unpassed row (one coalesced load), a ballot marks the
-// non-empty rows starting inside the window, and entry q's row is the last
-// such row starting at or before q (popc + fns) — no per-entry index array.
-// The row containing each warp range's first entry comes from a plan built
-// once per matrix (binary search).
+// seg_warp_kernel<true> expands CSR row ids on the fly from row_ptrs (a
+// serial chain of dependent loads per warp; kept for A/B): the CSR
+// load-balance strategy uses seg8 with a precomputed head plan (below).
 #pragma once
 
 #include <climits>
 
 #include "common.cuh"
+#include "reduce.cuh"
 
 namespace wk {
 
@@ -209,60 +205,250 @@ namespace wk {
 // (separately rounded, column order: rows inside one lane's 8 entries are the
 // reference fold bit for bit) and ONE warp segmented scan per window joins the
 // lanes — about an eighth of the shuffle work of seg_warp_kernel, whose
-// per-32-entry scans made it issue-bound. Loads are 16/32-byte vectors per
-// lane (each warp instruction covers 512 B / 1 KB contiguous). CSR row ids
-// come from the row starts falling inside the window, recorded in a per-warp
-// shared table (row of each head position + a 256-bit head mask).
+// per-32-entry scans made it issue-bound. Warp ranges are 2048 entries (8
+// windows); atomics only for a range's first and last row.
+//
+// CSR row ids come from a "head plan" built once per matrix: per 256-entry
+// window a 256-bit mask of the positions where a non-empty row starts, the
+// number of such heads before each window (hoff, exclusive scan) and the row
+// id of every head in order (hrow). It replaces a per-window walk of row_ptrs
+// (a serial chain of dependent loads) by independent loads of about the size
+// of row_ptrs itself (32 B per window + 4 B per non-empty row).
+//
+// Two data paths: seg8_kernel loads each lane's 8 entries with 16/32-byte
+// vector loads; seg8_tma_kernel (persistent, one CTA per SM) streams whole
+// windows into a per-warp shared-memory ring with cp.async.bulk, so the
+// matrix stream runs S windows ahead of the x gathers.
 // ---------------------------------------------------------------------------
 constexpr int kS8Win = 256;                  // entries per window (8 per lane)
 constexpr int kS8PerWarp = 8 * kS8Win;       // entries per warp range
-constexpr int kS8Warps = 8;                  // warps per block
-#ifndef WK_S8_MIN_BLOCKS
-#define WK_S8_MIN_BLOCKS 1
-#endif
-constexpr int kS8MinBlocks = WK_S8_MIN_BLOCKS;  // resident blocks per SM the register budget targets
+constexpr int kS8Warps = 8;                  // warps per block (direct kernel)
 
 inline int64_t seg8_warps(int64_t nnz) { return ceil_div(nnz, kS8PerWarp); }
-inline int64_t seg8_plan_bytes(int64_t nnz) { return ceil_div((seg8_warps(nnz) + 1) * 4, 16) * 16; }
+inline int64_t seg8_windows(int64_t nnz) { return ceil_div(nnz, kS8Win); }
 
-__global__ void seg8_plan_kernel(int64_t nrows, int64_t nnz, int64_t nwarps, const int* __restrict__ ptrs,
-                                 int* __restrict__ wrow) {
-    const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (w > nwarps) return;
-    const int64_t e = w * kS8PerWarp;
-    if (e >= nnz) {
-        wrow[w] = -1;
-        return;
+struct HeadPlan {
+    const int* hoff;
+    const unsigned* mask;
+    const int* hrow;
+};
+
+struct HeadPlanMut {
+    int* hoff;
+    unsigned* mask;
+    int* hrow;
+    void* scan_ws;
+};
+
+inline int64_t head_plan_bytes(int64_t nrows, int64_t nnz) {
+    const int64_t w = seg8_windows(nnz);
+    return ceil_div((w + 1) * 4, 256) * 256 + w * 32 + ceil_div(nrows * 4, 256) * 256 + scan_ws_bytes(w) + 256;
+}
+
+inline HeadPlanMut head_plan_views(void* plan, int64_t nrows, int64_t nnz) {
+    const int64_t w = seg8_windows(nnz);
+    char* p = reinterpret_cast<char*>(plan);
+    HeadPlanMut h;
+    h.hoff = reinterpret_cast<int*>(p);
+    p += ceil_div((w + 1) * 4, 256) * 256;
+    h.mask = reinterpret_cast<unsigned*>(p);
+    p += w * 32;
+    h.hrow = reinterpret_cast<int*>(p);
+    p += ceil_div(nrows * 4, 256) * 256;
+    h.scan_ws = p;
+    return h;
+}
+
+__global__ void head_mask_kernel(int64_t nrows, const int* __restrict__ ptrs, unsigned* __restrict__ mask) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const int p = ptrs[r];
+    if (ptrs[r + 1] > p) atomicOr(mask + (int64_t(p) >> 5), 1u << (p & 31));
+}
+
+__device__ __forceinline__ int window_heads(const unsigned* __restrict__ mask, int64_t w) {
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c += __popc(mask[w * 8 + k]);
+    return c;
+}
+
+__global__ void head_rows_kernel(int64_t nrows, const int* __restrict__ ptrs, const unsigned* __restrict__ mask,
+                                 const int* __restrict__ hoff, int* __restrict__ hrow) {
+    const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= nrows) return;
+    const int p = ptrs[r];
+    if (ptrs[r + 1] <= p) return;
+    const int64_t w = int64_t(p) >> 8;
+    const int word = (p & 255) >> 5;
+    int k = hoff[w];
+    for (int q = 0; q < word; ++q) k += __popc(mask[w * 8 + q]);
+    k += __popc(mask[w * 8 + word] & ((1u << (p & 31)) - 1u));
+    hrow[k] = int(r);
+}
+
+inline int build_head_plan(int64_t nrows, int64_t nnz, const int* ptrs, void* plan, cudaStream_t st) {
+    const int64_t nw = seg8_windows(nnz);
+    const HeadPlanMut h = head_plan_views(plan, nrows, nnz);
+    if (nw > 0) WK_CUDA(cudaMemsetAsync(h.mask, 0, size_t(nw) * 32, st));
+    if (nrows > 0) {
+        head_mask_kernel<<<(unsigned)ceil_div(nrows, 256), 256, 0, st>>>(nrows, ptrs, h.mask);
+        WK_LAUNCH_CHECK();
     }
-    int64_t lo = 0, hi = nrows;
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (int64_t(ptrs[mid]) <= e)
-            lo = mid;
-        else
-            hi = mid;
+    const unsigned* mask = h.mask;
+    WK_TRY(exclusive_scan(nw, [=] __device__(int64_t w) { return window_heads(mask, w); }, h.hoff, h.scan_ws, st));
+    if (nrows > 0) {
+        head_rows_kernel<<<(unsigned)ceil_div(nrows, 256), 256, 0, st>>>(nrows, ptrs, h.mask, h.hoff, h.hrow);
+        WK_LAUNCH_CHECK();
     }
-    wrow[w] = int(lo);
+    return 0;
+}
+
+// row containing entry e (0 <= e < nnz): the last head at or before e
+__device__ __forceinline__ int head_row_of(const HeadPlan& hp, int64_t e) {
+    const int64_t w = e >> 8;
+    const int pos = int(e & 255);
+    int k = __ldg(hp.hoff + w);
+    for (int q = 0; q < (pos >> 5); ++q) k += __popc(__ldg(hp.mask + w * 8 + q));
+    k += __popc(__ldg(hp.mask + w * 8 + (pos >> 5)) & (0xffffffffu >> (31 - (pos & 31))));
+    return __ldg(hp.hrow + k - 1);
+}
+
+// warp range [wlo, whi): its boundary rows and the head plan of its 8 windows
+// (mask words: lane l holds words l and l + 32 of the range; head offsets: lane < 8)
+struct RangeCsr {
+    unsigned pm0, pm1;
+    int phoff;
+};
+
+__device__ __forceinline__ RangeCsr seg8_range_csr(int lane, int64_t wlo, int64_t whi, int64_t nnz, const HeadPlan& hp,
+                                                   int& first_row, int& last_row) {
+    first_row = head_row_of(hp, wlo);
+    last_row = whi < nnz ? head_row_of(hp, whi) : -1;
+    const int64_t w0 = wlo >> 8, nwin = (nnz + kS8Win - 1) / kS8Win;
+    RangeCsr rc;
+    rc.pm0 = (w0 + (lane >> 3) < nwin) ? __ldg(hp.mask + w0 * 8 + lane) : 0u;
+    rc.pm1 = (w0 + 4 + (lane >> 3) < nwin) ? __ldg(hp.mask + w0 * 8 + 32 + lane) : 0u;
+    rc.phoff = (lane < 8 && w0 + lane < nwin) ? __ldg(hp.hoff + w0 + lane) : 0;
+    return rc;
+}
+
+// CSR row ids of window iw of the range: this lane's 8 mask bits, the heads of
+// the lanes before (warp exclusive scan), consecutive hrow entries
+__device__ __forceinline__ void seg8_csr_rows(int lane, int iw, const RangeCsr& rc, int nv, const HeadPlan& hp,
+                                              int (&rw)[8]) {
+    const unsigned FULL = 0xffffffffu;
+    const unsigned mw = __shfl_sync(FULL, iw < 4 ? rc.pm0 : rc.pm1, (iw * 8 + (lane >> 2)) & 31);
+    const unsigned bits = (mw >> ((lane & 3) * 8)) & 0xffu;
+    const int cnt = __popc(bits);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += o;
+    }
+    int idx = __shfl_sync(FULL, rc.phoff, iw) + incl - cnt;
+    int rcur = (idx > 0 && !(bits & 1u)) ? __ldg(hp.hrow + idx - 1) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if ((bits >> u) & 1u) {
+            rcur = __ldg(hp.hrow + idx);
+            ++idx;
+        }
+        rw[u] = u < nv ? rcur : -1;
+    }
+}
+
+// One window: per-lane sequential fold of the lane's 8 entries (a row ends
+// when the next entry's row differs), one warp segmented scan, emission of the
+// closed rows, and the carry of the row left open at lane 31 into the next
+// window of the same range (closed at the range's last window).
+template <class Emit>
+__device__ __forceinline__ void seg8_fold(int lane, int nv, bool last_window, const double (&pv)[8],
+                                          const int (&rw)[8], int& carry_row, double& carry, Emit emit) {
+    const unsigned FULL = 0xffffffffu;
+    const int first_r = nv > 0 ? rw[0] : -1;
+    const int nxt = __shfl_down_sync(FULL, first_r, 1);
+    double acc = 0.0, first_val = 0.0;
+    int first_emit = -1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        if (u < nv) {
+            acc = __dadd_rn(acc, pv[u]);
+            int rn;
+            if (u + 1 < nv) {
+                rn = rw[u + 1];
+            } else if (lane < 31 && nxt >= 0) {
+                rn = nxt;
+            } else {
+                rn = (lane == 31 && !last_window) ? INT_MIN : -1;  // INT_MIN: open, -1: range end
+            }
+            if (rn != rw[u] && rn != INT_MIN) {
+                if (first_emit < 0) {
+                    first_emit = rw[u];
+                    first_val = acc;
+                } else {
+                    emit(rw[u], acc);
+                }
+                acc = 0.0;
+            }
+        }
+    }
+    // warp segmented scan of (closed a row, partial since the last close)
+    int f = first_emit >= 0;
+    double sv = acc;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double ov = __shfl_up_sync(FULL, sv, d);
+        const int of = __shfl_up_sync(FULL, f, d);
+        if (lane >= d) {
+            if (!f) sv = __dadd_rn(ov, sv);
+            f |= of;
+        }
+    }
+    double ex = __shfl_up_sync(FULL, sv, 1);
+    int exf = __shfl_up_sync(FULL, f, 1);
+    if (lane == 0) {
+        ex = 0.0;
+        exf = 0;
+    }
+    // the window's carry-in continues the row of its first entry, or is complete
+    const int w_first = __shfl_sync(FULL, first_r, 0);
+    double cin = 0.0;
+    if (carry_row >= 0) {
+        if (carry_row == w_first)
+            cin = carry;
+        else if (lane == 0)
+            emit(carry_row, carry);
+    }
+    if (!exf) ex = __dadd_rn(cin, ex);
+    if (first_emit >= 0) emit(first_emit, __dadd_rn(ex, first_val));
+    const double t31 = __shfl_sync(FULL, sv, 31);
+    const int f31 = __shfl_sync(FULL, f, 31);
+    const int r31 = __shfl_sync(FULL, nv > 0 ? rw[nv - 1] : -1, 31);
+    if (!last_window) {
+        carry_row = r31;
+        carry = f31 ? t31 : __dadd_rn(cin, t31);
+    } else {
+        carry_row = -1;
+    }
 }
 
 template <bool kCsr>
-__global__ void __launch_bounds__(kS8Warps * 32, kS8MinBlocks)
-seg8_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ rows, const int* __restrict__ wrow,
-            const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
-            double* __restrict__ y, const int* __restrict__ skip) {
+__global__ void __launch_bounds__(kS8Warps * 32)
+seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
+            const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+            const int* __restrict__ skip, HeadPlan hp) {
     if (skip != nullptr && *skip) return;
-    const unsigned FULL = 0xffffffffu;
-    __shared__ int s_row[kS8Warps][kS8Win];
-    __shared__ unsigned s_mask[kS8Warps][kS8Win / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int64_t warp = int64_t(blockIdx.x) * kS8Warps + wib;
     const int64_t wlo = warp * kS8PerWarp;
     if (wlo >= nnz) return;
     const int64_t whi = (wlo + kS8PerWarp < nnz) ? wlo + kS8PerWarp : nnz;
     int first_row, last_row;
+    RangeCsr rc{0u, 0u, 0};
     if (kCsr) {
-        first_row = __ldg(wrow + warp);
-        last_row = __ldg(wrow + warp + 1);
+        rc = seg8_range_csr(lane, wlo, whi, nnz, hp, first_row, last_row);
     } else {
         first_row = __ldg(rows + wlo);
         last_row = __ldg(rows + whi - 1);
@@ -273,10 +459,8 @@ seg8_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ 
         else
             y[r] = accumulate ? __dadd_rn(y[r], v) : v;
     };
-    int64_t rnext = int64_t(first_row) + 1;  // CSR: first row whose start is not passed
-    int carry_row = -1;                      // open row entering the window, its partial
+    int carry_row = -1;
     double carry = 0.0;
-    int prev_last = first_row;               // row of the last entry of the previous window
     for (int64_t E = wlo; E < whi; E += kS8Win) {
         const int64_t kb = E + 8 * lane;
         const int nv = kb >= whi ? 0 : (whi - kb >= 8 ? 8 : int(whi - kb));
@@ -312,149 +496,185 @@ seg8_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ 
 #pragma unroll
             for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
         }
-        if (kCsr) {
-            // heads: non-empty rows starting inside [E, E + 256)
-            if (lane < kS8Win / 32) s_mask[wib][lane] = 0u;
-            __syncwarp();
-            // row starts of the next kSuper*32 rows in one batch of independent
-            // loads (the expansion is a serial chain per warp: one latency per
-            // batch instead of one per 32 rows — windows in sparse regions span
-            // hundreds of mostly empty rows)
-            constexpr int kSuper = 4;
-            for (;;) {
-                int s0[kSuper + 1];
-#pragma unroll
-                for (int k = 0; k < kSuper; ++k) {
-                    const int64_t rr = rnext + 32 * k + lane;
-                    s0[k] = rr < nrows ? __ldg(rows + rr) : INT_MAX;
-                }
-                {
-                    const int64_t rr = rnext + 32 * kSuper;  // one past the batch, for lane 31's s1
-                    s0[kSuper] = rr <= nrows ? __ldg(rows + rr) : INT_MAX;
-                }
-                int m = 0;
-#pragma unroll
-                for (int k = 0; k < kSuper; ++k) {
-                    const int64_t rr = rnext + 32 * k + lane;
-                    int s1 = __shfl_down_sync(FULL, s0[k], 1);
-                    const int nxt0 = __shfl_sync(FULL, s0[k + 1], 0);
-                    if (lane == 31) s1 = (k + 1 < kSuper) ? nxt0 : s0[kSuper];
-                    if (rr == nrows - 1) s1 = __ldg(rows + nrows);  // the last row ends at nnz
-                    const bool in = int64_t(s0[k]) < E + kS8Win;
-                    if (in && s1 > s0[k]) {
-                        const int p = int(int64_t(s0[k]) - E);
-                        s_row[wib][p] = int(rr);
-                        atomicOr(&s_mask[wib][p >> 5], 1u << (p & 31));
-                    }
-                    const int mk = __popc(__ballot_sync(FULL, in));
-                    m += mk;
-                    if (mk < 32) break;
-                }
-                rnext += m;
-                if (m < 32 * kSuper) break;
-            }
-            __syncwarp();
-            const unsigned bits = (s_mask[wib][lane >> 2] >> ((lane & 3) * 8)) & 0xffu;
-            // row open at this lane's first entry: the last head of the lanes
-            // before (inclusive max-scan of each lane's last head row)
-            int lastr = bits ? s_row[wib][8 * lane + 31 - __clz(bits)] : -1;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int o = __shfl_up_sync(FULL, lastr, d);
-                if (lane >= d && o > lastr) lastr = o;
-            }
-            int open = __shfl_up_sync(FULL, lastr, 1);
-            if (lane == 0 || open < 0) open = prev_last;
-            int rcur = open;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if ((bits >> u) & 1u) rcur = s_row[wib][8 * lane + u];
-                rw[u] = u < nv ? rcur : -1;
-            }
-            __syncwarp();
-        }
-        // row of the entry before / after this lane's range
-        const int first_r = nv > 0 ? rw[0] : -1;
-        const int nxt = __shfl_down_sync(FULL, first_r, 1);
-        const bool last_window = E + kS8Win >= whi;
-        // fold: a row ends after entry u when the next entry's row differs;
-        // lane 31's last row stays open (carried) unless this is the last window
-        double acc = 0.0, first_val = 0.0;
-        int first_emit = -1;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (u < nv) {
-                acc = __dadd_rn(acc, pv[u]);
-                int rn;
-                if (u + 1 < nv) {
-                    rn = rw[u + 1];
-                } else if (lane < 31 && nxt >= 0) {
-                    rn = nxt;
-                } else {
-                    rn = (lane == 31 && !last_window) ? INT_MIN : -1;  // INT_MIN: open, -1: range end
-                }
-                if (rn != rw[u] && rn != INT_MIN) {
-                    if (first_emit < 0) {
-                        first_emit = rw[u];
-                        first_val = acc;
-                    } else {
-                        emit(rw[u], acc);
-                    }
-                    acc = 0.0;
-                }
-            }
-        }
-        // warp segmented scan of (closed a row, partial since the last close)
-        int f = first_emit >= 0;
-        double sv = acc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double ov = __shfl_up_sync(FULL, sv, d);
-            const int of = __shfl_up_sync(FULL, f, d);
-            if (lane >= d) {
-                if (!f) sv = __dadd_rn(ov, sv);
-                f |= of;
-            }
-        }
-        double ex = __shfl_up_sync(FULL, sv, 1);
-        int exf = __shfl_up_sync(FULL, f, 1);
+        if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
+        seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
+    }
+}
+
+// ---- TMA-staged variant -------------------------------------------------------
+// Persistent grid (one CTA of W warps per SM). Warp g takes ranges g, g + G,
+// g + 2G, ... (G warps in the grid); its windows are streamed in order into
+// an S-deep ring: lane 0 issues one cp.async.bulk per array (values, columns,
+// COO rows) per window, mbarrier complete_tx per stage; the entries past the
+// last 4-entry boundary of the matrix are loaded directly by the consumer.
+template <int W, int S>
+struct Seg8TmaCfg {
+    static constexpr int kW = W, kS = S;
+    static constexpr size_t kValBytes = kS8Win * 8, kIdxBytes = kS8Win * 4;
+    static constexpr size_t kStage = kValBytes + 2 * kIdxBytes;  // values | columns | rows (COO)
+    static constexpr size_t kSmem = size_t(W) * S * kStage + size_t(W) * S * 8 + 128;
+};
+
+template <bool kCsr, class Cfg>
+__global__ void __launch_bounds__(Cfg::kW * 32, 1)
+seg8_tma_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                const int* __restrict__ skip, HeadPlan hp) {
+    constexpr int W = Cfg::kW, S = Cfg::kS;
+    if (skip != nullptr && *skip) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* wbase = smem + size_t(wib) * S * Cfg::kStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(W) * S * Cfg::kStage) + wib * S;
+    if (lane == 0) {
+        for (int st = 0; st < S; ++st) mbar_init(bars + st, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    const int64_t gwarp = int64_t(blockIdx.x) * W + wib, nwarps = int64_t(gridDim.x) * W;
+    const int64_t nranges = (nnz + kS8PerWarp - 1) / kS8PerWarp;
+    const int64_t body_end = nnz & ~int64_t(3);  // entries streamed by bulk copies
+    const uint64_t pol = policy_evict_first();
+    // producer cursor over this warp's windows: t -> range gwarp + (t / 8) * nwarps, window t % 8
+    int64_t pt = 0;
+    auto window_start = [&](int64_t t) -> int64_t {
+        const int64_t g = gwarp + (t >> 3) * nwarps;
+        return g < nranges ? g * kS8PerWarp + (t & 7) * kS8Win : nnz;
+    };
+    auto issue = [&](int st) -> bool {  // warp-uniform; lane 0 issues
+        const int64_t E = window_start(pt);
+        if (E >= nnz) return false;
+        ++pt;
         if (lane == 0) {
-            ex = 0.0;
-            exf = 0;
+            // a window past the last 4-entry boundary arms the stage with 0 bytes
+            // (completes at once; the consumer loads its entries directly)
+            const int64_t e1 = (E + kS8Win < body_end) ? E + kS8Win : body_end;
+            const uint32_t n = e1 > E ? uint32_t(e1 - E) : 0u;
+            unsigned char* sb = wbase + size_t(st) * Cfg::kStage;
+            mbar_arrive_expect_tx(bars + st, n * (kCsr ? 12u : 16u));
+            if (n) {
+                bulk_g2s_evict_first(sb, val + E, n * 8, bars + st, pol);
+                bulk_g2s_evict_first(sb + Cfg::kValBytes, col + E, n * 4, bars + st, pol);
+                if (!kCsr)
+                    bulk_g2s_evict_first(sb + Cfg::kValBytes + Cfg::kIdxBytes, rows + E, n * 4, bars + st, pol);
+            }
         }
-        // the window's carry-in continues the row of its first entry, or is complete
-        const int w_first = __shfl_sync(FULL, first_r, 0);
-        double cin = 0.0;
-        if (carry_row >= 0) {
-            if (carry_row == w_first)
-                cin = carry;
-            else if (lane == 0)
-                emit(carry_row, carry);
-        }
-        if (!exf) ex = __dadd_rn(cin, ex);
-        if (first_emit >= 0) emit(first_emit, __dadd_rn(ex, first_val));
-        // carry-out: lane 31's open partial (rows of the last window all closed)
-        const double t31 = __shfl_sync(FULL, sv, 31);
-        const int f31 = __shfl_sync(FULL, f, 31);
-        const int r31 = __shfl_sync(FULL, nv > 0 ? rw[nv - 1] : -1, 31);
-        if (!last_window) {
-            carry_row = r31;
-            carry = f31 ? t31 : __dadd_rn(cin, t31);
-            prev_last = r31;
+        return true;
+    };
+    for (int st = 0; st < S; ++st)
+        if (!issue(st)) break;
+    uint32_t i = 0;  // windows consumed
+    for (int64_t g = gwarp; g < nranges; g += nwarps) {
+        const int64_t wlo = g * kS8PerWarp;
+        const int64_t whi = (wlo + kS8PerWarp < nnz) ? wlo + kS8PerWarp : nnz;
+        int first_row, last_row;
+        RangeCsr rc{0u, 0u, 0};
+        if (kCsr) {
+            rc = seg8_range_csr(lane, wlo, whi, nnz, hp, first_row, last_row);
         } else {
-            carry_row = -1;
+            first_row = __ldg(rows + wlo);
+            last_row = __ldg(rows + whi - 1);
+        }
+        auto emit = [&](int r, double v) {
+            if (r == first_row || r == last_row)
+                atomicAdd(y + r, v);
+            else
+                y[r] = accumulate ? __dadd_rn(y[r], v) : v;
+        };
+        int carry_row = -1;
+        double carry = 0.0;
+        for (int64_t E = wlo; E < whi; E += kS8Win, ++i) {
+            const int st = int(i % S);
+            const int64_t kb = E + 8 * lane;
+            const int nv = kb >= whi ? 0 : (whi - kb >= 8 ? 8 : int(whi - kb));
+            const bool staged = E < body_end;
+            mbar_wait(bars + st, (i / S) & 1);
+            const unsigned char* sb = wbase + size_t(st) * Cfg::kStage;
+            int c[8], rw[8];
+            double v[8];
+            if (staged && kb + 8 <= body_end && nv == 8) {
+                const double2* sv = reinterpret_cast<const double2*>(sb) + 4 * lane;
+                const int4* sc = reinterpret_cast<const int4*>(sb + Cfg::kValBytes) + 2 * lane;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double2 t = sv[u];
+                    v[2 * u] = t.x;
+                    v[2 * u + 1] = t.y;
+                }
+                const int4 c0 = sc[0], c1 = sc[1];
+                c[0] = c0.x, c[1] = c0.y, c[2] = c0.z, c[3] = c0.w, c[4] = c1.x, c[5] = c1.y, c[6] = c1.z, c[7] = c1.w;
+                if (!kCsr) {
+                    const int4* sr = reinterpret_cast<const int4*>(sb + Cfg::kValBytes + Cfg::kIdxBytes) + 2 * lane;
+                    const int4 r0 = sr[0], r1 = sr[1];
+                    rw[0] = r0.x, rw[1] = r0.y, rw[2] = r0.z, rw[3] = r0.w;
+                    rw[4] = r1.x, rw[5] = r1.y, rw[6] = r1.z, rw[7] = r1.w;
+                }
+            } else {
+                const double* sv = reinterpret_cast<const double*>(sb);
+                const int* sc = reinterpret_cast<const int*>(sb + Cfg::kValBytes);
+                const int* sr = reinterpret_cast<const int*>(sb + Cfg::kValBytes + Cfg::kIdxBytes);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int64_t k = kb + u;
+                    const bool in = u < nv, sm = staged && k < body_end;
+                    c[u] = in ? (sm ? sc[k - E] : ld_stream(col + k)) : 0;
+                    v[u] = in ? (sm ? sv[k - E] : ld_stream(val + k)) : 0.0;
+                    if (!kCsr) rw[u] = in ? (sm ? sr[k - E] : ld_stream(rows + k)) : -1;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) fence_proxy_async_smem();
+            issue(st);  // refill this stage with the warp's next window
+            double pv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
+            if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
+            seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
         }
     }
 }
 
-inline int launch_seg8(bool csr, int64_t nnz, int64_t nrows, int accumulate, const int* rows, const int* wrow,
-                       const int* col, const double* val, const double* x, double* y, const int* skip,
-                       cudaStream_t st) {
+// seg8 kernel selection (env WK_SEG8_KERNEL or wk_config_set("seg8_kernel", i)):
+// 0 (default) = direct vector loads, 1 = TMA-staged persistent kernel (spmv.cu).
+int seg8_kernel_choice();
+
+template <bool kCsr>
+int launch_seg8_tma(int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
+                    const double* x, double* y, const int* skip, cudaStream_t st, HeadPlan hp) {
+    using Cfg = Seg8TmaCfg<16, 3>;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        WK_CUDA(cudaFuncSetAttribute(seg8_tma_kernel<kCsr, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(Cfg::kSmem)));
+        attr_set[dev & 63] = true;
+    }
+    int64_t grid = sm_count();
+    const int64_t need = ceil_div(seg8_warps(nnz), Cfg::kW);
+    if (grid > need) grid = need;
+    seg8_tma_kernel<kCsr, Cfg><<<(unsigned)grid, Cfg::kW * 32, Cfg::kSmem, st>>>(nnz, accumulate, rows, col, val, x,
+                                                                                y, skip, hp);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+// rows: COO row indices (csr = false) or unused (csr = true, row ids from hp).
+// The TMA path needs 16-byte aligned arrays.
+inline int launch_seg8(bool csr, int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
+                       const double* x, double* y, const int* skip, cudaStream_t st,
+                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr}) {
+    if (nnz == 0) return 0;
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (seg8_kernel_choice() == 1 && al(col) && al(val) && (csr || al(rows))) {
+        if (csr) return launch_seg8_tma<true>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
+        return launch_seg8_tma<false>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
+    }
     const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
     if (csr)
-        seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, nrows, accumulate, rows, wrow, col, val, x, y, skip);
+        seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
     else
-        seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, nrows, accumulate, rows, wrow, col, val, x, y, skip);
+        seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
     WK_LAUNCH_CHECK();
     return 0;
 }

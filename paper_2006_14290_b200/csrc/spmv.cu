@@ -205,6 +205,28 @@ static int coo_kernel_choice() {
     return g_coo_choice;
 }
 
+// seg8 data path (env WK_SEG8_KERNEL or wk_config_set("seg8_kernel", i)):
+// 0 (default) = direct vector loads, 1 = TMA-staged persistent kernel. The TMA
+// variant is 2x slower on R-MAT (1.27 -> 2.55 ms COO): the kernel is bound by
+// the random x gathers, and the register budget of the persistent grid (16
+// warps per SM) keeps fewer gathers in flight than the direct kernel's
+// 24-32 warps; streaming the matrix ahead does not pay for that.
+static int g_seg8_choice = -1;
+
+int set_seg8_kernel(int choice) {
+    WK_REQUIRE(choice >= 0 && choice <= 1, WK_ERR_INVALID, "seg8 kernel choice must be 0 or 1");
+    g_seg8_choice = choice;
+    return 0;
+}
+
+int seg8_kernel_choice() {
+    if (g_seg8_choice < 0) {
+        const char* e = getenv("WK_SEG8_KERNEL");
+        g_seg8_choice = (e != nullptr) ? atoi(e) : 0;
+    }
+    return g_seg8_choice;
+}
+
 static int log2i(int64_t v) {
     int l = 0;
     while ((int64_t(1) << l) < v) ++l;
@@ -477,8 +499,8 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
         if (nnz == 0) return 0;
         WK_REQUIRE(aligned(col, 16) && aligned(val, 16), WK_ERR_INVALID,
                    "csr load_balance needs 16-byte aligned col_idx / values");
-        return launch_seg8(true, nnz, nrows, 0, ptrs, reinterpret_cast<const int*>(merge_plan), col, val, x, y, skip,
-                           st);
+        const HeadPlanMut h = head_plan_views(merge_plan, nrows, nnz);
+        return launch_seg8(true, nnz, 0, nullptr, col, val, x, y, skip, st, HeadPlan{h.hoff, h.mask, h.hrow});
     }
     if (strategy == WK_CSR_ROWBLOCK) {
         // 32*k-row blocks; the stage capacity is the smallest that keeps a
@@ -519,7 +541,10 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
     }
     const int64_t tiles_per_block = kSpmvThreads / T;
     int64_t blocks = ceil_div(nrows, tiles_per_block);
-    const int64_t cap = int64_t(sm_count()) * 16;
+    // one row per tile in flight: the grid covers every row up to 2^20 blocks
+    // (short-row matrices are latency bound; a grid-stride loop serialises
+    // rows per thread)
+    const int64_t cap = int64_t(1) << 20;
     if (blocks > cap) blocks = cap;
     switch (T) {
 #define WK_SW(N) \
@@ -629,7 +654,7 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const
     if (nnz == 0) return 0;
     const int cc = coo_kernel_choice();
     if (cc == 3 && aligned(row, 16) && aligned(col, 16) && aligned(val, 16))
-        return launch_seg8(false, nnz, nrows, accumulate, row, nullptr, col, val, x, y, skip, st);
+        return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st);
     if (cc == 1 || cc == 3)
         return launch_seg_warp(false, nnz, nrows, accumulate, row, nullptr, col, val, x, y, skip, st);
     if (coo_kernel_choice() == 2) return launch_coo_tile(nnz, accumulate, row, col, val, x, y, skip, st);
@@ -690,16 +715,12 @@ int wk_csr_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void*
 
 int64_t wk_csr_merge_plan_bytes(int64_t nrows, int64_t nnz) { return csr_merge_plan_bytes(nrows, nnz); }
 
-int64_t wk_csr_load_balance_plan_bytes(int64_t nnz) { return seg8_plan_bytes(nnz); }
+int64_t wk_csr_load_balance_plan_bytes(int64_t nrows, int64_t nnz) { return head_plan_bytes(nrows, nnz); }
 
 int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
                                    wk_stream_t stream) {
     clear_error();
-    const int64_t nw = seg8_warps(nnz);
-    seg8_plan_kernel<<<(unsigned)ceil_div(nw + 1, 256), 256, 0, as_stream(stream)>>>(
-        nrows, nnz, nw, row_ptrs, reinterpret_cast<int*>(plan));
-    WK_LAUNCH_CHECK();
-    return 0;
+    return build_head_plan(nrows, nnz, row_ptrs, plan, as_stream(stream));
 }
 
 int wk_csr_merge_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan, wk_stream_t stream) {

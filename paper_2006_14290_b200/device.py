@@ -147,10 +147,12 @@ class DeviceCsr(DeviceMatrix):
         return self._merge_plan
 
     def load_balance_plan(self):
-        """row containing the first entry of every 1024-entry warp range (built once)."""
+        """head plan of the load-balance kernel (segwarp.cuh HeadPlan: per 256-entry
+        window the row-start mask and head count, the row id of every head;
+        built once)."""
         if getattr(self, "_lb_plan", None) is None:
             L = _lib.load()
-            self._lb_plan = torch.empty(int(L.wk_csr_load_balance_plan_bytes(self.nnz)), dtype=torch.uint8,
+            self._lb_plan = torch.empty(int(L.wk_csr_load_balance_plan_bytes(self.nrows, self.nnz)), dtype=torch.uint8,
                                         device=self.device)
             _lib.call("wk_csr_load_balance_plan_build", self.nrows, self.nnz, _ptr(self.row_ptrs),
                       _ptr(self._lb_plan), stream_handle(self.device))

@@ -124,13 +124,31 @@ def test_coo_golden(wk, ex, case, coo_kernel):
         assert sparse_ref.max_scaled_rel_err(y, case.y, sparse_ref.row_nnz(case.csr)) <= TOL
 
 
+@pytest.fixture
+def seg8_kernel(wk, request):
+    from paper_2006_14290_b200 import _lib
+
+    _lib.call("wk_config_set", b"seg8_kernel", request.param)
+    yield request.param
+    _lib.call("wk_config_set", b"seg8_kernel", 0)
+
+
+@pytest.mark.parametrize("seg8_kernel", [0, 1], indirect=True)
 @pytest.mark.parametrize("coo_kernel", COO_KERNELS, indirect=True)
-@pytest.mark.parametrize("shape", ["skewed", "many_tiles", "one_row"])
-def test_coo_hybrid_skewed(wk, ex, rng, shape, coo_kernel):
-    """COO and Hybrid (ELL + COO accumulate) on skewed / multi-tile inputs."""
+@pytest.mark.parametrize("shape", ["skewed", "many_tiles", "one_row", "multi_range"])
+def test_coo_hybrid_skewed(wk, ex, rng, shape, coo_kernel, seg8_kernel):
+    """COO and Hybrid (ELL + COO accumulate) on skewed / multi-tile inputs;
+    multi_range: more 2048-entry warp ranges than warps in the persistent
+    TMA grid (ring reuse across ranges), nnz not a multiple of 4."""
+    if seg8_kernel == 1 and coo_kernel != 3:
+        pytest.skip("seg8_kernel only selects the data path of coo_kernel 3")
     ncols = 70000
     if shape == "one_row":
         lens = np.array([0, 60000, 0, 3])
+    elif shape == "multi_range":
+        lens = np.minimum((rng.pareto(1.2, size=900001) * 4).astype(np.int64), 5000)
+        lens[rng.random(len(lens)) < 0.3] = 0
+        lens[-1] = 7 - int(lens[:-1].sum()) % 4  # nnz % 4 == 3: a tail past the last 4-entry boundary
     else:
         n = 400000 if shape == "many_tiles" else 30000
         lens = np.minimum((rng.pareto(1.3, size=n) * 5).astype(np.int64), 20000)
@@ -321,10 +339,11 @@ def _banded_case(rng, lens, ncols):
     return ptrs, cols.astype(np.int64), rng.standard_normal(int(ptrs[-1]))
 
 
+@pytest.mark.parametrize("seg8_kernel", [0, 1], indirect=True)
 @pytest.mark.parametrize("strategy", ["merge", "load_balance"])
 @pytest.mark.parametrize("shape", ["tile_spanning_row", "empty_runs", "tile_aligned", "all_empty", "one_row",
-                                   "skewed", "ints", "many_tiles"])
-def test_csr_balanced_edge_cases(wk, rng, shape, strategy):
+                                   "skewed", "ints", "many_tiles", "multi_range"])
+def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
     """merge-path and load-balance CSR: rows spanning many tiles / warp
     ranges, long runs of empty rows crossing them, rows ending exactly on tile /
     thread boundaries, empty matrices; tolerance 1e-12, exact on integer data;
@@ -349,6 +368,12 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy):
         # > 2 tiles per CTA of the persistent grid: every pipeline stage is reused
         lens = np.minimum((rng.pareto(1.5, size=400000) * 6).astype(np.int64), 20000)
         lens[rng.random(400000) < 0.3] = 0
+        ptrs, cols, vals = _banded_case(rng, lens, ncols)
+    elif shape == "multi_range":
+        # more 2048-entry warp ranges than warps in the persistent seg8 grid
+        lens = np.minimum((rng.pareto(1.2, size=900001) * 4).astype(np.int64), 5000)
+        lens[rng.random(len(lens)) < 0.3] = 0
+        lens[-1] = 7 - int(lens[:-1].sum()) % 4  # nnz % 4 == 3
         ptrs, cols, vals = _banded_case(rng, lens, ncols)
     else:
         ptrs, cols, vals = _merge_case(rng, lens, ncols, ints=(shape == "ints"))
