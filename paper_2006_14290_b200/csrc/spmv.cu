@@ -541,10 +541,7 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
     }
     const int64_t tiles_per_block = kSpmvThreads / T;
     int64_t blocks = ceil_div(nrows, tiles_per_block);
-    // one row per tile in flight: the grid covers every row up to 2^20 blocks
-    // (short-row matrices are latency bound; a grid-stride loop serialises
-    // rows per thread)
-    const int64_t cap = int64_t(1) << 20;
+    const int64_t cap = int64_t(sm_count()) * 16;
     if (blocks > cap) blocks = cap;
     switch (T) {
 #define WK_SW(N) \
