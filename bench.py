@@ -254,6 +254,7 @@ def run_gpu(args, rank, world, dist):
     peak, peak_src = peaks()
     out = {}
 
+    comm_mode = None
     if world == 1:
         A_csr = corpus.stencil3d(GRID, 27)
         A = D.csr_to_sellp(A_csr, SLICE)
@@ -263,10 +264,15 @@ def run_gpu(args, rank, world, dist):
 
         part = DI.stencil_slab_operator(GRID, GRID, GRID, corpus.points_27pt(), dist, fmt="sellp",
                                         slice_size=SLICE)
+        comm_mode = DI.maybe_enable_peer(part)
         A = part.local
         nnz = part.local_nnz
     n_local = A.nrows
     x = torch.rand(A.ncols, dtype=torch.float64, device=dev, generator=torch.Generator(device=dev).manual_seed(42))
+    if world > 1:
+        xe = part.new_vector()  # in the peer arena when the peer path is on
+        xe.copy_(x)
+        x = xe
     y = torch.empty(n_local, dtype=torch.float64, device=dev)
     if world == 1:
         step = lambda: wk.kernels.spmv_device(A, x, y)  # noqa: E731
@@ -327,7 +333,9 @@ def run_gpu(args, rank, world, dist):
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 per GPU (BASELINE config 2)"
-                               + (f", z-slab partitioned {GRID}x{GRID}x{GRID * world}, halo over NCCL" if world > 1 else ""),
+                               + (f", z-slab partitioned {GRID}x{GRID}x{GRID * world}, halo over "
+                                  f"{'NVLink peer stores' if comm_mode == 'peer' else comm_mode.upper()}"
+                                  if world > 1 else ""),
                    "rows_per_gpu": n_local, "nnz_per_gpu": int(nnz), "stored_per_gpu": int(A.stored),
                    "bytes_per_spmv": int(bytes_launch),
                    "l2": "operands 2.7 GB/step >> 126 MB L2: no flush needed between steps",

@@ -412,6 +412,34 @@ int wk_mm_parse_entries(const char* data, int64_t len, const wk_mm_header* heade
 int wk_mm_write(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
                 const double* vals, char* out, int64_t capacity, int64_t* written);
 
+/* ---- peer-memory communication for the row-block distributed solvers
+ *      (replaces the NCCL all-reduce / send-recv of distributed.py on GPUs
+ *      with peer access; csrc/peer.cu). Arenas are cudaMalloc'd, exported
+ *      with CUDA IPC and opened by every other rank. ---------------------- */
+#define WK_PEER_MAX 64
+typedef struct wk_peer_ctx {
+    int32_t rank, world;
+    void* arena[WK_PEER_MAX]; /* every rank's arena in this process's address space */
+    int64_t* seq;             /* device int64[2]: all-reduce / halo sequence numbers (zeroed) */
+    int32_t* error;           /* device int32: 1 / 2 after an all-reduce / halo wait timed out */
+} wk_peer_ctx;
+int wk_sym_alloc(int64_t bytes, void** ptr, void* ipc_handle /* 64 bytes out */);
+int wk_sym_open(const void* ipc_handle, void** ptr);
+int wk_sym_close(void* ptr);
+int wk_sym_free(void* ptr);
+/* bytes of the arena header (flags + all-reduce slots); vectors start after it */
+int64_t wk_peer_arena_header_bytes(void);
+/* dst[0..count) = sum over ranks of src[0..count) (count <= 32), summed in
+ * rank order: bit-identical on every rank. One kernel (stream-ordered). */
+int wk_peer_allreduce(const wk_peer_ctx* ctx, const double* src, double* dst, int32_t count, wk_stream_t stream);
+/* halo exchange of vector x (in this rank's arena): for each send j,
+ * peer_arena[send_peer[j]] + send_dst_offset[j] bytes receives
+ * x[send_idx[j][0..send_count[j])]; returns after the halos of every
+ * recv_peer arrived in this rank's copy (ticket: device u32, zeroed). */
+int wk_peer_exchange(const wk_peer_ctx* ctx, const double* x, int32_t nsend, const int32_t* send_peer,
+                     const int32_t* const* send_idx, const int64_t* send_count, const int64_t* send_dst_offset,
+                     int32_t nrecv, const int32_t* recv_peer, void* ticket, wk_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,15 @@ class WkMmHeader(ctypes.Structure):
                 ("body_offset", I64), ("body_line", I64)]
 
 
+WK_PEER_MAX = 64
+
+
+class WkPeerCtx(ctypes.Structure):
+    """Mirror of `wk_peer_ctx` (include/wk_sparse.h)."""
+
+    _fields_ = [("rank", I32), ("world", I32), ("arena", P * WK_PEER_MAX), ("seq", P), ("error", P)]
+
+
 class WkMatrix(ctypes.Structure):
     """Mirror of `wk_matrix` (include/wk_sparse.h)."""
 
@@ -93,6 +102,13 @@ _SIGS = {
     "wk_pcg_workspace_bytes": (I64, [I64]),
     "wk_pcg_jacobi_solve": (ctypes.c_int, [P, P, P, F64, I64, P, P, P, P, P]),
     "wk_reduce_microbench": (ctypes.c_int, [I32, I32, I32, P, P, P]),
+    "wk_sym_alloc": (ctypes.c_int, [I64, P, P]),
+    "wk_sym_open": (ctypes.c_int, [P, P]),
+    "wk_sym_close": (ctypes.c_int, [P]),
+    "wk_sym_free": (ctypes.c_int, [P]),
+    "wk_peer_arena_header_bytes": (I64, []),
+    "wk_peer_allreduce": (ctypes.c_int, [P, P, P, I32, P]),
+    "wk_peer_exchange": (ctypes.c_int, [P, P, I32, P, P, P, P, I32, P, P, P]),
     "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),
     "wk_spmv_hybrid_f64": (ctypes.c_int, [I64, I64, I64, I64, P, P, P, I64, P, P, P, P, P, P]),
     "wk_spmv": (ctypes.c_int, [P, P, P, P]),

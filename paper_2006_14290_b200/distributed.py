@@ -51,13 +51,17 @@ class Comm:
         self.rank = self.dist.get_rank(group)
         self.world = self.dist.get_world_size(group)
         self.backend = str(self.dist.get_backend(group)).lower()
+        self.peer = None  # PeerComm once an operator enables the peer-memory path
 
     def _staged(self, t):
         return self.backend == "gloo" and t.is_cuda
 
     def allreduce_(self, t):
         """In-place sum all-reduce (NCCL is called even for a single rank, so
-        the graph-captured path is the same code at every world size)."""
+        the graph-captured path is the same code at every world size); the
+        peer-memory kernel once `DistOperator.enable_peer` ran."""
+        if self.peer is not None:
+            return self.peer.allreduce_(t)
         if self.world == 1 and self.backend != "nccl":
             return t
         if self._staged(t):
@@ -249,16 +253,74 @@ class DistOperator:
         self._send_idx = {q: self.ops.index(v) for q, v in plan.send_idx.items()}
         self._send_buf = {q: self.ops.zeros(len(v)) for q, v in plan.send_idx.items()}
         self.launches_per_spmv = 1 + len(self._send_idx)
+        self.peer = None
+        self.n_ext_max = self.n_local + self.n_halo
+
+    def enable_peer(self, vectors=40):
+        """Switch halo exchange and all-reduces to the peer-memory kernels
+        (peer.py / csrc/peer.cu): a symmetric arena per rank sized for
+        `vectors` distributed vectors, IPC-opened by every rank. Collective
+        over the group. Vectors made by `new_vector` afterwards live in the
+        arena (same offsets on every rank)."""
+        from . import peer as PE
+
+        comm = self.comm
+        info = comm.allgather_obj((self.n_local, self.n_local + self.n_halo,
+                                   {q: off for q, (off, cnt) in self.plan.recv_ranges.items()}))
+        self.n_ext_max = max(e for _, e, _ in info)
+        if comm.peer is None:
+            comm.peer = PE.PeerComm(comm, PE.arena_bytes_for(self.n_ext_max, vectors), self.ops.device)
+        self.peer = comm.peer
+        # where my data lands in each receiver's copy of a vector (element offset)
+        self._peer_dst = {q: info[q][0] + info[q][2][comm.rank] for q in self._send_idx}
+        self._peer_recv = sorted(self.plan.recv_ranges)
+        self.launches_per_spmv = 2
+        return self
 
     @property
     def stored(self):
         return getattr(self.local, "stored", self.local_nnz)
 
+    def disable_peer(self):
+        if self.peer is not None:
+            self.peer.close()
+        self.peer = None
+        self.comm.peer = None
+        self.n_ext_max = self.n_local + self.n_halo
+        self.launches_per_spmv = 1 + len(self._send_idx)
+
     def new_vector(self):
-        """Zeroed vector with halo room: [n_local | n_halo]."""
+        """Zeroed vector with halo room: [n_local | n_halo] (in the peer arena
+        when the peer-memory path is enabled)."""
+        if self.peer is not None:
+            return self.peer.vector(self.n_local + self.n_halo, self.n_ext_max)
         return self.ops.zeros(self.n_local + self.n_halo)
 
+    def arena_mark(self):
+        """Allocation mark of the peer arena (None without the peer path)."""
+        return None if self.peer is None else self.peer.mark()
+
+    def arena_release(self, mark):
+        """Free every arena vector allocated after `mark` (the same sequence on
+        all ranks keeps the offsets in step)."""
+        if mark is not None and self.peer is not None:
+            self.peer.release(mark)
+
+    def new_block(self, count, ld):
+        """`count` vectors of leading dimension `ld` (>= n_ext_max on every
+        rank when the peer path is on), zeroed, contiguous."""
+        if self.peer is not None:
+            return self.peer.vector(count * ld)
+        return self.ops.zeros(count * ld)
+
     def exchange(self, x_ext):
+        if self.peer is not None:
+            off = self.peer.offset_of(x_ext)
+            if off is None:
+                raise ValueError("peer exchange needs a vector made by DistOperator.new_vector / new_block")
+            sends = [(q, idx, off + 8 * self._peer_dst[q]) for q, idx in self._send_idx.items()]
+            self.peer.exchange(x_ext, sends, self._peer_recv)
+            return
         sends = []
         for q, idx in self._send_idx.items():
             buf = self._send_buf[q]
@@ -299,6 +361,30 @@ class DistOperator:
                 "unit": "GFLOP/s", "h2d_bytes_per_step": int(8 * self.n_local * self.comm.world),
                 "d2h_bytes_per_step": int(8 * self.n_local * self.comm.world),
                 "ms_per_step": round(ms / steps, 4), "api": "distributed.DistOperator.spmv (pinned host x/y)"}
+
+
+def maybe_enable_peer(op, vectors=40):
+    """The peer-memory path (NVLink stores into the other ranks' IPC-mapped
+    arenas, no NCCL on the data path) unless WK_DIST_COMM=nccl; falls back to
+    NCCL on every rank if any rank cannot set it up (collective decision).
+    Returns "peer" or the process group's backend."""
+    import warnings
+
+    if os.environ.get("WK_DIST_COMM", "peer") != "peer" or op.comm.world == 1:
+        return op.comm.backend
+    try:
+        op.enable_peer(vectors)
+        return "peer"
+    except Exception as exc:  # pragma: no cover - depends on the box
+        warnings.warn(f"peer-memory path unavailable ({exc}); using {op.comm.backend}")
+        op.peer = None
+        op.comm.peer = None
+        return op.comm.backend
+
+
+def _check_peer(op):
+    if op.peer is not None:
+        op.peer.check()
 
 
 def _convert_local(dcsr, fmt, slice_size):
@@ -432,6 +518,7 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
     n = op.n_local
     if tol <= 0:
         raise ValueError("tol must be positive")
+    mark = op.arena_mark()
     b = b_local
     x = op.new_vector()
     r = ops.zeros(n)
@@ -459,7 +546,7 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
             ops.cg("wk_cg_update_p_beta", n, r, p, st, hist)
 
     if graph is None:
-        graph = comm.backend == "nccl" and os.environ.get("WK_DIST_GRAPH", "1") != "0"
+        graph = (comm.backend == "nccl" or comm.peer is not None) and os.environ.get("WK_DIST_GRAPH", "1") != "0"
     g = None
     first = True
     while not ops.read_state(st).done:
@@ -473,9 +560,13 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
             period()
         first = False
     h = ops.read_state(st)
+    _check_peer(op)
+    x = x[:n].clone() if mark is not None else x[:n]
+    del g, period
+    op.arena_release(mark)
     if h.breakdown:
         raise BreakdownError(f"p.Ap <= 0 at iteration {h.iteration}; system is not SPD")
-    return x[:n], hist[: h.iteration + 1]
+    return x, hist[: h.iteration + 1]
 
 
 def _capture(fn):
@@ -505,7 +596,7 @@ def _run_periods(ops, comm, st, cls, period, graph):
     """Replay `period` until the device `done` flag of state `st` is set;
     CUDA-graph captured after the first (eager) period when `graph`."""
     if graph is None:
-        graph = comm.backend == "nccl" and os.environ.get("WK_DIST_GRAPH", "1") != "0"
+        graph = (comm.backend == "nccl" or comm.peer is not None) and os.environ.get("WK_DIST_GRAPH", "1") != "0"
     g = None
     first = True
     while not ops.read_state(st, cls).done:
@@ -530,6 +621,7 @@ def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=
     if tol <= 0:
         raise ValueError("tol must be positive")
     C = _lib.WkBicgState
+    mark = op.arena_mark()
     x = ops.zeros(n)
     r, rh, v, t = ops.zeros(n), ops.zeros(n), ops.zeros(n), ops.zeros(n)
     p, sv = op.new_vector(), op.new_vector()
@@ -571,6 +663,9 @@ def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=
             ops.step("wk_bicg_step_r", st, hist)
 
     h = _run_periods(ops, comm, st, C, period, graph)
+    _check_peer(op)
+    del period
+    op.arena_release(mark)
     if h.breakdown:
         raise BreakdownError(f"BiCGSTAB breakdown at iteration {h.iteration}")
     return x, hist[: h.iteration + 1]
@@ -589,8 +684,9 @@ def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=Non
     if not (1 <= m <= 31):
         raise ValueError("restart must be in [1, 31]")
     C = _lib.WkGmresState
-    ld = ((n_ext + 31) // 32) * 32
-    V = ops.zeros((m + 1) * ld)
+    mark = op.arena_mark()
+    ld = ((op.n_ext_max + 31) // 32) * 32  # the same on every rank (peer arena offsets)
+    V = op.new_block(m + 1, ld)
     x = op.new_vector()
     w, r = ops.zeros(n), ops.zeros(n)
     H = ops.zeros((m + 1) * m)
@@ -627,7 +723,11 @@ def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=Non
         ops.step("wk_gmres_restart", st, hist)
 
     h = _run_periods(ops, comm, st, C, period, graph)
-    return x[:n], hist[: h.iteration + 1]
+    _check_peer(op)
+    x = x[:n].clone() if mark is not None else x[:n]
+    del period
+    op.arena_release(mark)
+    return x, hist[: h.iteration + 1]
 
 
 def bench_cg(grid, iters, dist, timed):
@@ -635,6 +735,7 @@ def bench_cg(grid, iters, dist, timed):
     from . import corpus
 
     op = stencil_slab_operator(grid, grid, None, corpus.points_7pt(), dist, fmt="sellp", weak=False, nz=grid)
+    mode = maybe_enable_peer(op)
     b = op.ops.zeros(op.n_local) + 1.0
     cg_solve(op, b, 1e-30, 50)
     torch.cuda.synchronize()
@@ -650,7 +751,7 @@ def bench_cg(grid, iters, dist, timed):
     return {"workload": f"distributed CG, 7-point Laplacian {grid}^3 z-slab partitioned over {op.comm.world} GPUs, "
                         f"SELL-P(64), tol 1e-30, {iters} iterations", "iterations": it, "ms": round(ms, 2),
             "it_per_s": round(it / (ms * 1e-3), 1), "n_gpus": op.comm.world, "scaling": "strong",
-            "halo_bytes_per_spmv": op.plan.bytes_per_exchange}
+            "halo_bytes_per_spmv": op.plan.bytes_per_exchange, "comm": mode}
 
 
 def bench_nonsym(grid, iters, dist):
@@ -660,8 +761,9 @@ def bench_nonsym(grid, iters, dist):
 
     op = stencil_slab_operator(grid, grid, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist, fmt="sellp",
                                weak=False, nz=grid)
+    mode = maybe_enable_peer(op)
     b = op.ops.zeros(op.n_local) + 1.0
-    out = {"workload": f"distributed BiCGSTAB / GMRES(30), 7-point convection-diffusion {grid}^3 z-slab partitioned "
+    out = {"comm": mode, "workload": f"distributed BiCGSTAB / GMRES(30), 7-point convection-diffusion {grid}^3 z-slab partitioned "
                        f"over {op.comm.world} GPUs, SELL-P(64), tol 1e-30, fixed iteration counts",
            "n_gpus": op.comm.world, "scaling": "strong"}
     for kind, fn in (("bicgstab", lambda it: bicgstab_solve(op, b, 1e-30, it)),

@@ -1,0 +1,139 @@
+"""The peer-memory data path of the distributed solvers (peer.py,
+csrc/peer.cu): halo exchange and all-reduces as kernels storing into the
+other ranks' IPC-mapped arenas, the whole solver period in one CUDA graph,
+no NCCL on the data path. Two ranks share cuda:0 (the GPU box has one GPU;
+CUDA IPC maps memory between processes on the same device exactly as between
+NVLink peers, and the device time-slices the two contexts while a rank waits
+on the other's flag). Checks: SpMV bitwise == the global fold, CG / BiCGSTAB
+/ GMRES(m) == the oracle (iteration count, history within 1e-10 ||b||),
+identical histories on both ranks, no wait timed out."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import corpus_ref, krylov_ref, sparse_ref  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2006_14290_b200 import corpus
+        from paper_2006_14290_b200 import distributed as DI
+
+        res = {}
+        op = DI.stencil_slab_operator(12, 10, 6, corpus.points_27pt(), dist, fmt="sellp").enable_peer()
+        x = op.new_vector()
+        g = torch.Generator(device="cuda").manual_seed(5 + rank)
+        x[: op.n_local] = torch.rand(op.n_local, dtype=torch.float64, device="cuda", generator=g)
+        y = torch.zeros(op.n_local, dtype=torch.float64, device="cuda")
+        op.spmv(x, y)
+        torch.cuda.synchronize()
+        res["slab_x"], res["slab_y"] = x[: op.n_local].cpu().numpy(), y.cpu().numpy()
+        # all-reduce of 40 values (two 32-wide chunks), rank-order sums
+        t = torch.arange(40, dtype=torch.float64, device="cuda") * (rank + 1) + 0.125
+        op.comm.allreduce_(t)
+        res["allreduce"] = t.cpu().numpy()
+        res["err0"] = int(op.peer.error.item())
+
+        opg = DI.stencil_slab_operator(12, 12, None, corpus.points_7pt(), dist, fmt="sellp", weak=False,
+                                       nz=12).enable_peer()
+        b = torch.ones(opg.n_local, dtype=torch.float64, device="cuda")
+        for graph in (False, True):
+            xs, hist = DI.cg_solve(opg, b, 1e-12, 500, graph=graph)
+            res[f"cg_x_{graph}"], res[f"cg_hist_{graph}"] = xs.cpu().numpy(), hist.cpu().numpy()
+        res["err1"] = int(opg.peer.error.item())
+
+        opn = DI.stencil_slab_operator(10, 10, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist,
+                                       fmt="csr", weak=False, nz=10).enable_peer()
+        bn = torch.ones(opn.n_local, dtype=torch.float64, device="cuda")
+        xs, hist = DI.bicgstab_solve(opn, bn, 1e-10, 500)
+        res["bicg_x"], res["bicg_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        xs, hist = DI.gmres_solve(opn, bn, 1e-10, 500, restart=30)
+        res["gmres_x"], res["gmres_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        res["err2"] = int(opn.peer.error.item())
+        torch.cuda.synchronize()
+        dist.barrier()
+        for o in (op, opg, opn):
+            o.peer.close()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.fixture(scope="module")
+def parts():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    return [out[0], out[1]]
+
+
+def test_peer_no_timeouts(parts):
+    for p in parts:
+        assert (p["err0"], p["err1"], p["err2"]) == (0, 0, 0)
+
+
+def test_peer_spmv_bitwise(parts):
+    m = corpus_ref.stencil(12, 10, 12, corpus_ref.points_27pt())
+    x = np.concatenate([p["slab_x"] for p in parts])
+    y = np.concatenate([p["slab_y"] for p in parts])
+    assert y.tobytes() == sparse_ref.spmv(m, x).tobytes()
+
+
+def test_peer_allreduce_rank_order(parts):
+    v = np.arange(40, dtype=np.float64)
+    want = (0.0 + (v * 1 + 0.125)) + (v * 2 + 0.125)
+    for p in parts:
+        assert p["allreduce"].tobytes() == want.tobytes()
+
+
+def test_peer_cg_graph(parts):
+    m = corpus_ref.stencil(12, 12, 12, corpus_ref.points_7pt())
+    sp = sparse_ref.csr_to_sellp(m, 64)
+    b = np.ones(m.nrows)
+    xr, hr = krylov_ref.cg_solve(lambda v: sparse_ref.spmv(sp, v), b, 1e-12, 500)
+    for graph in (False, True):
+        h0, h1 = parts[0][f"cg_hist_{graph}"], parts[1][f"cg_hist_{graph}"]
+        assert np.array_equal(h0, h1)
+        assert len(h0) == len(hr)
+        assert np.max(np.abs(h0 - hr)) / np.linalg.norm(b) <= 1e-10
+        x = np.concatenate([p[f"cg_x_{graph}"] for p in parts])
+        assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
+    assert np.array_equal(parts[0]["cg_hist_True"], parts[0]["cg_hist_False"])
+
+
+@pytest.mark.parametrize("solver", ["bicg", "gmres"])
+def test_peer_nonsymmetric(parts, solver):
+    m = corpus_ref.stencil(10, 10, 10, corpus_ref.points_7pt(beta=(1.0, 0.5, 0.25)))
+    b = np.ones(m.nrows)
+    f = lambda v: sparse_ref.spmv(m, v)  # noqa: E731
+    if solver == "bicg":
+        xr, hr = krylov_ref.bicgstab_solve(f, b, 1e-10, 500)
+    else:
+        xr, hr = krylov_ref.gmres_solve(f, b, 1e-10, 500, restart=30)
+    h0, h1 = parts[0][f"{solver}_hist"], parts[1][f"{solver}_hist"]
+    assert np.array_equal(h0, h1)
+    assert len(h0) == len(hr)
+    assert np.max(np.abs(h0 - hr)) / np.linalg.norm(b) <= 1e-10
+    x = np.concatenate([p[f"{solver}_x"] for p in parts])
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
