@@ -13,9 +13,8 @@
 // range can share with its neighbours (its first and last) go through
 // atomicAdd on a zero-filled y (or on y itself when accumulating, Hybrid).
 //
-// seg_warp_kernel<true> expands CSR row ids on the fly from row_ptrs (a
-// serial chain of dependent loads per warp; kept for A/B): the CSR
-// load-balance strategy uses seg8 with a precomputed head plan (below).
+// seg_warp_kernel is the COO A/B baseline (coo_kernel 1); the defaults are the
+// seg8 kernels below (COO, and CSR load_balance with a precomputed head plan).
 #pragma once
 
 #include <climits>
@@ -30,35 +29,10 @@ constexpr int kSwU = 4;           // batches of 32 entries per group
 
 inline int64_t seg_warps(int64_t nnz) { return ceil_div(nnz, kSwPerWarp); }
 
-// CSR plan: wrow[w] = row containing entry w*kSwPerWarp (w < nwarps), -1 for w = nwarps
-inline int64_t csr_balanced_plan_bytes(int64_t nnz) { return ceil_div((seg_warps(nnz) + 1) * 4, 16) * 16; }
-
-__global__ void csr_balanced_plan_kernel(int64_t nrows, int64_t nnz, int64_t nwarps, const int* __restrict__ ptrs,
-                                         int* __restrict__ wrow) {
-    const int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (w > nwarps) return;
-    const int64_t e = w * kSwPerWarp;
-    if (e >= nnz) {
-        wrow[w] = -1;
-        return;
-    }
-    // largest r in [0, nrows) with ptrs[r] <= e
-    int64_t lo = 0, hi = nrows;  // invariant: ptrs[lo] <= e, answer in [lo, hi)
-    while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (int64_t(ptrs[mid]) <= e)
-            lo = mid;
-        else
-            hi = mid;
-    }
-    wrow[w] = int(lo);
-}
-
-template <bool kCsr>
 __global__ void __launch_bounds__(256)
-seg_warp_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restrict__ rows,
-                const int* __restrict__ wrow, const int* __restrict__ col, const double* __restrict__ val,
-                const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip) {
+seg_warp_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                const int* __restrict__ skip) {
     if (skip != nullptr && *skip) return;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -67,18 +41,8 @@ seg_warp_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restric
     if (wlo >= nnz) return;
     const int64_t whi = (wlo + kSwPerWarp < nnz) ? wlo + kSwPerWarp : nnz;
     // rows this range can share with its neighbours
-    int first_row, last_row;
-    if (kCsr) {
-        first_row = __ldg(wrow + warp);
-        last_row = __ldg(wrow + warp + 1);  // row containing entry whi (-1 past the end)
-    } else {
-        first_row = __ldg(rows + wlo);
-        last_row = __ldg(rows + whi - 1);
-    }
-    // CSR row expansion state: the row of the last expanded entry, and the
-    // first row whose start has not been passed
-    int cur = first_row;
-    int64_t rnext = int64_t(first_row) + 1;
+    const int first_row = __ldg(rows + wlo);
+    const int last_row = __ldg(rows + whi - 1);
 
     auto emit = [&](int r, double v) {
         if (r == first_row || r == last_row)
@@ -99,7 +63,7 @@ seg_warp_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restric
             if (k < whi) {
                 gc[u] = ld_stream(col + k);
                 gv[u] = ld_stream(val + k);
-                if (!kCsr) gr[u] = ld_stream(rows + k);
+                gr[u] = ld_stream(rows + k);
             }
         }
     };
@@ -119,33 +83,6 @@ seg_warp_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restric
         double p[kSwU];
 #pragma unroll
         for (int u = 0; u < kSwU; ++u) p[u] = (b0 + u * 32 + lane < whi) ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
-        if (kCsr) {
-#pragma unroll
-            for (int u = 0; u < kSwU; ++u) {
-                const int64_t e = b0 + u * 32;
-                if (e >= whi) break;
-                int rq = cur;
-                for (;;) {
-                    const int64_t rr = rnext + lane;
-                    int s0 = INT_MAX;
-                    if (rr < nrows) s0 = __ldg(rows + rr);
-                    int s1 = __shfl_down_sync(FULL, s0, 1);
-                    if (lane == 31) s1 = (rr < nrows) ? __ldg(rows + rr + 1) : INT_MAX;
-                    const bool in = int64_t(s0) < e + 32;
-                    const unsigned inwin = __ballot_sync(FULL, in);
-                    const bool head = in && s1 > s0;
-                    const unsigned heads = __ballot_sync(FULL, head);
-                    const unsigned pm = __reduce_or_sync(FULL, head ? (1u << int(int64_t(s0) - e)) : 0u);
-                    const int cnt = __popc(pm & (FULL >> (31 - lane)));
-                    if (cnt > 0) rq = int(rnext) + int(__fns(heads, 0, cnt));
-                    const int m = __popc(inwin);
-                    rnext += m;
-                    if (m < 32) break;
-                }
-                r[u] = (e + lane < whi) ? rq : -1;
-                cur = __shfl_sync(FULL, rq, 31);
-            }
-        }
 #pragma unroll
         for (int u = 0; u < kSwU; ++u) {
             if (b0 + u * 32 >= whi) break;
@@ -182,15 +119,11 @@ seg_warp_kernel(int64_t nnz, int64_t nrows, int accumulate, const int* __restric
     if (carry_row >= 0 && lane == 0) emit(carry_row, carry);
 }
 
-inline int launch_seg_warp(bool csr, int64_t nnz, int64_t nrows, int accumulate, const int* rows, const int* wrow,
-                           const int* col, const double* val, const double* x, double* y, const int* skip,
-                           cudaStream_t st) {
+inline int launch_seg_warp(int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
+                           const double* x, double* y, const int* skip, cudaStream_t st) {
     const int64_t warps = seg_warps(nnz);
     const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
-    if (csr)
-        seg_warp_kernel<true><<<blocks, 256, 0, st>>>(nnz, nrows, accumulate, rows, wrow, col, val, x, y, skip);
-    else
-        seg_warp_kernel<false><<<blocks, 256, 0, st>>>(nnz, nrows, accumulate, rows, wrow, col, val, x, y, skip);
+    seg_warp_kernel<<<blocks, 256, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -653,7 +653,7 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const
     if (cc == 3 && aligned(row, 16) && aligned(col, 16) && aligned(val, 16))
         return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st);
     if (cc == 1 || cc == 3)
-        return launch_seg_warp(false, nnz, nrows, accumulate, row, nullptr, col, val, x, y, skip, st);
+        return launch_seg_warp(nnz, accumulate, row, col, val, x, y, skip, st);
     if (coo_kernel_choice() == 2) return launch_coo_tile(nnz, accumulate, row, col, val, x, y, skip, st);
     const int64_t warps = ceil_div(nnz, kCooPerWarp);
     const int64_t blocks = ceil_div(warps * 32, kSpmvThreads);
