@@ -256,7 +256,7 @@ constexpr int kCgsGroup = 8;  // basis vectors loaded together (16-byte loads in
 
 static int cgs_grid(int64_t n, int K) {
     int64_t g = ceil_div(ceil_div(n, 2), 256);
-    const int64_t cap = int64_t(sm_count()) * (K > 8 ? 2 : 4);
+    const int64_t cap = int64_t(sm_count()) * (K > 16 ? 2 : 4);
     if (g > cap) g = cap;
     if (g > kRedMaxBlocks) g = kRedMaxBlocks;
     return int(g < 1 ? 1 : g);
@@ -309,9 +309,11 @@ __global__ void __launch_bounds__(256)
 gmres_orth_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, double* __restrict__ w,
                const double* __restrict__ Hj, GS* s, RedWorkspace ws) {
     if (s->cycle_done) return;
-    double h[K];
-#pragma unroll
-    for (int q = 0; q < K; ++q) h[q] = q < k ? Hj[q] : 0.0;
+    // projections in shared memory (broadcast reads): keeps K doubles out of
+    // the register file, so more blocks stay resident
+    __shared__ double h[K];
+    if (threadIdx.x < K) h[threadIdx.x] = int(threadIdx.x) < k ? Hj[threadIdx.x] : 0.0;
+    __syncthreads();
     double acc = 0.0;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < np; i += T) {
@@ -368,7 +370,11 @@ static int gmres_multidot(int64_t n, int j, const double* V, int64_t ld, const d
         if (k <= 4) WK_CGS_LAUNCH(gmres_multidot_vec, 4, n, k, V, ld, w, Hj, skip, rw);
         if (k <= 8) WK_CGS_LAUNCH(gmres_multidot_vec, 8, n, k, V, ld, w, Hj, skip, rw);
         if (k <= 16) WK_CGS_LAUNCH(gmres_multidot_vec, 16, n, k, V, ld, w, Hj, skip, rw);
-        WK_CGS_LAUNCH(gmres_multidot_vec, kRedMaxVec, n, k, V, ld, w, Hj, skip, rw);
+        // k > 16: two passes of 16 vectors (w is read twice, but 32 register
+        // accumulators would leave one block per SM)
+        gmres_multidot_vec<16><<<cgs_grid(n, 16), 256, 0, st>>>(n, 16, V, ld, w, Hj, skip, rw);
+        WK_LAUNCH_CHECK();
+        WK_CGS_LAUNCH(gmres_multidot_vec, 16, n, k - 16, V + 16 * ld, ld, w, Hj + 16, skip, rw);
     }
     if (k <= 8) return gmres_multidot_k<8>(n, k, V, ld, w, Hj, s, ws, st);
     if (k <= 16) return gmres_multidot_k<16>(n, k, V, ld, w, Hj, s, ws, st);
