@@ -217,6 +217,59 @@ def cpu_sample(budget_s=10.0, steps=None):
             "nnz": nnz}, times
 
 
+def cpu_per_config(wk, corpus, D, reps=10):
+    """The reference algorithm on the host cores for the other BASELINE
+    configs (oracle/csrc/oracle.c, all threads, sequential per-row fold): the
+    CPU side of each GPU number in `formats` / `cg`. Bounded samples."""
+    import torch
+
+    from oracle import corpus_ref, native
+
+    threads = native.max_threads()
+    res = {}
+
+    def spmv_rate(prep, x, nnz, label, sample):
+        y = prep.spmv(x, nthreads=threads)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            prep.spmv(x, y, nthreads=threads)
+        ms = (time.perf_counter() - t0) / reps * 1e3
+        res[label] = {"GFLOP/s": round(2 * nnz / (ms * 1e-3) / 1e9, 3), "ms": round(ms, 3), "cores": threads,
+                      "kind": "port", "sample": sample}
+
+    # config 1: CSR 5-point Poisson 1000^2, the whole matrix
+    m = corpus_ref.poisson2d(1000)
+    spmv_rate(native.Prepared(m), np.random.default_rng(42).random(m.ncols), int(m.row_ptrs[-1]),
+              "cfg1_csr_poisson2d_1000", "whole matrix, or_spmv_csr")
+    # config 3: COO R-MAT scale 24, the first 32M sorted entries (the dense rows)
+    R = corpus.rmat(RMAT_SCALE)
+    k = min(R.nnz, 32 << 20)
+    from types import SimpleNamespace
+
+    nrows_s = int(R.row_idx[k - 1].item()) + 1
+    coo = SimpleNamespace(nrows=nrows_s, ncols=R.ncols, row_idx=R.row_idx[:k].cpu().numpy(),
+                          col_idx=R.col_idx[:k].cpu().numpy(), values=R.values[:k].cpu().numpy())
+    del R
+    spmv_rate(native.Prepared(coo), np.random.default_rng(42).random(coo.ncols), k, "cfg3_coo_rmat24_sample",
+              f"first {k} sorted entries (rows 0..{nrows_s - 1}), or_spmv_coo")
+    del coo
+    torch.cuda.empty_cache()
+    # config 4: CG on the 7-point 256^3 Laplacian, SELL-P(64), 20 iterations
+    A = D.csr_to_sellp(corpus.stencil3d(CG_GRID, 7), SLICE)
+    prep = native.Prepared(A.to_host())
+    del A
+    torch.cuda.empty_cache()
+    b = np.ones(prep.nrows)
+    its = 20
+    t0 = time.perf_counter()
+    _, hist = prep.cg(b, 1e-30, its, nthreads=threads)
+    sec = time.perf_counter() - t0
+    res["cfg4_cg_256"] = {"it_per_s": round((len(hist) - 1) / sec, 2), "iterations": len(hist) - 1,
+                          "ms": round(sec * 1e3, 1), "cores": threads, "kind": "port",
+                          "sample": f"{its} iterations of the whole system, or_cg_sellp"}
+    return res
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -360,6 +413,8 @@ def run_gpu(args, rank, world, dist):
         out["nonsymmetric"] = _safe(lambda: bench_nonsym(args, wk, corpus, D))
         torch.cuda.empty_cache()
         line["cpu_baseline"] = cpu_sample(budget_s=args.cpu_budget)[0] if not args.no_cpu else None
+        if not args.no_cpu:
+            out["cpu_baselines"] = _safe(lambda: cpu_per_config(wk, corpus, D))
     elif world > 1 and not args.quick:
         out["cg"] = _safe(lambda: part_cg(args, dist, world))
         torch.cuda.empty_cache()
