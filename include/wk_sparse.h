@@ -412,6 +412,21 @@ int wk_mm_parse_entries(const char* data, int64_t len, const wk_mm_header* heade
 int wk_mm_write(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, const int64_t* cols,
                 const double* vals, char* out, int64_t capacity, int64_t* written);
 
+/* CG steps of the peer-memory distributed path with the two scalar
+ * all-reduces fused into the kernels (peer: device copy of a wk_peer_ctx):
+ * the producers' reduction epilogues store their local p.Ap / r.r into every
+ * rank's arena, the consumers' prologues wait for all P partials and sum them
+ * in rank order. Iteration: spmv_dot_peer -> update_xr_alpha_peer
+ * [-> replace_r_peer every 50th] -> update_p_beta_peer. */
+int wk_cg_spmv_dot_peer(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
+                        void* peer, wk_stream_t stream);
+int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, double* x, double* r,
+                               wk_cg_state* state, void* workspace, void* peer, wk_stream_t stream);
+int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state,
+                         void* workspace, void* peer, wk_stream_t stream);
+int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
+                             void* workspace, void* peer, wk_stream_t stream);
+
 /* ---- peer-memory communication for the row-block distributed solvers
  *      (replaces the NCCL all-reduce / send-recv of distributed.py on GPUs
  *      with peer access; csrc/peer.cu). Arenas are cudaMalloc'd, exported

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "peer_dev.cuh"
 
 namespace wk {
 
@@ -43,6 +44,7 @@ struct DotEpilogue {
     unsigned* ticket;
     wk_cg_state* state;
     int finalize;
+    PeerCtx* peer;      // non-null: push the local p.q to every rank (fused all-reduce)
 };
 
 }  // namespace wk

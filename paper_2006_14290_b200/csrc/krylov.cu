@@ -70,10 +70,14 @@ static int cg_init_finish(wk_cg_state* s, double tol, int64_t max_iters, double*
 }
 
 static int cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* s, void* ws, bool finalize,
-                     cudaStream_t st) {
+                     cudaStream_t st, PeerCtx* peer = nullptr) {
     return launch_map_reduce(
         n, [=] __device__(int64_t i) { return __dmul_rn(__ldcs(p + i), __ldcs(q + i)); },
         [=] __device__(double t) {
+            if (peer != nullptr) {
+                peer_push_scalar(peer, t);
+                return;
+            }
             s->pq = t;
             if (finalize) cg_alpha_step(s);
         },
@@ -83,18 +87,22 @@ static int cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* s
 // q = A p and state->pq = p.q: fused into the SELL-P(64) kernel when
 // possible, else SpMV then a separate reduction.
 static int cg_spmv_dot(const wk_matrix* A, int64_t n, const double* p, double* q, wk_cg_state* s, void* ws,
-                       bool finalize, cudaStream_t st) {
-    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st);
+                       bool finalize, cudaStream_t st, PeerCtx* peer = nullptr) {
+    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st, peer);
     if (rc != 1) return rc;
     WK_TRY(wk_spmv_masked(A, p, q, &s->done, st));
     if (n == 0)
         return launch_scalar([=] __device__() {
             if (!s->done) {
+                if (peer != nullptr) {
+                    peer_push_scalar(peer, 0.0);
+                    return;
+                }
                 s->pq = 0.0;
                 if (finalize) cg_alpha_step(s);
             }
         }, st);
-    return cg_dot_pq(n, p, q, s, ws, finalize, st);
+    return cg_dot_pq(n, p, q, s, ws, finalize, st, peer);
 }
 
 // Vectorised CG vector updates (double2, two independent pairs in flight per
@@ -118,13 +126,15 @@ static int vec_grid(int64_t n) {
 template <bool kAlphaIn>
 __global__ void __launch_bounds__(256)
 cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
-                 double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize) {
+                 double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize,
+                 PeerCtx* peer) {
     if (s->done) return;
     double alpha;
     bool repl, brk = false;
     int64_t it_new = 0;
     if (kAlphaIn) {
-        const double pq = s->pq;
+        // p.Ap: all-reduced by the caller (state->pq), or the peers' pushed partials
+        const double pq = (peer != nullptr) ? peer_wait_sum_block(peer) : s->pq;
         it_new = s->iteration + 1;
         brk = pq <= 0.0;  // kernels.py:317 (NaN falls through)
         alpha = s->rho / pq;
@@ -200,8 +210,12 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
             s->alpha = alpha;
         }
         if (!repl) {
-            s->rr = total;
-            if (finalize) cg_beta_step(s, hist);
+            if (peer != nullptr) {
+                peer_push_scalar(peer, total);
+            } else {
+                s->rr = total;
+                if (finalize) cg_beta_step(s, hist);
+            }
         }
     }
 }
@@ -211,9 +225,11 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
 template <bool kBetaIn>
 __global__ void __launch_bounds__(256)
 cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, wk_cg_state* s, double* hist,
-                RedWorkspace ws) {
+                RedWorkspace ws, PeerCtx* peer) {
     if (s->done) return;
-    const double beta = kBetaIn ? s->rr / s->rho : s->beta;
+    double rr = 0.0;
+    if (kBetaIn) rr = (peer != nullptr) ? peer_wait_sum_block(peer) : s->rr;
+    const double beta = kBetaIn ? rr / s->rho : s->beta;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
@@ -237,14 +253,18 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
     if (kBetaIn) {
         double total;
-        if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) cg_beta_step(s, hist);
+        if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) {
+            s->rr = rr;
+            cg_beta_step(s, hist);
+        }
     }
 }
 
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
                         double* hist, void* ws, bool finalize, cudaStream_t st) {
     if (n > 0 && vec_ok(p, q, x, r)) {
-        cg_update_xr_vec<false><<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0);
+        cg_update_xr_vec<false><<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0,
+                                                            nullptr);
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -267,7 +287,7 @@ static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, 
 }
 
 static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, wk_cg_state* s, double* hist,
-                        void* ws, bool finalize, cudaStream_t st) {
+                        void* ws, bool finalize, cudaStream_t st, PeerCtx* peer = nullptr) {
     return launch_map_reduce(
         n,
         [=] __device__(int64_t i) {
@@ -278,6 +298,10 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
         },
         [=] __device__(double t) {
             if (!cg_replacing(s)) return;
+            if (peer != nullptr) {
+                peer_push_scalar(peer, t);
+                return;
+            }
             s->rr = t;
             if (finalize) cg_beta_step(s, hist);
         },
@@ -287,7 +311,7 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
 static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st) {
     if (n > 0 && vec_ok(r, p, r, p)) {
         cg_update_p_vec<false><<<vec_grid(n), 256, 0, st>>>(n, r, p, const_cast<wk_cg_state*>(s), nullptr,
-                                                          RedWorkspace{nullptr, nullptr});
+                                                          RedWorkspace{nullptr, nullptr}, nullptr);
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -356,7 +380,7 @@ int wk_cg_update_xr_alpha(int64_t n, const double* p, const double* q, double* x
     clear_error();
     WK_REQUIRE(vec_ok(p, q, x, r), WK_ERR_INVALID, "wk_cg_update_xr_alpha needs 16-byte aligned vectors");
     cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, p, q, x, r, state, nullptr,
-                                                                                  red_ws(workspace), 0);
+                                                                                  red_ws(workspace), 0, nullptr);
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -366,7 +390,7 @@ int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* stat
     clear_error();
     WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta needs 16-byte aligned vectors");
     cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, r, p, state, hist,
-                                                                                 red_ws(workspace));
+                                                                                 red_ws(workspace), nullptr);
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -379,6 +403,51 @@ int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream) {
 int wk_cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* state, wk_stream_t stream) {
     clear_error();
     return cg_update_p(n, r, p, state, as_stream(stream));
+}
+
+// ---------------- CG steps with the all-reduces fused (peer-memory path) ---------
+// Each producer's reduction epilogue pushes its local partial to every rank
+// (peer_dev.cuh); the next kernel's prologue waits for the P partials and sums
+// them in rank order. One iteration: spmv_dot (push p.Ap) -> update_xr_alpha
+// (wait p.Ap, alpha, x/r, push r.r) [-> replace_r on replacement iterations]
+// -> update_p_beta (wait r.r, beta, p): no separate all-reduce kernels.
+
+int wk_cg_spmv_dot_peer(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
+                        void* peer, wk_stream_t stream) {
+    clear_error();
+    return cg_spmv_dot(A, A->nrows, p, q, state, workspace, false, as_stream(stream),
+                       reinterpret_cast<PeerCtx*>(peer));
+}
+
+int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, double* x, double* r,
+                               wk_cg_state* state, void* workspace, void* peer, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(vec_ok(p, q, x, r), WK_ERR_INVALID, "wk_cg_update_xr_alpha_peer needs 16-byte aligned vectors");
+    cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
+        n, p, q, x, r, state, nullptr, red_ws(workspace), 0, reinterpret_cast<PeerCtx*>(peer));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state,
+                         void* workspace, void* peer, wk_stream_t stream) {
+    clear_error();
+    PeerCtx* pc = reinterpret_cast<PeerCtx*>(peer);
+    if (n == 0)
+        return launch_scalar([=] __device__() {
+            if (!state->done && cg_replacing(state)) peer_push_scalar(pc, 0.0);
+        }, as_stream(stream));
+    return cg_replace_r(n, b, q, r, state, nullptr, workspace, false, as_stream(stream), pc);
+}
+
+int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
+                             void* workspace, void* peer, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta_peer needs 16-byte aligned vectors");
+    cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
+        n, r, p, state, hist, red_ws(workspace), reinterpret_cast<PeerCtx*>(peer));
+    WK_LAUNCH_CHECK();
+    return 0;
 }
 
 // ---------------- single-GPU CG ---------------------------------------------------

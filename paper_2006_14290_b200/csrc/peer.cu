@@ -21,39 +21,9 @@
 // device-side convergence flags of the solvers then agree, as with NCCL).
 // Spins are bounded (~10 s): on timeout the kernel sets an error word
 // instead of hanging the GPU.
-#include "common.cuh"
+#include "peer_dev.cuh"
 
 namespace wk {
-
-constexpr int kPeerMax = 64;
-constexpr int kPeerSlots = 32;
-constexpr int64_t kArFlags = 0, kHaloFlags = 512, kSlots = 1024, kArenaHeader = 1024 + 2 * kPeerMax * kPeerSlots * 8;
-
-struct PeerCtx {
-    int rank, world;
-    char* arena[kPeerMax];  // every rank's arena, mapped into this process (own included)
-    long long* seq;         // device: [0] all-reduce seq, [1] halo seq
-    int* error;             // device: set on a wait timeout
-};
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// wait until flag >= seq (bounded); returns false on timeout
-__device__ __forceinline__ bool wait_flag(const unsigned long long* flag, unsigned long long seq) {
-    for (long long it = 0; it < (1ll << 27); ++it) {
-        if (ld_acquire_sys(flag) >= seq) return true;
-        __nanosleep(64);
-    }
-    return false;
-}
 
 __global__ void peer_allreduce_kernel(PeerCtx ctx, const double* __restrict__ src, double* __restrict__ dst,
                                       int count) {
@@ -78,7 +48,7 @@ __global__ void peer_allreduce_kernel(PeerCtx ctx, const double* __restrict__ sr
     const double* slots = reinterpret_cast<const double*>(ctx.arena[ctx.rank] + kSlots) + par * kPeerMax * kPeerSlots;
     for (int i = 0; i < count; ++i) {
         double acc = 0.0;
-        for (int q = 0; q < ctx.world; ++q) acc = __dadd_rn(acc, slots[q * kPeerSlots + i]);
+        for (int q = 0; q < ctx.world; ++q) acc = __dadd_rn(acc, __ldcv(slots + q * kPeerSlots + i));
         dst[i] = acc;
     }
     ctx.seq[0] = (long long)seq;

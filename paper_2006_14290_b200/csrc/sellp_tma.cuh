@@ -181,8 +181,12 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         RedWorkspace ws{dot.partials, dot.ticket};
         double total;
         if (grid_reduce_last<WARPS * 32>(dacc, ws, total) && threadIdx.x == 0) {
-            dot.state->pq = total;
-            if (dot.finalize) cg_alpha_step(dot.state);
+            if (dot.peer != nullptr) {
+                peer_push_scalar(dot.peer, total);  // consumed by the next kernel's prologue
+            } else {
+                dot.state->pq = total;
+                if (dot.finalize) cg_alpha_step(dot.state);
+            }
         }
     }
 }
@@ -192,7 +196,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
 template <class Cfg, bool kDot = false, bool kEll = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
-                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0}, int64_t ell_width = 0,
+                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr}, int64_t ell_width = 0,
                        int64_t ell_stride = 0) {
     static bool attr_set[64] = {false};
     int dev = 0;

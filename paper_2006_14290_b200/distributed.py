@@ -500,7 +500,7 @@ _RHO, _PQ, _RR = 0, 1, 2  # float64 slots of wk_cg_state
 REPLACE_EVERY = 50  # kernels.py:322, kReplaceEvery in krylov.cu
 
 
-def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
+def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None, fused=True):
     """Row-block distributed CG with the reference's update order
     (kernels.py:283-331), all scalars on the device. Returns (x_local, hist)
     (device tensors). Iteration control is identical on all ranks because
@@ -544,6 +544,23 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None):
                 ops.cg("wk_cg_replace_r", n, b, q, r, st)
             comm.allreduce_(f64[_RR:_RR + 1])
             ops.cg("wk_cg_update_p_beta", n, r, p, st, hist)
+
+    def period_fused():
+        """The same period on the peer-memory path with both all-reduces fused
+        into the kernels (producer epilogue push, consumer prologue wait)."""
+        pc = op.peer.ctx_dev
+        for j in range(1, REPLACE_EVERY + 1):
+            op.exchange(p)
+            ops.step("wk_cg_spmv_dot_peer", op.local.wk_ptr(), p, q, st, ops.ws.red, pc)
+            ops.step("wk_cg_update_xr_alpha_peer", n, p, q, x, r, st, ops.ws.red, pc)
+            if j == REPLACE_EVERY:
+                op.exchange(x)
+                ops.spmv_masked(op.local, x, q, st)
+                ops.step("wk_cg_replace_r_peer", n, b, q, r, st, ops.ws.red, pc)
+            ops.step("wk_cg_update_p_beta_peer", n, r, p, st, hist, ops.ws.red, pc)
+
+    if op.peer is not None and fused:
+        period = period_fused  # noqa: F811
 
     if graph is None:
         graph = (comm.backend == "nccl" or comm.peer is not None) and os.environ.get("WK_DIST_GRAPH", "1") != "0"

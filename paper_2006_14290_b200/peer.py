@@ -119,6 +119,8 @@ class PeerComm:
             self.ctx.arena[q] = a
         self.ctx.seq = self.seq.data_ptr()
         self.ctx.error = self.error.data_ptr()
+        # device copy of the context for the fused kernels (wk_cg_*_peer)
+        self.ctx_dev = torch.frombuffer(bytearray(bytes(self.ctx)), dtype=torch.uint8).to(self.device)
         self._top = self.header
         self._keep = []
 

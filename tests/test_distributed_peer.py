@@ -55,8 +55,10 @@ def _worker(rank, world, port, out):
                                        nz=12).enable_peer()
         b = torch.ones(opg.n_local, dtype=torch.float64, device="cuda")
         for graph in (False, True):
-            xs, hist = DI.cg_solve(opg, b, 1e-12, 500, graph=graph)
+            xs, hist = DI.cg_solve(opg, b, 1e-12, 500, graph=graph)  # all-reduces fused into the CG kernels
             res[f"cg_x_{graph}"], res[f"cg_hist_{graph}"] = xs.cpu().numpy(), hist.cpu().numpy()
+        xs, hist = DI.cg_solve(opg, b, 1e-12, 500, graph=True, fused=False)  # separate all-reduce kernels
+        res["cg_x_unfused"], res["cg_hist_unfused"] = xs.cpu().numpy(), hist.cpu().numpy()
         res["err1"] = int(opg.peer.error.item())
 
         opn = DI.stencil_slab_operator(10, 10, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist,
@@ -120,6 +122,10 @@ def test_peer_cg_graph(parts):
         x = np.concatenate([p[f"cg_x_{graph}"] for p in parts])
         assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
     assert np.array_equal(parts[0]["cg_hist_True"], parts[0]["cg_hist_False"])
+    # fused (epilogue push / prologue wait) and separate all-reduce kernels: same sums, same bits
+    for p in parts:
+        assert np.array_equal(p["cg_hist_unfused"], p["cg_hist_True"])
+        assert np.array_equal(p["cg_x_unfused"], p["cg_x_True"])
 
 
 @pytest.mark.parametrize("solver", ["bicg", "gmres"])
