@@ -417,15 +417,27 @@ int wk_mm_write(int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rows, 
  * the producers' reduction epilogues store their local p.Ap / r.r into every
  * rank's arena, the consumers' prologues wait for all P partials and sum them
  * in rank order. Iteration: spmv_dot_peer -> update_xr_alpha_peer
- * [-> replace_r_peer every 50th] -> update_p_beta_peer. */
+ * [-> replace_r_peer every 50th] -> update_p_beta_peer. With `halo`
+ * (device wk_peer_halo, may be NULL) update_p_beta_peer also stores the new
+ * p's boundary rows into the neighbours' copies of p and releases their halo
+ * flags, and spmv_dot_peer waits for the incoming halo before its gathers: no
+ * exchange kernel either. */
+typedef struct wk_peer_halo {
+    int32_t n;                  /* sends (<= 8)                                     */
+    int32_t peer[8];
+    int64_t lo[8], hi[8];       /* owned rows [lo, hi) go to peer ...               */
+    int64_t dst_off[8];         /* ... at this byte offset of its arena             */
+    int32_t nrecv;
+    int32_t recv_peer[8];
+} wk_peer_halo;
 int wk_cg_spmv_dot_peer(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
-                        void* peer, wk_stream_t stream);
+                        void* peer, const void* halo, wk_stream_t stream);
 int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, double* x, double* r,
                                wk_cg_state* state, void* workspace, void* peer, wk_stream_t stream);
 int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state,
                          void* workspace, void* peer, wk_stream_t stream);
 int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
-                             void* workspace, void* peer, wk_stream_t stream);
+                             void* workspace, void* peer, const void* halo, wk_stream_t stream);
 
 /* ---- peer-memory communication for the row-block distributed solvers
  *      (replaces the NCCL all-reduce / send-recv of distributed.py on GPUs

@@ -49,6 +49,13 @@ class WkPeerCtx(ctypes.Structure):
     _fields_ = [("rank", I32), ("world", I32), ("arena", P * WK_PEER_MAX), ("seq", P), ("error", P)]
 
 
+class WkPeerHalo(ctypes.Structure):
+    """Mirror of `wk_peer_halo` (include/wk_sparse.h)."""
+
+    _fields_ = [("n", I32), ("peer", I32 * 8), ("lo", I64 * 8), ("hi", I64 * 8), ("dst_off", I64 * 8),
+                ("nrecv", I32), ("recv_peer", I32 * 8)]
+
+
 class WkMatrix(ctypes.Structure):
     """Mirror of `wk_matrix` (include/wk_sparse.h)."""
 
@@ -107,10 +114,10 @@ _SIGS = {
     "wk_sym_close": (ctypes.c_int, [P]),
     "wk_sym_free": (ctypes.c_int, [P]),
     "wk_peer_arena_header_bytes": (I64, []),
-    "wk_cg_spmv_dot_peer": (ctypes.c_int, [P, P, P, P, P, P, P]),
+    "wk_cg_spmv_dot_peer": (ctypes.c_int, [P, P, P, P, P, P, P, P]),
     "wk_cg_update_xr_alpha_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
     "wk_cg_replace_r_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
-    "wk_cg_update_p_beta_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
+    "wk_cg_update_p_beta_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
     "wk_peer_allreduce": (ctypes.c_int, [P, P, P, I32, P]),
     "wk_peer_exchange": (ctypes.c_int, [P, P, I32, P, P, P, P, I32, P, P, P]),
     "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),

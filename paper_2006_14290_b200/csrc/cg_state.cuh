@@ -45,6 +45,7 @@ struct DotEpilogue {
     wk_cg_state* state;
     int finalize;
     PeerCtx* peer;      // non-null: push the local p.q to every rank (fused all-reduce)
+    const PeerHalo* halo;  // non-null: wait for the pushed halo of x before the first gather
 };
 
 }  // namespace wk

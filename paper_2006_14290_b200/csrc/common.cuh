@@ -71,7 +71,7 @@ int set_seg8_kernel(int choice);
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
-                   cudaStream_t st, void* peer = nullptr);
+                   cudaStream_t st, void* peer = nullptr, const void* halo = nullptr);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

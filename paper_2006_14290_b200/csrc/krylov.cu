@@ -86,10 +86,19 @@ static int cg_dot_pq(int64_t n, const double* p, const double* q, wk_cg_state* s
 
 // q = A p and state->pq = p.q: fused into the SELL-P(64) kernel when
 // possible, else SpMV then a separate reduction.
+__global__ void halo_wait_kernel(const PeerCtx* c, const PeerHalo* h, const int* skip) {
+    if (*skip) return;
+    halo_wait(c, h);
+}
+
 static int cg_spmv_dot(const wk_matrix* A, int64_t n, const double* p, double* q, wk_cg_state* s, void* ws,
-                       bool finalize, cudaStream_t st, PeerCtx* peer = nullptr) {
-    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st, peer);
+                       bool finalize, cudaStream_t st, PeerCtx* peer = nullptr, const PeerHalo* halo = nullptr) {
+    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st, peer, halo);
     if (rc != 1) return rc;
+    if (halo != nullptr) {  // other formats: a separate wait before the SpMV
+        halo_wait_kernel<<<1, 32, 0, st>>>(peer, halo, &s->done);
+        WK_LAUNCH_CHECK();
+    }
     WK_TRY(wk_spmv_masked(A, p, q, &s->done, st));
     if (n == 0)
         return launch_scalar([=] __device__() {
@@ -225,7 +234,7 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
 template <bool kBetaIn>
 __global__ void __launch_bounds__(256)
 cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, wk_cg_state* s, double* hist,
-                RedWorkspace ws, PeerCtx* peer) {
+                RedWorkspace ws, PeerCtx* peer, const PeerHalo* halo) {
     if (s->done) return;
     double rr = 0.0;
     if (kBetaIn) rr = (peer != nullptr) ? peer_wait_sum_block(peer) : s->rr;
@@ -244,18 +253,34 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
         pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
         pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
         p2[k] = pa;
+        if (halo != nullptr) {  // the boundary rows go straight into the neighbours' halo copies
+            halo_store(peer, halo, 2 * k, pa.x);
+            halo_store(peer, halo, 2 * k + 1, pa.y);
+        }
         if (h1) {
             pb.x = __dadd_rn(rb.x, __dmul_rn(beta, pb.x));
             pb.y = __dadd_rn(rb.y, __dmul_rn(beta, pb.y));
             p2[k1] = pb;
+            if (halo != nullptr) {
+                halo_store(peer, halo, 2 * k1, pb.x);
+                halo_store(peer, halo, 2 * k1 + 1, pb.y);
+            }
         }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
+        if (halo != nullptr) halo_store(peer, halo, n - 1, p[n - 1]);
+    }
+    if (halo != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) __threadfence_system();  // this block's peer stores, before its ticket
+    }
     if (kBetaIn) {
         double total;
         if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) {
             s->rr = rr;
             cg_beta_step(s, hist);
+            if (halo != nullptr) halo_release(peer, halo);
         }
     }
 }
@@ -311,7 +336,7 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
 static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st) {
     if (n > 0 && vec_ok(r, p, r, p)) {
         cg_update_p_vec<false><<<vec_grid(n), 256, 0, st>>>(n, r, p, const_cast<wk_cg_state*>(s), nullptr,
-                                                          RedWorkspace{nullptr, nullptr}, nullptr);
+                                                          RedWorkspace{nullptr, nullptr}, nullptr, nullptr);
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -390,7 +415,7 @@ int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* stat
     clear_error();
     WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta needs 16-byte aligned vectors");
     cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, r, p, state, hist,
-                                                                                 red_ws(workspace), nullptr);
+                                                                                 red_ws(workspace), nullptr, nullptr);
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -413,10 +438,10 @@ int wk_cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* sta
 // -> update_p_beta (wait r.r, beta, p): no separate all-reduce kernels.
 
 int wk_cg_spmv_dot_peer(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
-                        void* peer, wk_stream_t stream) {
+                        void* peer, const void* halo, wk_stream_t stream) {
     clear_error();
     return cg_spmv_dot(A, A->nrows, p, q, state, workspace, false, as_stream(stream),
-                       reinterpret_cast<PeerCtx*>(peer));
+                       reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo));
 }
 
 int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, double* x, double* r,
@@ -441,11 +466,12 @@ int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r,
 }
 
 int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
-                             void* workspace, void* peer, wk_stream_t stream) {
+                             void* workspace, void* peer, const void* halo, wk_stream_t stream) {
     clear_error();
     WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta_peer needs 16-byte aligned vectors");
     cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
-        n, r, p, state, hist, red_ws(workspace), reinterpret_cast<PeerCtx*>(peer));
+        n, r, p, state, hist, red_ws(workspace), reinterpret_cast<PeerCtx*>(peer),
+        reinterpret_cast<const PeerHalo*>(halo));
     WK_LAUNCH_CHECK();
     return 0;
 }

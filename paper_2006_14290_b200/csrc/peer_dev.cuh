@@ -75,4 +75,42 @@ __device__ __forceinline__ double peer_wait_sum_block(const PeerCtx* c) {
     return g;
 }
 
+// Halo of one distributed vector pushed by the kernel that produces it:
+// owned rows [lo_j, hi_j) go to rank peer_j at byte offset dst_off_j of its
+// arena (the receiver's copy of the vector); the receiving kernel waits for
+// the flags of recv_peer[] (slab partitions: contiguous boundary planes).
+constexpr int kHaloMax = 8;
+struct PeerHalo {
+    int n;
+    int peer[kHaloMax];
+    long long lo[kHaloMax], hi[kHaloMax];
+    long long dst_off[kHaloMax];
+    int nrecv;
+    int recv_peer[kHaloMax];
+};
+
+__device__ __forceinline__ void halo_store(const PeerCtx* c, const PeerHalo* h, long long i, double v) {
+    for (int j = 0; j < h->n; ++j)
+        if (i >= h->lo[j] && i < h->hi[j])
+            reinterpret_cast<double*>(c->arena[h->peer[j]] + h->dst_off[j])[i - h->lo[j]] = v;
+}
+
+// last block, thread 0, after every block's system fence: release the halo
+// flags at the receivers (seq[1] advances)
+__device__ __forceinline__ void halo_release(PeerCtx* c, const PeerHalo* h) {
+    const unsigned long long seq = (unsigned long long)c->seq[1] + 1ull;
+    __threadfence_system();
+    for (int j = 0; j < h->n; ++j)
+        st_release_sys(reinterpret_cast<unsigned long long*>(c->arena[h->peer[j]] + kHaloFlags) + c->rank, seq);
+    c->seq[1] = (long long)seq;
+}
+
+// consumer (thread 0): the halos pushed under the current seq[1] have landed
+__device__ __forceinline__ void halo_wait(const PeerCtx* c, const PeerHalo* h) {
+    const unsigned long long seq = (unsigned long long)c->seq[1];
+    const unsigned long long* flags = reinterpret_cast<const unsigned long long*>(c->arena[c->rank] + kHaloFlags);
+    for (int j = 0; j < h->nrecv; ++j)
+        if (!wait_flag(flags + h->recv_peer[j], seq)) *c->error = 2;
+}
+
 }  // namespace wk

@@ -133,6 +133,12 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     };
     seek();
     for (int st = 0; st < S && pvalid; ++st) issue(st);
+    if (kDot && dot.halo != nullptr) {
+        // the matrix stream is already in flight; the x gathers wait for the
+        // neighbours' halo stores (peer-memory distributed CG)
+        if (threadIdx.x == 0) halo_wait(dot.peer, dot.halo);
+        __syncthreads();
+    }
 
     uint32_t i = 0;  // chunks consumed by this warp
     double dacc = 0.0;
@@ -196,7 +202,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
 template <class Cfg, bool kDot = false, bool kEll = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
-                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr}, int64_t ell_width = 0,
+                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int64_t ell_width = 0,
                        int64_t ell_stride = 0) {
     static bool attr_set[64] = {false};
     int dev = 0;

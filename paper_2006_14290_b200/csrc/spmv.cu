@@ -273,14 +273,14 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
 // Returns 1 when the operand cannot take the fused path (caller falls back to
 // SpMV + separate dot), 0 on success, an error code otherwise.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
-                   cudaStream_t st, void* peer) {
+                   cudaStream_t st, void* peer, const void* halo) {
     if (A->format != WK_FMT_SELLP || A->slice_size != 64 || sellp_kernel_choice() == 0 || !aligned(A->values, 16) ||
         !aligned(A->col_idx, 16) || !aligned(q, 16) || !aligned(p, 16) || A->nrows == 0)
         return 1;
     char* w = reinterpret_cast<char*>(red_ws);
     DotEpilogue dot{reinterpret_cast<double*>(w),
                     reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
-                    reinterpret_cast<PeerCtx*>(peer)};
+                    reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo)};
     return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
                                                              A->values, A->row_lengths, p, q, &s->done, st, dot);
 }
@@ -297,7 +297,7 @@ int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
     if (ell_kernel_choice() == 1 && stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16) &&
         width > 0)
         return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, false, true>(
-            nrows, ncols, nullptr, col, val, row_lengths, x, y, skip, st, DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr},
+            nrows, ncols, nullptr, col, val, row_lengths, x, y, skip, st, DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr},
             width, stride);
     const bool vec = (stride % 2 == 0) && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {

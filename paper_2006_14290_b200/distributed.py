@@ -296,6 +296,31 @@ class DistOperator:
             return self.peer.vector(self.n_local + self.n_halo, self.n_ext_max)
         return self.ops.zeros(self.n_local + self.n_halo)
 
+    def peer_halo(self, vec):
+        """Device `wk_peer_halo` for pushing `vec`'s boundary rows from the
+        kernel that writes them, or None when a send set is not a contiguous
+        row range (then the exchange kernel runs instead)."""
+        if self.peer is None or len(self._send_idx) > 8 or len(self._peer_recv) > 8:
+            return None
+        off = self.peer.offset_of(vec)
+        if off is None:
+            return None
+        h = _lib.WkPeerHalo()
+        h.n = len(self._send_idx)
+        for j, (q, idx_h) in enumerate(sorted(self.plan.send_idx.items())):
+            idx_h = np.asarray(idx_h, dtype=np.int64)
+            lo = int(idx_h[0]) if len(idx_h) else 0
+            if len(idx_h) and not np.array_equal(idx_h, np.arange(lo, lo + len(idx_h))):
+                return None
+            h.peer[j], h.lo[j], h.hi[j] = q, lo, lo + len(idx_h)
+            h.dst_off[j] = off + 8 * self._peer_dst[q]
+        h.nrecv = len(self._peer_recv)
+        for j, q in enumerate(self._peer_recv):
+            h.recv_peer[j] = q
+        t = torch.frombuffer(bytearray(bytes(h)), dtype=torch.uint8).to(self.ops.device)
+        self._halo_keep = getattr(self, "_halo_keep", []) + [t]
+        return t
+
     def arena_mark(self):
         """Allocation mark of the peer arena (None without the peer path)."""
         return None if self.peer is None else self.peer.mark()
@@ -545,22 +570,30 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None, fused=True):
             comm.allreduce_(f64[_RR:_RR + 1])
             ops.cg("wk_cg_update_p_beta", n, r, p, st, hist)
 
+    halo = op.peer_halo(p) if (op.peer is not None and fused) else None
+
     def period_fused():
         """The same period on the peer-memory path with both all-reduces fused
-        into the kernels (producer epilogue push, consumer prologue wait)."""
+        into the kernels (producer epilogue push, consumer prologue wait) and,
+        for contiguous boundary rows (slabs), the halo of p stored by the
+        p-update kernel itself and awaited by the SpMV: one iteration is
+        three kernels and no communication kernel."""
         pc = op.peer.ctx_dev
         for j in range(1, REPLACE_EVERY + 1):
-            op.exchange(p)
-            ops.step("wk_cg_spmv_dot_peer", op.local.wk_ptr(), p, q, st, ops.ws.red, pc)
+            if halo is None:
+                op.exchange(p)
+            ops.step("wk_cg_spmv_dot_peer", op.local.wk_ptr(), p, q, st, ops.ws.red, pc, halo)
             ops.step("wk_cg_update_xr_alpha_peer", n, p, q, x, r, st, ops.ws.red, pc)
             if j == REPLACE_EVERY:
                 op.exchange(x)
                 ops.spmv_masked(op.local, x, q, st)
                 ops.step("wk_cg_replace_r_peer", n, b, q, r, st, ops.ws.red, pc)
-            ops.step("wk_cg_update_p_beta_peer", n, r, p, st, hist, ops.ws.red, pc)
+            ops.step("wk_cg_update_p_beta_peer", n, r, p, st, hist, ops.ws.red, pc, halo)
 
     if op.peer is not None and fused:
         period = period_fused  # noqa: F811
+        if halo is not None:
+            op.exchange(p)  # iteration 1's halo (later ones come from the p-update kernel)
 
     if graph is None:
         graph = (comm.backend == "nccl" or comm.peer is not None) and os.environ.get("WK_DIST_GRAPH", "1") != "0"
