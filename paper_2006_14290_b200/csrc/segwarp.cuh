@@ -368,7 +368,7 @@ __device__ __forceinline__ void seg8_fold(int lane, int nv, bool last_window, co
 }
 
 template <bool kCsr>
-__global__ void __launch_bounds__(kS8Warps * 32)
+__global__ void __launch_bounds__(kS8Warps * 32, kCsr ? 3 : 4)
 seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
             const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
             const int* __restrict__ skip, HeadPlan hp) {
