@@ -150,3 +150,52 @@ def test_peer_nonsymmetric(parts, solver):
     assert np.max(np.abs(h0 - hr)) / np.linalg.norm(b) <= 1e-10
     x = np.concatenate([p[f"{solver}_x"] for p in parts])
     assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
+
+
+def _worker3(rank, world, port, out):
+    """Three ranks: the middle one sends / receives two halos (both planes)."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2006_14290_b200 import corpus
+        from paper_2006_14290_b200 import distributed as DI
+
+        res = {}
+        opg = DI.stencil_slab_operator(9, 9, None, corpus.points_7pt(), dist, fmt="sellp", weak=False,
+                                       nz=12).enable_peer()
+        b = torch.ones(opg.n_local, dtype=torch.float64, device="cuda")
+        xs, hist = DI.cg_solve(opg, b, 1e-12, 500)  # fused all-reduces + fused halo push, graph
+        res["x"], res["hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        xs, hist = DI.cg_solve(opg, b, 1e-12, 500, fused=False)  # exchange + all-reduce kernels
+        res["x_unfused"], res["hist_unfused"] = xs.cpu().numpy(), hist.cpu().numpy()
+        res["err"] = int(opg.peer.error.item())
+        opg.peer.close()
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_cg_three_ranks():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+
+    mgr = mp.get_context("spawn").Manager()
+    out = mgr.dict()
+    mp.spawn(_worker3, args=(3, _free_port(), out), nprocs=3, join=True)
+    parts = [out[0], out[1], out[2]]
+    m = corpus_ref.stencil(9, 9, 12, corpus_ref.points_7pt())
+    sp = sparse_ref.csr_to_sellp(m, 64)
+    b = np.ones(m.nrows)
+    xr, hr = krylov_ref.cg_solve(lambda v: sparse_ref.spmv(sp, v), b, 1e-12, 500)
+    for p in parts:
+        assert p["err"] == 0
+        assert np.array_equal(p["hist"], parts[0]["hist"])
+        assert np.array_equal(p["hist"], p["hist_unfused"]) and np.array_equal(p["x"], p["x_unfused"])
+    assert len(parts[0]["hist"]) == len(hr)
+    assert np.max(np.abs(parts[0]["hist"] - hr)) / np.linalg.norm(b) <= 1e-10
+    x = np.concatenate([p["x"] for p in parts])
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(m)) <= 1e-10
