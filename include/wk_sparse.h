@@ -59,9 +59,11 @@ enum { WK_FMT_CSR = 0, WK_FMT_COO = 1, WK_FMT_ELL = 2, WK_FMT_SELLP = 3, WK_FMT_
  * tiles of 2048 (row end | nonzero) items per CTA, equal work whatever the
  * row-length skew (rows inside one thread's 8 items fold bitwise, others are
  * joined by deterministic segmented scans); LOAD_BALANCE = Ginkgo's
- * load_balance: 1024 nonzeros per warp, warp segmented scans with row ids
- * expanded from row_ptrs on the fly, atomics for the rows shared between
- * warps (the fastest for skewed matrices; not deterministic in the last bits). */
+ * load_balance: 2048 nonzeros per warp, warp segmented scans with row ids
+ * from a head plan (wk_csr_load_balance_plan_*), the partial sum of a row
+ * continuing past a warp's range kept as that range's carry and added in
+ * range order by a fix-up kernel (the fastest for skewed matrices;
+ * deterministic, no atomics). */
 enum { WK_CSR_STREAM = 0, WK_CSR_SUBWARP = 1, WK_CSR_ROWBLOCK = 2, WK_CSR_MERGE = 3, WK_CSR_LOAD_BALANCE = 4 };
 
 const char* wk_last_error(void);

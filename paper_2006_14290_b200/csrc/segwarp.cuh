@@ -164,6 +164,8 @@ struct HeadPlan {
     const int* hoff;
     const unsigned* mask;
     const int* hrow;
+    int* crow;       // per warp range: the row continuing past the range (-1: none) ...
+    double* cval;    // ... and the range's part of it (added in range order by the fix-up)
 };
 
 struct HeadPlanMut {
@@ -171,11 +173,14 @@ struct HeadPlanMut {
     unsigned* mask;
     int* hrow;
     void* scan_ws;
+    int* crow;
+    double* cval;
 };
 
 inline int64_t head_plan_bytes(int64_t nrows, int64_t nnz) {
-    const int64_t w = seg8_windows(nnz);
-    return ceil_div((w + 1) * 4, 256) * 256 + w * 32 + ceil_div(nrows * 4, 256) * 256 + scan_ws_bytes(w) + 256;
+    const int64_t w = seg8_windows(nnz), g = seg8_warps(nnz);
+    return ceil_div((w + 1) * 4, 256) * 256 + w * 32 + ceil_div(nrows * 4, 256) * 256 + ceil_div(scan_ws_bytes(w), 256) * 256 +
+           ceil_div(g * 4, 256) * 256 + g * 8 + 256;
 }
 
 inline HeadPlanMut head_plan_views(void* plan, int64_t nrows, int64_t nnz) {
@@ -189,6 +194,10 @@ inline HeadPlanMut head_plan_views(void* plan, int64_t nrows, int64_t nnz) {
     h.hrow = reinterpret_cast<int*>(p);
     p += ceil_div(nrows * 4, 256) * 256;
     h.scan_ws = p;
+    p += ceil_div(scan_ws_bytes(w), 256) * 256;
+    h.crow = reinterpret_cast<int*>(p);
+    p += ceil_div(seg8_warps(nnz) * 4, 256) * 256;
+    h.cval = reinterpret_cast<double*>(p);
     return h;
 }
 
@@ -245,6 +254,10 @@ __device__ __forceinline__ int head_row_of(const HeadPlan& hp, int64_t e) {
     for (int q = 0; q < (pos >> 5); ++q) k += __popc(__ldg(hp.mask + w * 8 + q));
     k += __popc(__ldg(hp.mask + w * 8 + (pos >> 5)) & (0xffffffffu >> (31 - (pos & 31))));
     return __ldg(hp.hrow + k - 1);
+}
+
+__device__ __forceinline__ bool head_at(const HeadPlan& hp, int64_t e) {
+    return (__ldg(hp.mask + (e >> 5)) >> (e & 31)) & 1u;
 }
 
 // warp range [wlo, whi): its boundary rows and the head plan of its 8 windows
@@ -386,11 +399,24 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
         first_row = __ldg(rows + wlo);
         last_row = __ldg(rows + whi - 1);
     }
+    // CSR: deterministic. Every row is stored by the range that closes it; a
+    // row continuing past the range end leaves its part in the range's carry
+    // slot, added in range order by seg8_fixup_kernel (no atomics). COO
+    // (kernels.py:229-253 semantics): atomics for the two rows a range can
+    // share with its neighbours.
+    const bool carries = kCsr && whi < nnz && !head_at(hp, whi);
+    if (kCsr && lane == 0) hp.crow[warp] = carries ? last_row : -1;
     auto emit = [&](int r, double v) {
-        if (r == first_row || r == last_row)
+        if (kCsr) {
+            if (carries && r == last_row)
+                hp.cval[warp] = v;
+            else
+                y[r] = v;
+        } else if (r == first_row || r == last_row) {
             atomicAdd(y + r, v);
-        else
+        } else {
             y[r] = accumulate ? __dadd_rn(y[r], v) : v;
+        }
     };
     int carry_row = -1;
     double carry = 0.0;
@@ -432,6 +458,21 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
         if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
         seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
     }
+}
+
+// rows cut by warp-range boundaries (CSR): the first range of each run of
+// equal carry rows adds the run's parts, in range order, in front of the part
+// stored by the range that closed the row
+__global__ void seg8_fixup_kernel(int64_t nranges, const int* __restrict__ crow, const double* __restrict__ cval,
+                                  double* __restrict__ y, const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= nranges) return;
+    const int r = crow[g];
+    if (r < 0 || (g > 0 && crow[g - 1] == r)) return;
+    double s = cval[g];
+    for (int64_t u = g + 1; u < nranges && crow[u] == r; ++u) s = __dadd_rn(s, cval[u]);
+    y[r] = __dadd_rn(s, y[r]);
 }
 
 // ---- TMA-staged variant -------------------------------------------------------
@@ -508,11 +549,19 @@ seg8_tma_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const
             first_row = __ldg(rows + wlo);
             last_row = __ldg(rows + whi - 1);
         }
+        const bool carries = kCsr && whi < nnz && !head_at(hp, whi);
+        if (kCsr && lane == 0) hp.crow[g] = carries ? last_row : -1;
         auto emit = [&](int r, double v) {
-            if (r == first_row || r == last_row)
+            if (kCsr) {
+                if (carries && r == last_row)
+                    hp.cval[g] = v;
+                else
+                    y[r] = v;
+            } else if (r == first_row || r == last_row) {
                 atomicAdd(y + r, v);
-            else
+            } else {
                 y[r] = accumulate ? __dadd_rn(y[r], v) : v;
+            }
         };
         int carry_row = -1;
         double carry = 0.0;
@@ -596,19 +645,29 @@ int launch_seg8_tma(int64_t nnz, int accumulate, const int* rows, const int* col
 // The TMA path needs 16-byte aligned arrays.
 inline int launch_seg8(bool csr, int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
                        const double* x, double* y, const int* skip, cudaStream_t st,
-                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr}) {
+                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr}) {
     if (nnz == 0) return 0;
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     if (seg8_kernel_choice() == 1 && al(col) && al(val) && (csr || al(rows))) {
-        if (csr) return launch_seg8_tma<true>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
-        return launch_seg8_tma<false>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
+        if (csr) {
+            WK_TRY(launch_seg8_tma<true>(nnz, accumulate, rows, col, val, x, y, skip, st, hp));
+        } else {
+            return launch_seg8_tma<false>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
+        }
+    } else {
+        const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
+        if (csr)
+            seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
+        else
+            seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
+        WK_LAUNCH_CHECK();
+        if (!csr) return 0;
     }
-    const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
-    if (csr)
-        seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
-    else
-        seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
-    WK_LAUNCH_CHECK();
+    const int64_t nranges = seg8_warps(nnz);
+    if (nranges > 1) {
+        seg8_fixup_kernel<<<(unsigned)ceil_div(nranges, 256), 256, 0, st>>>(nranges, hp.crow, hp.cval, y, skip);
+        WK_LAUNCH_CHECK();
+    }
     return 0;
 }
 

@@ -163,7 +163,8 @@ class DeviceCsr(DeviceMatrix):
         folds one row from a TMA-staged block; bitwise), load_balance
         otherwise (Ginkgo's choice for irregular matrices: equal nonzeros per
         warp whatever the row-length skew). Decided once per matrix (one D2H
-        read). `merge` (deterministic) and `stream` (bitwise) are explicit
+        read); deterministic (range carries added in range order, no
+        atomics). `merge` (deterministic) and `stream` (bitwise) are explicit
         choices."""
         if getattr(self, "_auto", None) is None:
             if self.nrows == 0:

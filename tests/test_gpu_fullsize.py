@@ -120,7 +120,9 @@ def test_cfg3_rmat24_coo_csr_hybrid(wk):
     scale = lens_d.to(torch.float64).clamp(min=1) * yc.abs().clamp(min=1)
     for strat in ("load_balance", "merge"):
         C.with_strategy(strat)
-        assert ((_spmv(C, x) - yc).abs() / scale).max().item() <= TOL, strat
+        z = _spmv(C, x)
+        assert ((z - yc).abs() / scale).max().item() <= TOL, strat
+        assert torch.equal(_spmv(C, x), z), strat  # deterministic at 16.7M rows / 268M entries
     del C
     H = D.csr_to_hybrid(D.coo_to_csr(R), width=4)
     assert ((_spmv(H, x) - yc).abs() / scale).max().item() <= TOL

@@ -71,7 +71,9 @@ CSR_BITWISE_ROW = {"stream": 256, "rowblock": 64}  # rows up to this length fold
 def test_csr_golden(wk, case, strategy):
     """stream / rowblock fold short rows bitwise; merge (merge-path tiles)
     reassociates rows cut by thread boundaries: 1e-12 scaled, exact on
-    integer data, deterministic. auto resolves to rowblock or merge."""
+    integer data; load_balance (seg8 warp ranges) adds the partial sums of a
+    row cut by range boundaries in range order. Both are deterministic. auto
+    resolves to rowblock or load_balance."""
     from paper_2006_14290_b200 import device as D
 
     e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
@@ -85,7 +87,7 @@ def test_csr_golden(wk, case, strategy):
     if resolved in CSR_BITWISE_ROW:
         short = lens <= CSR_BITWISE_ROW[resolved]
         assert y[short].tobytes() == case.y[short].tobytes()
-    elif resolved == "merge":
+    elif resolved in ("merge", "load_balance"):
         assert wk.spmv_csr(m, case.x, e).tobytes() == y.tobytes()  # deterministic
 
 
@@ -347,7 +349,7 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
     """merge-path and load-balance CSR: rows spanning many tiles / warp
     ranges, long runs of empty rows crossing them, rows ending exactly on tile /
     thread boundaries, empty matrices; tolerance 1e-12, exact on integer data;
-    merge is deterministic."""
+    both are deterministic."""
     ncols = 70000
     if shape == "tile_spanning_row":
         lens = np.array([3, 50000, 2, 0, 7000, 1] + [5] * 900)
@@ -389,8 +391,8 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
     if shape == "ints":
         assert np.array_equal(y, y_ref)
     assert np.all(y[lens == 0] == 0.0)
+    assert wk.spmv_csr(csr, x, e).tobytes() == y.tobytes()  # both deterministic (no atomics)
     if strategy == "merge":
-        assert wk.spmv_csr(csr, x, e).tobytes() == y.tobytes()
         # rows folded inside one thread's 8 items are the reference fold exactly
         one = lens <= 1
         assert y[one].tobytes() == y_ref[one].tobytes()
