@@ -74,7 +74,8 @@ int wk_device_sm_count(void);
  * 0 = register-only SELL-P kernel, 1..10 = TMA pipeline configurations
  * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr;
  * "coo_kernel": 0..3 (default 3, spmv.cu coo_kernel_choice); "ell_kernel":
- * 0 = register kernel (default), 1 = TMA pipeline; "seg8_kernel" (COO /
+ * 0 = register kernel, 1 = SELL-P(64) warp pipeline, 2 (default) .. 4 =
+ * ell_tma_kernel (512-row tiles, producer warp); "seg8_kernel" (COO /
  * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring */
 int wk_config_set(const char* key, int64_t value);
 

@@ -28,7 +28,8 @@ struct SellpTmaCfg {
 // Consume one landed chunk: nj <= J columns for this lane's two rows.
 // kGuard (ELL's last, partial 64-row block): rows past nrows hold stale
 // shared memory and must not gather.
-template <int J, bool kLen, bool kGuard = false>
+// kColStride: distance between the staged columns (64 = one SELL-P slice).
+template <int J, bool kLen, bool kGuard = false, int kColStride = 64>
 __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const int* __restrict__ c, int nj,
                                             int j0, int len0, int len1, const double* __restrict__ x, double& a0,
                                             double& a1, bool ok0 = true, bool ok1 = true) {
@@ -37,8 +38,8 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
 #pragma unroll
     for (int jj = 0; jj < J; ++jj) {
         if (jj < nj) {
-            vv[jj] = *reinterpret_cast<const double2*>(v + jj * 64);
-            const int2 cc = *reinterpret_cast<const int2*>(c + jj * 64);
+            vv[jj] = *reinterpret_cast<const double2*>(v + jj * kColStride);
+            const int2 cc = *reinterpret_cast<const int2*>(c + jj * kColStride);
             x0[jj] = (!kGuard || ok0) ? ld_x(x, cc.x) : 0.0;
             x1[jj] = (!kGuard || ok1) ? ld_x(x, cc.y) : 0.0;
         }

@@ -21,6 +21,7 @@
 #include "segwarp.cuh"
 #include "csr_tma.cuh"
 #include "sellp_tma.cuh"
+#include "ell_tma.cuh"
 
 namespace wk {
 
@@ -167,11 +168,12 @@ static int csr_kernel_choice() {
 }
 
 // ELL kernel selection (env WK_ELL_KERNEL or wk_config_set("ell_kernel", i)):
-// 0 (default) = register kernel, 1 = TMA pipeline (see launch_ell).
+// 0 = register kernel, 1 = SELL-P(64) warp pipeline with ELL addressing,
+// 2 (default) .. 4 = ell_tma_kernel configurations (see launch_ell).
 static int g_ell_choice = -1;
 
 int set_ell_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 1, WK_ERR_INVALID, "ell kernel choice must be 0 or 1");
+    WK_REQUIRE(choice >= 0 && choice <= 4, WK_ERR_INVALID, "ell kernel choice must be 0..4");
     g_ell_choice = choice;
     return 0;
 }
@@ -179,7 +181,7 @@ int set_ell_kernel(int choice) {
 static int ell_kernel_choice() {
     if (g_ell_choice < 0) {
         const char* e = getenv("WK_ELL_KERNEL");
-        g_ell_choice = (e != nullptr) ? atoi(e) : 0;
+        g_ell_choice = (e != nullptr) ? atoi(e) : 2;
     }
     return g_ell_choice;
 }
@@ -294,8 +296,16 @@ int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
     // Measured 1.7 ms vs 0.49 ms for the register kernel on the 27-point
     // 200^3 ELL (columns 64 MB apart: the many small copies do not stream),
     // so the register kernel is the default.
-    if (ell_kernel_choice() == 1 && stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16) &&
-        width > 0)
+    const int choice = ell_kernel_choice();
+    const bool tma_ok = stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16) && width > 0;
+    if (choice >= 2 && tma_ok) {
+        switch (choice) {
+            case 3: return launch_ell_tma<EllTmaCfg<2, 8, 448, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
+            case 4: return launch_ell_tma<EllTmaCfg<2, 6, 512, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
+            default: return launch_ell_tma<EllTmaCfg<4, 4, 448, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
+        }
+    }
+    if (choice == 1 && tma_ok)
         return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, false, true>(
             nrows, ncols, nullptr, col, val, row_lengths, x, y, skip, st, DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr},
             width, stride);

@@ -186,10 +186,13 @@ def ell_kernel(wk, request):
 
     _lib.call("wk_config_set", b"ell_kernel", request.param)
     yield request.param
-    _lib.call("wk_config_set", b"ell_kernel", 0)
+    _lib.call("wk_config_set", b"ell_kernel", 2)
 
 
-@pytest.mark.parametrize("ell_kernel", [0, 1], indirect=True)
+ELL_KERNELS = (0, 1, 2, 3, 4)  # register, SELL-P warp pipeline, ell_tma_kernel configs (2 = default)
+
+
+@pytest.mark.parametrize("ell_kernel", ELL_KERNELS, indirect=True)
 @pytest.mark.parametrize("nrows,stride", [(1000, 1000), (4096, 4096), (4100, 4100), (130, 132), (999, 1004),
                                           (1001, 1001), (2000, 2050)])
 def test_ell_strides_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
@@ -210,6 +213,26 @@ def test_ell_strides_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
         x[0] = x0
         y_ref = sparse_ref.spmv(csr, x)
         assert wk.spmv_ell(ell, x, ex).tobytes() == y_ref.tobytes()
+
+
+@pytest.mark.parametrize("ell_kernel", ELL_KERNELS, indirect=True)
+@pytest.mark.parametrize("nrows,stride", [(400003, 400004), (400000, 400000)])
+def test_ell_many_tiles_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
+    """More 512-row tiles than CTAs in the persistent grid (every ring stage
+    reused across tiles), a partial last tile, a width that is not a multiple
+    of the stage's column count; bitwise vs the oracle."""
+    ncols = 50000
+    lens = rng.integers(0, 11, size=nrows)
+    lens[7] = 13
+    ptrs = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    rows = np.repeat(np.arange(nrows), lens)
+    start = rng.integers(0, ncols - 13, size=nrows)
+    cols = start[rows] + (np.arange(ptrs[-1]) - ptrs[rows])
+    csr = wk.CsrMatrix(nrows, ncols, ptrs, cols, rng.standard_normal(len(cols)))
+    ell = wk.csr_to_ell(csr, stride=stride, exec=ex)
+    assert ell.width == 13
+    x = rng.standard_normal(ncols)
+    assert wk.spmv_ell(ell, x, ex).tobytes() == sparse_ref.spmv(csr, x).tobytes()
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
