@@ -76,7 +76,9 @@ int wk_device_sm_count(void);
  * "coo_kernel": 0..3 (default 3, spmv.cu coo_kernel_choice); "ell_kernel":
  * 0 = register kernel, 1 = SELL-P(64) warp pipeline, 2 (default) .. 4 =
  * ell_tma_kernel (512-row tiles, producer warp); "seg8_kernel" (COO /
- * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring */
+ * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring;
+ * "fill_kernel" (CSR -> SELL-P / ELL / Hybrid-ELL fill): 0 = staged scatter,
+ * 1 (default) = TMA-staged ring */
 int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */

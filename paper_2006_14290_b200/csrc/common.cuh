@@ -67,6 +67,7 @@ int set_csr_kernel(int choice);
 int set_coo_kernel(int choice);
 int set_ell_kernel(int choice);
 int set_seg8_kernel(int choice);
+int set_fill_kernel(int choice);
 
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.
@@ -161,6 +162,27 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
         "%4;" ::"r"(smem_addr(dst)),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
+}
+
+// 1-D bulk async copy shared -> global (TMA engine), tracked by bulk groups of
+// the issuing thread. dst/src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// wait until at most N of this thread's committed bulk groups still read shared memory
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -272,6 +272,54 @@ def test_from_entries_duplicates(wk):
     assert m.values.tobytes() == ez.coo.values.tobytes()
 
 
+@pytest.fixture
+def fill_kernel(wk, request):
+    from paper_2006_14290_b200 import _lib
+
+    _lib.call("wk_config_set", b"fill_kernel", request.param)
+    yield request.param
+    _lib.call("wk_config_set", b"fill_kernel", 1)
+
+
+@pytest.mark.parametrize("fill_kernel", [0, 1], indirect=True)
+@pytest.mark.parametrize("ss", [1, 4, 32, 64, 256])
+def test_sellp_fill_kernels_bitwise(wk, ex, rng, ss, fill_kernel):
+    """CSR -> SELL-P fill, staged scatter and TMA ring: many slices per CTA of
+    the persistent grid, slices too wide for a stage (a 5000-entry row, direct
+    path), empty slices, a last slice whose 16-byte-widened range would pass
+    nnz; every array bitwise vs the oracle (sparse.py:219-242)."""
+    nrows, ncols = 150001, 40000
+    lens = rng.integers(0, 12, size=nrows)
+    lens[1000:1000 + 3 * ss] = 0
+    lens[77] = 5000
+    lens[-1] = 3 - int(lens[:-1].sum()) % 4 + 4  # nnz % 4 == 3
+    ptrs = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    rows = np.repeat(np.arange(nrows), lens)
+    start = rng.integers(0, ncols - 5000, size=nrows)
+    cols = start[rows] + (np.arange(ptrs[-1]) - ptrs[rows])
+    csr = wk.CsrMatrix(nrows, ncols, ptrs, cols, rng.standard_normal(len(cols)))
+    assert csr.nnz % 4 == 3
+    got = wk.csr_to_sellp(csr, ss, ex)
+    ref = sparse_ref.csr_to_sellp(csr, ss)
+    assert np.array_equal(got.slice_sets, ref.slice_sets)
+    assert np.array_equal(got.row_lengths, ref.row_lengths)
+    assert np.array_equal(got.col_idx, ref.col_idx)
+    assert got.values.tobytes() == ref.values.tobytes()
+    if ss != 64:
+        return
+    # the same kernels fill ELL (tiles of 2^k rows, stride padding rows) and the Hybrid ELL part (clipped rows)
+    for stride in (nrows, nrows + 3, nrows + 1000):
+        ell = wk.csr_to_ell(csr, stride=stride, exec=ex)
+        eref = sparse_ref.csr_to_ell(csr, stride=stride)
+        assert np.array_equal(ell.col_idx, eref.col_idx) and ell.values.tobytes() == eref.values.tobytes()
+        assert np.array_equal(ell.row_lengths, eref.row_lengths)
+    hyb = wk.csr_to_hybrid(csr, width=5, exec=ex)
+    href = sparse_ref.csr_to_hybrid(csr, 5)
+    assert np.array_equal(hyb.ell.col_idx, href.ell.col_idx)
+    assert hyb.ell.values.tobytes() == href.ell.values.tobytes()
+    assert np.array_equal(hyb.coo.col_idx, href.coo.col_idx) and hyb.coo.values.tobytes() == href.coo.values.tobytes()
+
+
 # ---- edge cases -----------------------------------------------------------------------------
 
 

@@ -5,17 +5,19 @@
 #   gpurun -- 'bash tools/ncu_capture.sh [tag]'
 set -u
 TAG=${1:-cur}
+ONLY=${2:-}
 OUT=gpurun_out/ncu
 mkdir -p "$OUT"
 NCU="ncu --set full --clock-control none --import-source on"
 cap() {  # name kernel-regex skip count cmd...
     local name=$1 rx=$2 skip=$3 cnt=$4
     shift 4
+    if [ -n "$ONLY" ] && ! [[ " $ONLY " == *" $name "* ]]; then return; fi
     timeout 600 $NCU -k "regex:$rx" -s "$skip" -c "$cnt" -f -o "$OUT/${TAG}_$name" "$@" > "$OUT/${TAG}_$name.log" 2>&1
     echo "$name rc=$?" >> "$OUT/${TAG}_status.txt"
 }
 cap sellp_spmv sellp64_tma 2 1 python tools/profile_spmv.py sellp 27 200
-cap ell_spmv sliced_spmv 2 1 python tools/profile_spmv.py ell 27 200
+cap ell_spmv ell_tma_kernel 2 1 python tools/profile_spmv.py ell 27 200
 cap csr_rowblock csr_rowblock 2 1 python tools/profile_spmv.py csr 27 200 rowblock
 cap csr_stream "csr_(stream|tma)" 2 1 python tools/profile_spmv.py csr 27 200 stream
 cap csr_rmat seg8 2 1 python tools/profile_spmv.py csr_rmat 0 24 load_balance
@@ -23,7 +25,9 @@ cap csr_merge_rmat csr_merge_kernel 2 1 python tools/profile_spmv.py csr_rmat 0 
 cap coo_rmat seg8 2 1 python tools/profile_spmv.py coo 0 24
 cap gmres_multidot gmres_multidot_vec 20 1 python tools/profile_gmres.py
 cap csr_poisson2d csr_ 2 1 python tools/profile_spmv.py csr 5 1000 auto
-if [ -n "${WK_NCU_LAUNCHES:-1}" ]; then
+cap ell_fill ell_fill_kernel 2 1 python tools/profile_spmv.py convert 27 200
+cap sellp_fill sellp_fill_kernel 2 1 python tools/profile_spmv.py convert 27 200
+if [ -z "$ONLY" ]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file "$OUT/${TAG}_launches.csv" python bench.py --steps 4 --warmup 3 > "$OUT/${TAG}_launches_bench.log" 2>&1
     echo "launches rc=$?" >> "$OUT/${TAG}_status.txt"

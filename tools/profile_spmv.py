@@ -1,5 +1,6 @@
 """One format's SpMV a few times, for ncu: python tools/profile_spmv.py FMT [points] [n] [csr strategy]
-FMT in csr, sellp, ell, coo(R-MAT scale n), hybrid(R-MAT)."""
+FMT in csr, sellp, ell, coo(R-MAT scale n), hybrid(R-MAT), convert (CSR -> ELL and
+CSR -> SELL-P(64) of the stencil, 5 times each)."""
 import sys
 sys.path.insert(0, '.')
 import torch
@@ -20,6 +21,15 @@ else:
         A = D.csr_to_sellp(A, 64)
     elif fmt == "ell":
         A = D.csr_to_ell(A)
+if fmt == "convert":
+    for _ in range(5):
+        E = D.csr_to_ell(A, width=27 if pts == 27 else None)
+        del E
+        S = D.csr_to_sellp(A, 64)
+        del S
+    torch.cuda.synchronize()
+    print("ok convert", A.nrows)
+    sys.exit(0)
 strategy = sys.argv[4] if len(sys.argv) > 4 else None
 if strategy and getattr(A, "fmt", None) == "csr":
     A.with_strategy(strategy)
