@@ -25,8 +25,8 @@ cap csr_merge_rmat csr_merge_kernel 2 1 python tools/profile_spmv.py csr_rmat 0 
 cap coo_rmat seg8 2 1 python tools/profile_spmv.py coo 0 24
 cap gmres_multidot gmres_multidot_vec 20 1 python tools/profile_gmres.py
 cap csr_poisson2d csr_ 2 1 python tools/profile_spmv.py csr 5 1000 auto
-cap ell_fill ell_fill_kernel 2 1 python tools/profile_spmv.py convert 27 200
-cap sellp_fill sellp_fill_kernel 2 1 python tools/profile_spmv.py convert 27 200
+cap ell_fill fill_tma_kernel 2 1 python tools/profile_spmv.py convert 27 200
+cap sellp_fill fill_tma_kernel 3 1 python tools/profile_spmv.py convert 27 200
 if [ -z "$ONLY" ]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
         --log-file "$OUT/${TAG}_launches.csv" python bench.py --steps 4 --warmup 3 > "$OUT/${TAG}_launches_bench.log" 2>&1
