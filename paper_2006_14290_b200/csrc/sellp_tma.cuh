@@ -84,6 +84,21 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     int64_t ps = gwarp, pbase = 0;
     int pj = 0, pw = 0;
     bool pvalid = false;
+    // slice offsets are read one slice ahead (registers): the loads of the
+    // next slice's sets[] entries are in flight while this slice streams,
+    // instead of stalling the warp at every slice change (7-point slices are
+    // only 2 chunks long)
+    int64_t q0 = 0, q1 = 0, n0 = 0, n1 = 0;
+    if (!kEll) {
+        if (ps < nslices) {
+            q0 = __ldg(sets + ps);
+            q1 = __ldg(sets + ps + 1);
+        }
+        if (ps + nwarps < nslices) {
+            n0 = __ldg(sets + ps + nwarps);
+            n1 = __ldg(sets + ps + nwarps + 1);
+        }
+    }
     auto seek = [&]() {
         pvalid = false;
         while (ps < nslices) {
@@ -98,15 +113,20 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
                 pj = 0;
                 continue;
             }
-            const int64_t s0 = __ldg(sets + ps);
-            pw = int(__ldg(sets + ps + 1) - s0);
+            pw = int(q1 - q0);
             if (pj < pw) {
-                pbase = s0 * 64;
+                pbase = q0 * 64;
                 pvalid = true;
                 return;
             }
             ps += nwarps;
             pj = 0;
+            q0 = n0;
+            q1 = n1;
+            if (ps + nwarps < nslices) {
+                n0 = __ldg(sets + ps + nwarps);
+                n1 = __ldg(sets + ps + nwarps + 1);
+            }
         }
     };
     auto issue = [&](int st) {
@@ -143,8 +163,18 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
 
     uint32_t i = 0;  // chunks consumed by this warp
     double dacc = 0.0;
+    int cw = 0, cwn = 0;  // consumer: this slice's width and the next one's (read ahead)
+    if (!kEll) {
+        if (gwarp < nslices) cw = int(__ldg(sets + gwarp + 1) - __ldg(sets + gwarp));
+        if (gwarp + nwarps < nslices) cwn = int(__ldg(sets + gwarp + nwarps + 1) - __ldg(sets + gwarp + nwarps));
+    }
     for (int64_t s = gwarp; s < nslices; s += nwarps) {
-        const int w = kEll ? int(ell_width) : int(__ldg(sets + s + 1) - __ldg(sets + s));
+        const int w = kEll ? int(ell_width) : cw;
+        if (!kEll) {
+            cw = cwn;
+            if (s + 2 * nwarps < nslices)
+                cwn = int(__ldg(sets + s + 2 * nwarps + 1) - __ldg(sets + s + 2 * nwarps));
+        }
         const int64_t r0 = s * 64 + 2 * lane;
         const bool partial = kEll && (s + 1) * 64 > nrows;
         int len0 = w, len1 = w;
