@@ -425,6 +425,9 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
         const int nv = kb >= whi ? 0 : (whi - kb >= 8 ? 8 : int(whi - kb));
         double pv[8];
         int rw[8];
+        // CSR row ids first: their hrow loads overlap the matrix stream and
+        // the gathers instead of waiting behind the products
+        if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
         {
             int c[8];
             double v[8];
@@ -455,7 +458,6 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
 #pragma unroll
             for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
         }
-        if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
         seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
     }
 }
