@@ -166,6 +166,7 @@ struct HeadPlan {
     const int* hrow;
     int* crow;       // per warp range: the row continuing past the range (-1: none) ...
     double* cval;    // ... and the range's part of it (added in range order by the fix-up)
+    const int* rrow; // row of each warp range's first entry (ranges + 1 entries; last = -1)
 };
 
 struct HeadPlanMut {
@@ -175,12 +176,13 @@ struct HeadPlanMut {
     void* scan_ws;
     int* crow;
     double* cval;
+    int* rrow;
 };
 
 inline int64_t head_plan_bytes(int64_t nrows, int64_t nnz) {
     const int64_t w = seg8_windows(nnz), g = seg8_warps(nnz);
     return ceil_div((w + 1) * 4, 256) * 256 + w * 32 + ceil_div(nrows * 4, 256) * 256 + ceil_div(scan_ws_bytes(w), 256) * 256 +
-           ceil_div(g * 4, 256) * 256 + g * 8 + 256;
+           ceil_div(g * 4, 256) * 256 + ceil_div(g * 8, 256) * 256 + (g + 1) * 4 + 256;
 }
 
 inline HeadPlanMut head_plan_views(void* plan, int64_t nrows, int64_t nnz) {
@@ -198,6 +200,8 @@ inline HeadPlanMut head_plan_views(void* plan, int64_t nrows, int64_t nnz) {
     h.crow = reinterpret_cast<int*>(p);
     p += ceil_div(seg8_warps(nnz) * 4, 256) * 256;
     h.cval = reinterpret_cast<double*>(p);
+    p += ceil_div(seg8_warps(nnz) * 8, 256) * 256;
+    h.rrow = reinterpret_cast<int*>(p);
     return h;
 }
 
@@ -229,6 +233,16 @@ __global__ void head_rows_kernel(int64_t nrows, const int* __restrict__ ptrs, co
     hrow[k] = int(r);
 }
 
+__device__ __forceinline__ int head_row_of(const HeadPlan& hp, int64_t e);
+
+// row of the first entry of every warp range (range g starts at g * kS8PerWarp)
+__global__ void range_rows_kernel(int64_t nranges, int64_t nnz, HeadPlan hp, int* __restrict__ rrow) {
+    const int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g > nranges) return;
+    const int64_t e = g * kS8PerWarp;
+    rrow[g] = e < nnz ? head_row_of(hp, e) : -1;
+}
+
 inline int build_head_plan(int64_t nrows, int64_t nnz, const int* ptrs, void* plan, cudaStream_t st) {
     const int64_t nw = seg8_windows(nnz);
     const HeadPlanMut h = head_plan_views(plan, nrows, nnz);
@@ -243,6 +257,10 @@ inline int build_head_plan(int64_t nrows, int64_t nnz, const int* ptrs, void* pl
         head_rows_kernel<<<(unsigned)ceil_div(nrows, 256), 256, 0, st>>>(nrows, ptrs, h.mask, h.hoff, h.hrow);
         WK_LAUNCH_CHECK();
     }
+    const int64_t g = seg8_warps(nnz);
+    range_rows_kernel<<<(unsigned)ceil_div(g + 1, 256), 256, 0, st>>>(
+        g, nnz, HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, nullptr}, h.rrow);
+    WK_LAUNCH_CHECK();
     return 0;
 }
 
@@ -269,8 +287,9 @@ struct RangeCsr {
 
 __device__ __forceinline__ RangeCsr seg8_range_csr(int lane, int64_t wlo, int64_t whi, int64_t nnz, const HeadPlan& hp,
                                                    int& first_row, int& last_row) {
-    first_row = head_row_of(hp, wlo);
-    last_row = whi < nnz ? head_row_of(hp, whi) : -1;
+    const int64_t g = wlo / kS8PerWarp;  // ranges start at multiples of kS8PerWarp
+    first_row = __ldg(hp.rrow + g);
+    last_row = __ldg(hp.rrow + g + 1);  // row of entry whi (-1 past nnz)
     const int64_t w0 = wlo >> 8, nwin = (nnz + kS8Win - 1) / kS8Win;
     RangeCsr rc;
     rc.pm0 = (w0 + (lane >> 3) < nwin) ? __ldg(hp.mask + w0 * 8 + lane) : 0u;
@@ -647,7 +666,7 @@ int launch_seg8_tma(int64_t nnz, int accumulate, const int* rows, const int* col
 // The TMA path needs 16-byte aligned arrays.
 inline int launch_seg8(bool csr, int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
                        const double* x, double* y, const int* skip, cudaStream_t st,
-                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr}) {
+                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}) {
     if (nnz == 0) return 0;
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     if (seg8_kernel_choice() == 1 && al(col) && al(val) && (csr || al(rows))) {

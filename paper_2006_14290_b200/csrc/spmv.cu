@@ -512,7 +512,7 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
                    "csr load_balance needs 16-byte aligned col_idx / values");
         const HeadPlanMut h = head_plan_views(merge_plan, nrows, nnz);
         return launch_seg8(true, nnz, 0, nullptr, col, val, x, y, skip, st,
-                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval});
+                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow});
     }
     if (strategy == WK_CSR_ROWBLOCK) {
         // 32*k-row blocks; the stage capacity is the smallest that keeps a

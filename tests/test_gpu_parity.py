@@ -282,7 +282,7 @@ def fill_kernel(wk, request):
 
 
 @pytest.mark.parametrize("fill_kernel", [0, 1], indirect=True)
-@pytest.mark.parametrize("ss", [1, 4, 32, 64, 256])
+@pytest.mark.parametrize("ss", [1, 4, 32, 64, 256, 512])
 def test_sellp_fill_kernels_bitwise(wk, ex, rng, ss, fill_kernel):
     """CSR -> SELL-P fill, staged scatter and TMA ring: many slices per CTA of
     the persistent grid, slices too wide for a stage (a 5000-entry row, direct
