@@ -78,7 +78,9 @@ int wk_device_sm_count(void);
  * ell_tma_kernel (512-row tiles, producer warp); "seg8_kernel" (COO /
  * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring;
  * "fill_kernel" (CSR -> SELL-P / ELL / Hybrid-ELL fill): 0 = staged scatter,
- * 1 (default) = TMA-staged ring */
+ * 1 (default) = TMA-staged ring; "cg_pingpong" (wk_cg_solve): 1 (default) =
+ * consecutive kernels walk the rows in alternating directions (L2 reuse), 0 =
+ * all forward */
 int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */

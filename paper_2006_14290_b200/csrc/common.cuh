@@ -68,11 +68,12 @@ int set_coo_kernel(int choice);
 int set_ell_kernel(int choice);
 int set_seg8_kernel(int choice);
 int set_fill_kernel(int choice);
+int set_cg_pingpong(int v);
 
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
-                   cudaStream_t st, void* peer = nullptr, const void* halo = nullptr);
+                   cudaStream_t st, void* peer = nullptr, const void* halo = nullptr, int rev = 0);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -92,8 +92,9 @@ __global__ void halo_wait_kernel(const PeerCtx* c, const PeerHalo* h, const int*
 }
 
 static int cg_spmv_dot(const wk_matrix* A, int64_t n, const double* p, double* q, wk_cg_state* s, void* ws,
-                       bool finalize, cudaStream_t st, PeerCtx* peer = nullptr, const PeerHalo* halo = nullptr) {
-    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st, peer, halo);
+                       bool finalize, cudaStream_t st, PeerCtx* peer = nullptr, const PeerHalo* halo = nullptr,
+                       int rev = 0) {
+    const int rc = spmv_dot_fused(A, p, q, s, ws, finalize ? 1 : 0, st, peer, halo, rev);
     if (rc != 1) return rc;
     if (halo != nullptr) {  // other formats: a separate wait before the SpMV
         halo_wait_kernel<<<1, 32, 0, st>>>(peer, halo, &s->done);
@@ -136,7 +137,7 @@ template <bool kAlphaIn>
 __global__ void __launch_bounds__(256)
 cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
                  double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize,
-                 PeerCtx* peer) {
+                 PeerCtx* peer, int rev = 0) {
     if (s->done) return;
     double alpha;
     bool repl, brk = false;
@@ -160,9 +161,10 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
     double2* r2 = reinterpret_cast<double2*>(r);
     double acc = 0.0;
     const int64_t np_eff = n_eff >> 1;
-    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np_eff; k += 2 * T) {
-        const int64_t k1 = k + T;
-        const bool h1 = k1 < np;
+    // rev: pairs visited from the end (see cg_solve: kernels alternate directions)
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np_eff; kl += 2 * T) {
+        const bool h1 = kl + T < np;
+        const int64_t k = rev ? np - 1 - kl : kl, k1 = rev ? np - 1 - (kl + T) : kl + T;
         double2 pa = __ldcs(p2 + k), xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
         if (h1) {
             pb = __ldcs(p2 + k1);
@@ -234,7 +236,7 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
 template <bool kBetaIn>
 __global__ void __launch_bounds__(256)
 cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, wk_cg_state* s, double* hist,
-                RedWorkspace ws, PeerCtx* peer, const PeerHalo* halo) {
+                RedWorkspace ws, PeerCtx* peer, const PeerHalo* halo, int rev = 0) {
     if (s->done) return;
     double rr = 0.0;
     if (kBetaIn) rr = (peer != nullptr) ? peer_wait_sum_block(peer) : s->rr;
@@ -242,9 +244,9 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
-    for (int64_t k = int64_t(blockIdx.x) * 256 + threadIdx.x; k < np; k += 2 * T) {
-        const int64_t k1 = k + T;
-        const bool h1 = k1 < np;
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += 2 * T) {
+        const bool h1 = kl + T < np;
+        const int64_t k = rev ? np - 1 - kl : kl, k1 = rev ? np - 1 - (kl + T) : kl + T;
         double2 ra = __ldcs(r2 + k), pa = p2[k], rb{0, 0}, pb{0, 0};
         if (h1) {
             rb = __ldcs(r2 + k1);
@@ -286,10 +288,10 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
 }
 
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
-                        double* hist, void* ws, bool finalize, cudaStream_t st) {
+                        double* hist, void* ws, bool finalize, cudaStream_t st, int rev = 0) {
     if (n > 0 && vec_ok(p, q, x, r)) {
         cg_update_xr_vec<false><<<vec_grid(n), 256, 0, st>>>(n, p, q, x, r, s, hist, red_ws(ws), finalize ? 1 : 0,
-                                                            nullptr);
+                                                            nullptr, rev);
         WK_LAUNCH_CHECK();
         return 0;
     }
@@ -333,15 +335,30 @@ static int cg_replace_r(int64_t n, const double* b, const double* q, double* r, 
         ws, &s->done, st);
 }
 
-static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st) {
+static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* s, cudaStream_t st, int rev = 0) {
     if (n > 0 && vec_ok(r, p, r, p)) {
         cg_update_p_vec<false><<<vec_grid(n), 256, 0, st>>>(n, r, p, const_cast<wk_cg_state*>(s), nullptr,
-                                                          RedWorkspace{nullptr, nullptr}, nullptr, nullptr);
+                                                          RedWorkspace{nullptr, nullptr}, nullptr, nullptr, rev);
         WK_LAUNCH_CHECK();
         return 0;
     }
     return launch_masked_map(
         n, [=] __device__(int64_t i) { p[i] = __dadd_rn(r[i], __dmul_rn(s->beta, p[i])); }, &s->done, st);
+}
+
+static int g_cg_pingpong = -1;
+static int cg_pingpong_choice() {
+    if (g_cg_pingpong < 0) {
+        const char* e = getenv("WK_CG_PINGPONG");
+        g_cg_pingpong = e != nullptr ? atoi(e) : 1;
+    }
+    return g_cg_pingpong;
+}
+
+int set_cg_pingpong(int v) {
+    WK_REQUIRE(v == 0 || v == 1, WK_ERR_INVALID, "cg_pingpong must be 0 or 1");
+    g_cg_pingpong = v;
+    return 0;
 }
 
 }  // namespace wk
@@ -506,15 +523,22 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     WK_CUDA(cudaMemsetAsync(red, 0, size_t(red_ws_bytes()), st));
     WK_TRY(cg_init_local(n, b, x, r, p, s, red, st));
     WK_TRY(cg_init_finish(s, tol, max_iters, hist, st));
+    // L2 ping-pong: consecutive kernels walk the rows in opposite directions,
+    // so each starts on the rows the previous one touched last (the most
+    // recently written q / r / p are still in the 126 MB L2). Iteration i:
+    // SpMV d, x/r update !d, p update d, with d flipping every iteration (the
+    // 50-iteration period is even). Knob: wk_config_set("cg_pingpong", 0|1).
+    const bool pp = cg_pingpong_choice() != 0;
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kReplaceEvery; ++i) {
-            WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs));
-            WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs));
+            const int d = pp ? (i & 1) : 0;
+            WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs, nullptr, nullptr, d));
+            WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs, pp ? 1 - d : 0));
             if (i == kReplaceEvery - 1) {
                 WK_TRY(wk_spmv_masked(A, x, q, &s->done, cs));
                 WK_TRY(cg_replace_r(n, b, q, r, s, hist, red, true, cs));
             }
-            WK_TRY(cg_update_p(n, r, p, s, cs));
+            WK_TRY(cg_update_p(n, r, p, s, cs, d));
         }
         return 0;
     });

@@ -47,6 +47,7 @@ int wk_config_set(const char* key, int64_t value) {
     if (key != nullptr && strcmp(key, "ell_kernel") == 0) return wk::set_ell_kernel(int(value));
     if (key != nullptr && strcmp(key, "seg8_kernel") == 0) return wk::set_seg8_kernel(int(value));
     if (key != nullptr && strcmp(key, "fill_kernel") == 0) return wk::set_fill_kernel(int(value));
+    if (key != nullptr && strcmp(key, "cg_pingpong") == 0) return wk::set_cg_pingpong(int(value));
     wk::set_error("unknown configuration key '%s'", key ? key : "(null)");
     return WK_ERR_INVALID;
 }

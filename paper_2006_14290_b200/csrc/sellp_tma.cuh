@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
 sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
                    const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
                    const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip,
-                   DotEpilogue dot, int64_t ell_width = 0, int64_t ell_stride = 0) {
+                   DotEpilogue dot, int64_t ell_width = 0, int64_t ell_stride = 0, int rev = 0) {
     constexpr int J = Cfg::kJ, S = Cfg::kS, WARPS = Cfg::kWarps, CH = Cfg::kChunk;
     if (skip != nullptr && *skip) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -79,6 +79,10 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     const int64_t gwarp = int64_t(blockIdx.x) * WARPS + warp;
     const int64_t nwarps = int64_t(gridDim.x) * WARPS;
     const uint64_t pol = policy_evict_first();
+    // rev: walk the slices from the last one down (a CG iteration alternates
+    // directions so each kernel starts on the rows the previous one touched
+    // last, which are still in L2); per-row results do not depend on it
+    auto SP = [&](int64_t k) -> int64_t { return rev ? nslices - 1 - k : k; };
 
     // producer cursor (warp-uniform; lane 0 issues)
     int64_t ps = gwarp, pbase = 0;
@@ -91,12 +95,12 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     int64_t q0 = 0, q1 = 0, n0 = 0, n1 = 0;
     if (!kEll) {
         if (ps < nslices) {
-            q0 = __ldg(sets + ps);
-            q1 = __ldg(sets + ps + 1);
+            q0 = __ldg(sets + SP(ps));
+            q1 = __ldg(sets + SP(ps) + 1);
         }
         if (ps + nwarps < nslices) {
-            n0 = __ldg(sets + ps + nwarps);
-            n1 = __ldg(sets + ps + nwarps + 1);
+            n0 = __ldg(sets + SP(ps + nwarps));
+            n1 = __ldg(sets + SP(ps + nwarps) + 1);
         }
     }
     auto seek = [&]() {
@@ -105,7 +109,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             if (kEll) {
                 pw = int(ell_width);
                 if (pj < pw) {
-                    pbase = ps * 64;
+                    pbase = SP(ps) * 64;
                     pvalid = true;
                     return;
                 }
@@ -124,8 +128,8 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             q0 = n0;
             q1 = n1;
             if (ps + nwarps < nslices) {
-                n0 = __ldg(sets + ps + nwarps);
-                n1 = __ldg(sets + ps + nwarps + 1);
+                n0 = __ldg(sets + SP(ps + nwarps));
+                n1 = __ldg(sets + SP(ps + nwarps) + 1);
             }
         }
     };
@@ -165,18 +169,19 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     double dacc = 0.0;
     int cw = 0, cwn = 0;  // consumer: this slice's width and the next one's (read ahead)
     if (!kEll) {
-        if (gwarp < nslices) cw = int(__ldg(sets + gwarp + 1) - __ldg(sets + gwarp));
-        if (gwarp + nwarps < nslices) cwn = int(__ldg(sets + gwarp + nwarps + 1) - __ldg(sets + gwarp + nwarps));
+        if (gwarp < nslices) cw = int(__ldg(sets + SP(gwarp) + 1) - __ldg(sets + SP(gwarp)));
+        if (gwarp + nwarps < nslices)
+            cwn = int(__ldg(sets + SP(gwarp + nwarps) + 1) - __ldg(sets + SP(gwarp + nwarps)));
     }
     for (int64_t s = gwarp; s < nslices; s += nwarps) {
         const int w = kEll ? int(ell_width) : cw;
         if (!kEll) {
             cw = cwn;
             if (s + 2 * nwarps < nslices)
-                cwn = int(__ldg(sets + s + 2 * nwarps + 1) - __ldg(sets + s + 2 * nwarps));
+                cwn = int(__ldg(sets + SP(s + 2 * nwarps) + 1) - __ldg(sets + SP(s + 2 * nwarps)));
         }
-        const int64_t r0 = s * 64 + 2 * lane;
-        const bool partial = kEll && (s + 1) * 64 > nrows;
+        const int64_t r0 = SP(s) * 64 + 2 * lane;
+        const bool partial = kEll && (SP(s) + 1) * 64 > nrows;
         int len0 = w, len1 = w;
         if (!finite0) {
             len0 = r0 < nrows ? row_lengths[r0] : 0;
@@ -234,7 +239,7 @@ template <class Cfg, bool kDot = false, bool kEll = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
                        DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int64_t ell_width = 0,
-                       int64_t ell_stride = 0) {
+                       int64_t ell_stride = 0, int rev = 0) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -248,7 +253,7 @@ int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const 
     const int64_t need = ceil_div(nslices, Cfg::kWarps);
     if (grid > need) grid = need;
     sellp64_tma_kernel<Cfg, kDot, kEll><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
-        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, ell_width, ell_stride);
+        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, ell_width, ell_stride, rev);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -275,7 +275,7 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
 // Returns 1 when the operand cannot take the fused path (caller falls back to
 // SpMV + separate dot), 0 on success, an error code otherwise.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
-                   cudaStream_t st, void* peer, const void* halo) {
+                   cudaStream_t st, void* peer, const void* halo, int rev) {
     if (A->format != WK_FMT_SELLP || A->slice_size != 64 || sellp_kernel_choice() == 0 || !aligned(A->values, 16) ||
         !aligned(A->col_idx, 16) || !aligned(q, 16) || !aligned(p, 16) || A->nrows == 0)
         return 1;
@@ -284,7 +284,8 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
                     reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
                     reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo)};
     return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
-                                                             A->values, A->row_lengths, p, q, &s->done, st, dot);
+                                                             A->values, A->row_lengths, p, q, &s->done, st, dot,
+                                                             0, 0, rev);
 }
 
 int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col,
