@@ -55,7 +55,23 @@ static int local_dot(int64_t n, F f, E epi, void* ws, const int* skip, cudaStrea
     return launch_map_reduce(n, f, epi, ws, skip, st);
 }
 
+// Vectorised paths (vmap_kernel, reduce.cuh) when every vector is 16-byte
+// aligned; the scalar map_reduce lambdas below are the fallback. Same
+// element arithmetic; the per-thread summation order of the dots differs.
+struct NoScalars {
+    __device__ int operator()() const { return 0; }
+};
+template <int N>
+struct NoEpi {
+    __device__ void operator()(double (&)[N]) const {}
+};
+
 static int bicg_rho(int64_t n, const double* rh, const double* r, BS* s, void* ws, cudaStream_t st) {
+    if (n > 0 && vmap_ok({rh, r}))
+        return launch_vmap<2, 0, 1>(
+            n, VecArgs<2, 0>{{rh, r}, {nullptr}}, NoScalars{},
+            [] __device__(int, const double(&in)[2], double(&)[1], double(&red)[1]) { red[0] = __dmul_rn(in[0], in[1]); },
+            [=] __device__(double(&t)[1]) { s->rho_new = t[0]; }, ws, &s->done, st);
     return local_dot(
         n, [=] __device__(int64_t i) { return __dmul_rn(rh[i], r[i]); },
         [=] __device__(double t) { s->rho_new = t; }, ws, &s->done, st);
@@ -75,6 +91,13 @@ static int bicg_step_beta(BS* s, cudaStream_t st) {
 }
 
 static int bicg_update_p(int64_t n, const double* r, const double* v, double* p, BS* s, cudaStream_t st) {
+    if (n > 0 && vmap_ok({r, v, p}))
+        return launch_vmap<3, 1, 0>(
+            n, VecArgs<3, 1>{{r, v, p}, {p}}, [=] __device__() { return make_double2(s->beta, s->omega); },
+            [] __device__(double2 c, const double(&in)[3], double(&out)[1], double(&)[1]) {
+                out[0] = __dadd_rn(in[0], __dmul_rn(c.x, __dadd_rn(in[2], -__dmul_rn(c.y, in[1]))));
+            },
+            NoEpi<1>{}, nullptr, &s->done, st);
     return launch_masked_map(
         n,
         [=] __device__(int64_t i) {
@@ -84,6 +107,11 @@ static int bicg_update_p(int64_t n, const double* r, const double* v, double* p,
 }
 
 static int bicg_rv(int64_t n, const double* rh, const double* v, BS* s, void* ws, cudaStream_t st) {
+    if (n > 0 && vmap_ok({rh, v}))
+        return launch_vmap<2, 0, 1>(
+            n, VecArgs<2, 0>{{rh, v}, {nullptr}}, NoScalars{},
+            [] __device__(int, const double(&in)[2], double(&)[1], double(&red)[1]) { red[0] = __dmul_rn(in[0], in[1]); },
+            [=] __device__(double(&t)[1]) { s->rv = t[0]; }, ws, &s->done, st);
     return local_dot(
         n, [=] __device__(int64_t i) { return __dmul_rn(rh[i], v[i]); }, [=] __device__(double t) { s->rv = t; },
         ws, &s->done, st);
@@ -103,6 +131,15 @@ static int bicg_step_alpha(BS* s, cudaStream_t st) {
 }
 
 static int bicg_update_s(int64_t n, const double* r, const double* v, double* sv, BS* s, void* ws, cudaStream_t st) {
+    if (n > 0 && vmap_ok({r, v, sv}))
+        return launch_vmap<2, 1, 1>(
+            n, VecArgs<2, 1>{{r, v}, {sv}}, [=] __device__() { return s->alpha; },
+            [] __device__(double alpha, const double(&in)[2], double(&out)[1], double(&red)[1]) {
+                const double si = __dadd_rn(in[0], -__dmul_rn(alpha, in[1]));
+                out[0] = si;
+                red[0] = __dmul_rn(si, si);
+            },
+            [=] __device__(double(&t)[1]) { s->ss = t[0]; }, ws, &s->done, st);
     return local_dot(
         n,
         [=] __device__(int64_t i) {
@@ -128,6 +165,14 @@ static int bicg_step_s(BS* s, double* hist, cudaStream_t st) {
 
 static int bicg_half_x(int64_t n, const double* p, double* x, BS* s, void* ws, cudaStream_t st) {
     if (n == 0) return launch_scalar([=] __device__() { s->apply_half = 0; }, st);
+    if (vmap_ok({p, x}))  // runs only when the flag is set (once, at an early exit)
+        return launch_vmap<2, 1, 1, true>(
+            n, VecArgs<2, 1>{{x, p}, {x}}, [=] __device__() { return s->alpha; },
+            [] __device__(double alpha, const double(&in)[2], double(&out)[1], double(&red)[1]) {
+                out[0] = __dadd_rn(in[0], __dmul_rn(alpha, in[1]));
+                red[0] = 0.0;
+            },
+            [=] __device__(double(&)[1]) { s->apply_half = 0; }, ws, &s->apply_half, st);
     return launch_map_reduce(
         n,
         [=] __device__(int64_t i) {
@@ -142,6 +187,18 @@ static int bicg_tt_ts(int64_t n, const double* t, const double* sv, BS* s, void*
         return launch_scalar([=] __device__() {
             if (!s->done) s->tt = s->ts = 0.0;
         }, st);
+    if (vmap_ok({t, sv}))
+        return launch_vmap<2, 0, 2>(
+            n, VecArgs<2, 0>{{t, sv}, {nullptr}}, NoScalars{},
+            [] __device__(int, const double(&in)[2], double(&)[1], double(&red)[2]) {
+                red[0] = __dmul_rn(in[0], in[0]);
+                red[1] = __dmul_rn(in[0], in[1]);
+            },
+            [=] __device__(double(&tot)[2]) {
+                s->tt = tot[0];
+                s->ts = tot[1];
+            },
+            ws, &s->done, st);
     return launch_map_reduce_n<2>(
         n,
         [=] __device__(int64_t i, double(&acc)[2]) {
@@ -170,6 +227,16 @@ static int bicg_step_omega(BS* s, cudaStream_t st) {
 
 static int bicg_update_xr(int64_t n, const double* p, const double* sv, const double* t, double* x, double* r, BS* s,
                           void* ws, cudaStream_t st) {
+    if (n > 0 && vmap_ok({p, sv, t, x, r}))
+        return launch_vmap<4, 2, 1>(
+            n, VecArgs<4, 2>{{x, p, sv, t}, {x, r}}, [=] __device__() { return make_double2(s->alpha, s->omega); },
+            [] __device__(double2 c, const double(&in)[4], double(&out)[2], double(&red)[1]) {
+                out[0] = __dadd_rn(__dadd_rn(in[0], __dmul_rn(c.x, in[1])), __dmul_rn(c.y, in[2]));
+                const double ri = __dadd_rn(in[2], -__dmul_rn(c.y, in[3]));
+                out[1] = ri;
+                red[0] = __dmul_rn(ri, ri);
+            },
+            [=] __device__(double(&tot)[1]) { s->rr = tot[0]; }, ws, &s->done, st);
     return local_dot(
         n,
         [=] __device__(int64_t i) {

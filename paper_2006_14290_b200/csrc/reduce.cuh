@@ -10,6 +10,8 @@
 // BASELINE.md §2.
 #pragma once
 
+#include <initializer_list>
+
 #include "common.cuh"
 
 namespace wk {
@@ -132,6 +134,108 @@ map_reduce_kernel(int64_t n, F f, Epi epi, RedWorkspace ws, const int* __restric
 template <typename F, typename Epi>
 int launch_map_reduce(int64_t n, F f, Epi epi, void* ws, const int* skip, cudaStream_t st) {
     map_reduce_kernel<<<red_grid(n), kRedThreads, 0, st>>>(n, f, epi, red_ws(ws), skip);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised element-wise step with optional fused reductions (the Krylov
+// BLAS-1 updates): NIN input vectors, NOUT output vectors (may alias inputs:
+// every load of an iteration precedes its stores), NRED sums. Each thread
+// handles two double2 pairs per iteration (k and k + T), so four elements of
+// every vector are in flight per thread; the solver scalars are read ONCE per
+// thread by `pro()` instead of once per element (a scalar read through the
+// state pointer cannot be hoisted past the vector stores). Per-thread sums run
+// in a fixed element order and are folded by grid_reduce_last_n: deterministic.
+//   f(c, const double (&in)[NIN], double (&out)[NOUT], double (&red)[NRED])
+// All vectors 16-byte aligned (vmap_ok); the callers fall back to the scalar
+// map_reduce kernels otherwise.
+// ---------------------------------------------------------------------------
+template <int NIN, int NOUT>
+struct VecArgs {
+    const double* in[NIN > 0 ? NIN : 1];
+    double* out[NOUT > 0 ? NOUT : 1];
+};
+
+inline int vmap_grid(int64_t n) {
+    int64_t g = ceil_div(ceil_div(n, 2), int64_t(kRedThreads) * 2);
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (g > cap) g = cap;
+    if (g > kRedMaxBlocks) g = kRedMaxBlocks;
+    return int(g < 1 ? 1 : g);
+}
+
+// kRunIf: run only while *skip != 0 (instead of skipping then)
+template <int NIN, int NOUT, int NRED, bool kRunIf, typename Pro, typename F, typename Epi>
+__global__ void __launch_bounds__(kRedThreads)
+vmap_kernel(int64_t n, VecArgs<NIN, NOUT> a, Pro pro, F f, Epi epi, RedWorkspace ws, const int* __restrict__ skip) {
+    constexpr int NR = NRED > 0 ? NRED : 1, NO = NOUT > 0 ? NOUT : 1;
+    if (skip != nullptr && (kRunIf ? *skip == 0 : *skip != 0)) return;
+    const auto c = pro();
+    double acc[NR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) acc[q] = 0.0;
+    auto elem = [&](const double (&in)[NIN > 0 ? NIN : 1], double (&out)[NO]) {
+        double red[NR];
+        f(c, in, out, red);
+#pragma unroll
+        for (int q = 0; q < NRED; ++q) acc[q] += red[q];
+    };
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * kRedThreads;
+    for (int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; k < np; k += 2 * T) {
+        const int64_t k1 = k + T;
+        const bool h1 = k1 < np;
+        double2 va[NIN > 0 ? NIN : 1], vb[NIN > 0 ? NIN : 1];
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) {
+            va[q] = reinterpret_cast<const double2*>(a.in[q])[k];
+            vb[q] = h1 ? reinterpret_cast<const double2*>(a.in[q])[k1] : make_double2(0.0, 0.0);
+        }
+        double i0[NIN > 0 ? NIN : 1], i1[NIN > 0 ? NIN : 1], o0[NO], o1[NO];
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) {
+            i0[q] = va[q].x;
+            i1[q] = va[q].y;
+        }
+        elem(i0, o0);
+        elem(i1, o1);
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) reinterpret_cast<double2*>(a.out[q])[k] = make_double2(o0[q], o1[q]);
+        if (h1) {
+#pragma unroll
+            for (int q = 0; q < NIN; ++q) {
+                i0[q] = vb[q].x;
+                i1[q] = vb[q].y;
+            }
+            elem(i0, o0);
+            elem(i1, o1);
+#pragma unroll
+            for (int q = 0; q < NOUT; ++q) reinterpret_cast<double2*>(a.out[q])[k1] = make_double2(o0[q], o1[q]);
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        double i0[NIN > 0 ? NIN : 1], o0[NO];
+#pragma unroll
+        for (int q = 0; q < NIN; ++q) i0[q] = a.in[q][n - 1];
+        elem(i0, o0);
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) a.out[q][n - 1] = o0[q];
+    }
+    if (NRED > 0) {
+        double total[NR];
+        if (grid_reduce_last_n<NR>(acc, ws, total) && threadIdx.x == 0) epi(total);
+    }
+}
+
+inline bool vmap_ok(std::initializer_list<const void*> ptrs) {
+    for (const void* p : ptrs)
+        if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+    return true;
+}
+
+template <int NIN, int NOUT, int NRED, bool kRunIf = false, typename Pro, typename F, typename Epi>
+int launch_vmap(int64_t n, VecArgs<NIN, NOUT> a, Pro pro, F f, Epi epi, void* ws, const int* skip, cudaStream_t st) {
+    vmap_kernel<NIN, NOUT, NRED, kRunIf><<<vmap_grid(n), kRedThreads, 0, st>>>(n, a, pro, f, epi, red_ws(ws), skip);
     WK_LAUNCH_CHECK();
     return 0;
 }
