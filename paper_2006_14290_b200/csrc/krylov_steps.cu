@@ -288,7 +288,15 @@ static int gmres_init_finish(GS* s, double tol, int64_t max_iters, int restart, 
 }
 
 static int gmres_cycle_start(int64_t n, const double* r, double* V0, double* g, GS* s, cudaStream_t st) {
-    WK_TRY(launch_masked_map(n, [=] __device__(int64_t i) { V0[i] = r[i] / s->beta; }, &s->done, st));
+    int rc;
+    if (n > 0 && vmap_ok({r, V0}))
+        rc = launch_vmap<1, 1, 0>(
+            n, VecArgs<1, 1>{{r}, {V0}}, [=] __device__() { return s->beta; },
+            [] __device__(double beta, const double(&in)[1], double(&out)[1], double(&)[1]) { out[0] = in[0] / beta; },
+            NoEpi<1>{}, nullptr, &s->done, st);
+    else
+        rc = launch_masked_map(n, [=] __device__(int64_t i) { V0[i] = r[i] / s->beta; }, &s->done, st);
+    if (rc) return rc;
     return launch_scalar([=] __device__() {
         if (s->done) return;
         for (int i = 0; i <= s->restart; ++i) g[i] = 0.0;
@@ -509,6 +517,11 @@ static int gmres_givens(int j, double* H, double* cs_, double* sn_, double* g, G
 }
 
 static int gmres_next_basis(int64_t n, const double* w, double* Vn, GS* s, cudaStream_t st) {
+    if (n > 0 && vmap_ok({w, Vn}))
+        return launch_vmap<1, 1, 0>(
+            n, VecArgs<1, 1>{{w}, {Vn}}, [=] __device__() { return s->hn; },
+            [] __device__(double hn, const double(&in)[1], double(&out)[1], double(&)[1]) { out[0] = in[0] / hn; },
+            NoEpi<1>{}, nullptr, &s->cycle_done, st);
     return launch_masked_map(n, [=] __device__(int64_t i) { Vn[i] = w[i] / s->hn; }, &s->cycle_done, st);
 }
 
@@ -539,6 +552,15 @@ static int gmres_residual(int64_t n, const double* b, const double* w, double* r
         return launch_scalar([=] __device__() {
             if (!s->done) s->sq = 0.0;
         }, st);
+    if (vmap_ok({b, w, r}))
+        return launch_vmap<2, 1, 1>(
+            n, VecArgs<2, 1>{{b, w}, {r}}, NoScalars{},
+            [] __device__(int, const double(&in)[2], double(&out)[1], double(&red)[1]) {
+                const double ri = __dadd_rn(in[0], -in[1]);
+                out[0] = ri;
+                red[0] = __dmul_rn(ri, ri);
+            },
+            [=] __device__(double(&t)[1]) { s->sq = t[0]; }, ws, &s->done, st);
     return launch_map_reduce(
         n,
         [=] __device__(int64_t i) {
