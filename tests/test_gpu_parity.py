@@ -688,6 +688,61 @@ def test_reduce_microbench(wk, ex, shared):
 # ---- BiCGSTAB / GMRES (no reference: vs the oracle restatement) ----------------------------------
 
 
+@pytest.mark.parametrize("n", [1, 7, 1000, 300001])
+def test_bicg_steps_vector_and_scalar_paths(wk, rng, n):
+    """The BiCGSTAB step kernels take the vectorised path (vmap_kernel) for
+    16-byte aligned vectors and the scalar map/reduce path otherwise: same
+    element arithmetic (bitwise vectors), dots within 1e-13 relative; the
+    half-step x update runs only while apply_half is set and clears it."""
+    import ctypes
+
+    from paper_2006_14290_b200 import _lib
+
+    L = _lib.load()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    ws = torch.zeros(int(L.wk_reduce_workspace_bytes()), dtype=torch.uint8, device="cuda")
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    host = {k: rng.standard_normal(n) for k in ("x", "p", "sv", "t", "r", "v", "rh")}
+
+    def run(offset):
+        buf = {k: torch.zeros(n + 2, dtype=torch.float64, device="cuda") for k in host}
+        vec = {k: buf[k][offset: offset + n] for k in host}
+        for k in host:
+            vec[k].copy_(torch.from_numpy(host[k]))
+        h = _lib.WkBicgState()
+        h.alpha, h.omega, h.beta, h.apply_half = 0.37, -1.25, 0.81, 1
+        state = torch.frombuffer(bytearray(bytes(h)), dtype=torch.uint8).to("cuda")
+        S = P(state)
+        _lib.check(L.wk_bicg_update_xr(n, P(vec["p"]), P(vec["sv"]), P(vec["t"]), P(vec["x"]), P(vec["r"]), S,
+                                       P(ws), st), "xr")
+        _lib.check(L.wk_bicg_update_p(n, P(vec["r"]), P(vec["v"]), P(vec["p"]), S, st), "p")
+        _lib.check(L.wk_bicg_update_s(n, P(vec["r"]), P(vec["v"]), P(vec["sv"]), S, P(ws), st), "s")
+        _lib.check(L.wk_bicg_tt_ts(n, P(vec["t"]), P(vec["sv"]), S, P(ws), st), "tt")
+        _lib.check(L.wk_bicg_rho(n, P(vec["rh"]), P(vec["r"]), S, P(ws), st), "rho")
+        _lib.check(L.wk_bicg_rv(n, P(vec["rh"]), P(vec["v"]), S, P(ws), st), "rv")
+        _lib.check(L.wk_bicg_half_x(n, P(vec["p"]), P(vec["x"]), S, P(ws), st), "half")
+        x_after_one = vec["x"].clone()
+        _lib.check(L.wk_bicg_half_x(n, P(vec["p"]), P(vec["x"]), S, P(ws), st), "half again")  # flag now clear
+        torch.cuda.synchronize()
+        out = _lib.WkBicgState.from_buffer_copy(bytes(state.cpu().numpy()))
+        assert out.apply_half == 0 and torch.equal(vec["x"], x_after_one)
+        return {k: vec[k].cpu().numpy() for k in ("x", "r", "p", "sv")}, out
+
+    va, sa = run(0)   # aligned: vectorised
+    vs, ss = run(1)   # offset by one element: scalar fallback
+    for k in va:
+        assert va[k].tobytes() == vs[k].tobytes(), k
+    for f in ("rr", "ss", "tt", "ts", "rho_new", "rv"):
+        a, b = getattr(sa, f), getattr(ss, f)
+        assert abs(a - b) <= 1e-13 * max(1.0, abs(b)), f
+    # element arithmetic against numpy (kernels.py-style separate roundings)
+    x0, p0, sv0, t0 = host["x"], host["p"], host["sv"], host["t"]
+    x1 = (x0 + 0.37 * p0) + (-1.25) * sv0
+    r1 = sv0 - (-1.25) * t0
+    assert np.array_equal(va["r"], r1)
+    assert np.allclose(va["x"], x1 + 0.37 * (r1 + 0.81 * (p0 - (-1.25) * host["v"])), rtol=0, atol=1e-12)
+
+
 @pytest.mark.parametrize("grid", [12, 11])
 @pytest.mark.parametrize("solver", ["bicgstab", "gmres"])
 def test_nonsymmetric_solvers_match_oracle(wk, ex, solver, grid):
