@@ -502,7 +502,8 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
     if (strategy == WK_CSR_LOAD_BALANCE) {
         WK_REQUIRE(merge_plan != nullptr, WK_ERR_INVALID,
                    "csr load_balance strategy needs a plan (wk_csr_load_balance_plan_build)");
-        // skip-aware zero fill: the boundary rows are added atomically
+        // skip-aware zero fill: rows without entries are never stored by the
+        // kernel (every other row is stored once, by the range closing it)
         if (skip == nullptr) {
             WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
         } else {

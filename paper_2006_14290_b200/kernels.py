@@ -39,6 +39,11 @@ def spmv_device(d, x, y=None, stream=None):
 
 
 def _launches(d):
+    """Kernels one SpMV enqueues: COO zero-fill + seg8, Hybrid ELL + COO
+    part, CSR load_balance zero-fill + seg8 + range fix-up, merge tiles +
+    fix-up; one otherwise."""
+    if d.fmt == "csr":
+        return {_lib.WK_CSR_LOAD_BALANCE: 3, _lib.WK_CSR_MERGE: 2}.get(d.strategy, 1)
     return {"coo": 2, "hybrid": 2}.get(d.fmt, 1)
 
 
