@@ -214,7 +214,21 @@ def cpu_sample(budget_s=10.0, steps=None):
               f"({m.nrows} rows, {nnz} nnz, full x), SELL-P({SLICE}), {len(times)} reps")
     return {"value": round(2 * nnz / mean / 1e9, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
             "sample": sample, "ms_per_rep": round(mean * 1e3, 3), "impl": "oracle/csrc/oracle.c or_spmv_sellp",
-            "nnz": nnz}, times
+            "nnz": nnz, "host": host_info()}, times
+
+
+def host_info():
+    """CPU model and logical CPU count of the host the CPU baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def cpu_per_config(wk, corpus, D, reps=10):
