@@ -9,13 +9,15 @@ import paper_2006_14290_b200 as wk  # noqa: E402
 from paper_2006_14290_b200 import corpus  # noqa: E402
 from paper_2006_14290_b200 import device as D  # noqa: E402
 
-A = D.csr_to_sellp(corpus.convection_diffusion3d(256), 64)
+grid = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+A = D.csr_to_sellp(corpus.convection_diffusion3d(grid), 64)
 b = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
 ex = wk.make_executor("b200")
 which = sys.argv[1] if len(sys.argv) > 1 else "bicgstab"
 if which == "bicgstab":
-    wk.bicgstab_solve(A, b, 1e-30, 3, ex)
+    wk.bicgstab_solve(A, b, 1e-30, iters, ex)
 else:
-    wk.gmres_solve(A, b, 1e-30, 3, ex, restart=30)
+    wk.gmres_solve(A, b, 1e-30, iters, ex, restart=30)
 torch.cuda.synchronize()
 print("ok")
