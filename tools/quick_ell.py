@@ -24,12 +24,17 @@ def t(d, x, n=20):
     return round(ms, 4), round(d.algorithmic_bytes() / ms / 1e6, 1), y
 
 
-A = corpus.stencil3d(200, 27)
+pts = int(sys.argv[1]) if len(sys.argv) > 1 else 27
+grid = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+A = corpus.stencil3d(grid, pts)
 x = torch.rand(A.ncols, dtype=torch.float64, device='cuda')
 E = D.csr_to_ell(A)
+S = D.csr_to_sellp(A, 64)
 del A
+print("sellp", t(S, x)[:2], flush=True)
+del S
 ref = None
-for k in (0, 1, 2, 3, 4, 2):
+for k in (0, 2, 3, 4):
     _lib.call("wk_config_set", b"ell_kernel", k)
     ms, gbs, y = t(E, x)
     if ref is None:
