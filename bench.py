@@ -255,6 +255,23 @@ def cpu_per_config(wk, corpus, D, reps=10):
     m = corpus_ref.poisson2d(1000)
     spmv_rate(native.Prepared(m), np.random.default_rng(42).random(m.ncols), int(m.row_ptrs[-1]),
               "cfg1_csr_poisson2d_1000", "whole matrix, or_spmv_csr")
+    # config 1 with the reference AS SHIPPED (warpkit's pure-Python sequential
+    # oracle, one core) on the first 100k rows, when the offline install of the
+    # reference (baseline/_ref) is present
+    ref = _shipped_reference()
+    if ref is not None:
+        rows = 100_000
+        e = int(m.row_ptrs[rows])
+        sub = ref.sparse.CsrMatrix(rows, m.ncols, np.asarray(m.row_ptrs[: rows + 1], np.int64),
+                                   np.asarray(m.col_idx[:e], np.int64), np.asarray(m.values[:e], np.float64))
+        x1 = np.random.default_rng(42).random(m.ncols)
+        t0 = time.perf_counter()
+        ref.sparse.dense_spmv_reference(sub, x1)
+        sec = time.perf_counter() - t0
+        res["cfg1_reference_as_shipped"] = {
+            "GFLOP/s": round(2 * e / sec / 1e9, 5), "ms": round(sec * 1e3, 1), "cores": 1, "kind": "reference",
+            "sample": f"warpkit.sparse.dense_spmv_reference on the first {rows} rows ({e} nnz) of the "
+                      f"5-point Poisson 1000^2 matrix (pure Python, sparse.py:367-430)"}
     # config 3: COO R-MAT scale 24, the first 32M sorted entries (the dense rows)
     R = corpus.rmat(RMAT_SCALE)
     k = min(R.nnz, 32 << 20)
@@ -282,6 +299,21 @@ def cpu_per_config(wk, corpus, D, reps=10):
                           "ms": round(sec * 1e3, 1), "cores": threads, "kind": "port",
                           "sample": f"{its} iterations of the whole system, or_cg_sellp"}
     return res
+
+
+def _shipped_reference():
+    """warpkit from the offline install baseline/_ref (None if absent)."""
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(root, "warpkit")):
+        return None
+    if root not in sys.path:
+        sys.path.append(root)
+    try:
+        import warpkit
+        import warpkit.sparse  # noqa: F401
+    except Exception:
+        return None
+    return warpkit
 
 
 def run_reference(args, rank):
