@@ -95,7 +95,8 @@ __device__ void scatter_block(int64_t nrows, int64_t r0, int64_t nrb_slots, int6
     const int64_t cnt = src_hi - src_lo;
     const bool staged = cnt <= kStageCap && nrb_slots <= kConvThreads * 4;
     if (staged) {
-        for (int64_t i = threadIdx.x; i <= nreal; i += kConvThreads) s_ptr[i] = ptrs[r0 + i] - int(src_lo);
+        // (no row pointers to stage for a block of padding rows only: r0 may lie past nrows)
+        for (int64_t i = threadIdx.x; nreal > 0 && i <= nreal; i += kConvThreads) s_ptr[i] = ptrs[r0 + i] - int(src_lo);
         for (int64_t i = threadIdx.x; i < cnt; i += kConvThreads) {
             s_col[i] = __ldcs(col + src_lo + i);
             s_val[i] = __ldcs(val + src_lo + i);
@@ -206,7 +207,8 @@ fill_tma_kernel(int64_t nrows, int log2r, int64_t ntiles, const int* __restrict_
     // row pointers of the next tile are loaded one iteration ahead (registers)
     auto load_ptrs = [&](int64_t t, int& p0, int& p1) {
         const int64_t r0 = t * R, nreal = t < ntiles ? real_rows(r0) : 0;
-        p0 = tid <= nreal ? ptrs[r0 + tid] : 0;
+        // nothing to read past the last tile or for tiles of padding rows only
+        p0 = (nreal > 0 && tid <= nreal) ? ptrs[r0 + tid] : 0;
         p1 = (tid == 0 && R <= nreal) ? ptrs[r0 + R] : 0;  // entry R (thread 0), R == blockDim
     };
     int p0, p1;

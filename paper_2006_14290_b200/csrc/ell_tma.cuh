@@ -62,6 +62,7 @@ ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
                 const int st = int(i % S);
                 if (i >= uint32_t(S)) mbar_wait(empty + st, ((i / S) - 1) & 1);
                 const int nj = (width - int64_t(c) * J < J) ? int(width - int64_t(c) * J) : J;
+                fence_proxy_async_smem();  // the consumers' reads of this stage before the new bulk writes
                 mbar_arrive_expect_tx(full + st, uint32_t(nj) * uint32_t(cnt) * 12u);
                 for (int jj = 0; jj < nj; ++jj) {
                     const int64_t off = (int64_t(c) * J + jj) * stride + base;
