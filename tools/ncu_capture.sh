@@ -19,6 +19,7 @@ cap() {  # name kernel-regex skip count cmd...
 cap sellp_spmv sellp64_tma 2 1 python tools/profile_spmv.py sellp 27 200
 cap sellp_spmv_7pt sellp64_tma 2 1 python tools/profile_spmv.py sellp 7 256
 cap ell_spmv ell_tma_kernel 2 1 python tools/profile_spmv.py ell 27 200
+cap ell_spmv_7pt ell_tma_kernel 2 1 python tools/profile_spmv.py ell 7 256
 cap csr_rowblock csr_rowblock 2 1 python tools/profile_spmv.py csr 27 200 rowblock
 cap csr_stream "csr_(stream|tma)" 2 1 python tools/profile_spmv.py csr 27 200 stream
 cap csr_rmat seg8 2 1 python tools/profile_spmv.py csr_rmat 0 24 load_balance
