@@ -165,7 +165,8 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         __syncthreads();
     }
 
-    uint32_t i = 0;  // chunks consumed by this warp
+    int cst = 0;            // ring stage of the next chunk
+    uint32_t cphase = 0;    // its mbarrier phase parity
     double dacc = 0.0;
     int cw = 0, cwn = 0;  // consumer: this slice's width and the next one's (read ahead)
     if (!kEll) {
@@ -189,8 +190,8 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         }
         double a0 = 0.0, a1 = 0.0;
         for (int j0 = 0; j0 < w; j0 += J) {
-            const int st = int(i % S);
-            mbar_wait(bars + st, (i / S) & 1);
+            const int st = cst;
+            mbar_wait(bars + st, cphase);
             const int nj = (w - j0 < J) ? w - j0 : J;
             const double* v = sval + st * CH + 2 * lane;
             const int* c = scol + st * CH + 2 * lane;
@@ -205,7 +206,10 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
                 if (lane == 0) fence_proxy_async_smem();
                 issue(st);
             }
-            ++i;
+            if (++cst == S) {
+                cst = 0;
+                cphase ^= 1u;
+            }
         }
         if (r0 + 1 < nrows) {
             __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
