@@ -27,11 +27,14 @@ struct EllTmaCfg {
     static constexpr size_t kSmem = size_t(S) * J * kRows * (sizeof(double) + sizeof(int)) + 2 * S * 8;
 };
 
-template <class Cfg>
+// kDot (CG): also p.q over the owned rows into the DotEpilogue (x = p);
+// rev: tiles walked from the last one (CG's L2 ping-pong, krylov.cu).
+template <class Cfg, bool kDot = false>
 __global__ void __launch_bounds__(Cfg::kT + 32, Cfg::kCtas)
 ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* __restrict__ col,
                const double* __restrict__ val, const int* __restrict__ row_lengths, const double* __restrict__ x,
-               double* __restrict__ y, const int* __restrict__ skip) {
+               double* __restrict__ y, const int* __restrict__ skip,
+               DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int rev = 0) {
     constexpr int J = Cfg::kJ, S = Cfg::kS, T = Cfg::kT, R = Cfg::kRows;
     if (skip != nullptr && *skip) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -50,12 +53,15 @@ ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
     __syncthreads();
     const int64_t ntiles = (nrows + R - 1) / R;
     const int nchunks = int((width + J - 1) / J);
+    auto TL = [&](int64_t k) -> int64_t { return rev ? ntiles - 1 - k : k; };
+    double dacc = 0.0;
 
     if (tid >= T) {  // producer warp: lane 0 streams the (tile, chunk) sequence
-        if (tid != T) return;
+        if (tid == T) {
         const uint64_t pol = policy_evict_first();
         uint32_t i = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int64_t tk = blockIdx.x; tk < ntiles; tk += gridDim.x) {
+            const int64_t tile = TL(tk);
             const int64_t base = tile * R;
             const int64_t cnt = (stride - base < R) ? stride - base : R;  // multiple of 4 (stride % 4 == 0)
             for (int c = 0; c < nchunks; ++c, ++i) {
@@ -73,13 +79,15 @@ ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
                 }
             }
         }
-        return;
-    }
+        }
+        if (!kDot) return;
+    } else {
 
     const int lane = tid & 31;
     const bool finite0 = ncols == 0 || isfinite(__ldg(x));
     uint32_t i = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t tk = blockIdx.x; tk < ntiles; tk += gridDim.x) {
+        const int64_t tile = TL(tk);
         const int64_t r0 = tile * R + 2 * tid;
         const bool ok0 = r0 < nrows, ok1 = r0 + 1 < nrows;
         const bool partial = (tile + 1) * R > nrows;
@@ -105,29 +113,50 @@ ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + st);
         }
-        if (ok1)
+        if (ok1) {
             __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
-        else if (ok0)
+            if (kDot) {
+                const double2 p = *reinterpret_cast<const double2*>(x + r0);
+                dacc += __dmul_rn(p.x, a0);
+                dacc += __dmul_rn(p.y, a1);
+            }
+        } else if (ok0) {
             st_stream(y + r0, a0);
+            if (kDot) dacc += __dmul_rn(x[r0], a0);
+        }
+    }
+    }
+    if (kDot) {
+        RedWorkspace ws{dot.partials, dot.ticket};
+        double total;
+        if (grid_reduce_last<T + 32>(dacc, ws, total) && threadIdx.x == 0) {
+            if (dot.peer != nullptr) {
+                peer_push_scalar(dot.peer, total);
+            } else {
+                dot.state->pq = total;
+                if (dot.finalize) cg_alpha_step(dot.state);
+            }
+        }
     }
 }
 
-template <class Cfg>
+template <class Cfg, bool kDot = false>
 int launch_ell_tma(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col, const double* val,
-                   const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st) {
+                   const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
+                   DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int rev = 0) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(ell_tma_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        WK_CUDA(cudaFuncSetAttribute(ell_tma_kernel<Cfg, kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
     int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
     const int64_t ntiles = ceil_div(nrows, int64_t(Cfg::kRows));
     if (grid > ntiles) grid = ntiles;
-    ell_tma_kernel<Cfg><<<(unsigned)grid, Cfg::kT + 32, Cfg::kSmem, st>>>(nrows, ncols, width, stride, col, val,
-                                                                         row_lengths, x, y, skip);
+    ell_tma_kernel<Cfg, kDot><<<(unsigned)grid, Cfg::kT + 32, Cfg::kSmem, st>>>(nrows, ncols, width, stride, col,
+                                                                               val, row_lengths, x, y, skip, dot, rev);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -276,6 +276,16 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
 // SpMV + separate dot), 0 on success, an error code otherwise.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
                    cudaStream_t st, void* peer, const void* halo, int rev) {
+    if (A->format == WK_FMT_ELL && halo == nullptr && ell_kernel_choice() >= 2 && A->stride % 4 == 0 &&
+        A->width > 0 && aligned(A->values, 16) && aligned(A->col_idx, 16) && aligned(q, 16) && aligned(p, 16) &&
+        A->nrows > 0) {
+        char* w = reinterpret_cast<char*>(red_ws);
+        DotEpilogue dot{reinterpret_cast<double*>(w),
+                        reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
+                        reinterpret_cast<PeerCtx*>(peer), nullptr};
+        return launch_ell_tma<EllTmaCfg<4, 4, 448, 1>, true>(A->nrows, A->ncols, A->width, A->stride, A->col_idx,
+                                                            A->values, A->row_lengths, p, q, &s->done, st, dot, rev);
+    }
     if (A->format != WK_FMT_SELLP || A->slice_size != 64 || sellp_kernel_choice() == 0 || !aligned(A->values, 16) ||
         !aligned(A->col_idx, 16) || !aligned(q, 16) || !aligned(p, 16) || A->nrows == 0)
         return 1;
