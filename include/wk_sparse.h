@@ -436,6 +436,9 @@ typedef struct wk_peer_halo {
     int64_t dst_off[8];         /* ... at this byte offset of its arena             */
     int32_t nrecv;
     int32_t recv_peer[8];
+    int64_t int_lo, int_hi;     /* slices [int_lo, int_hi) of the local SELL-P matrix
+                                   gather no halo column: the fused SpMV folds them
+                                   before waiting for the halo (empty range: wait first) */
 } wk_peer_halo;
 int wk_cg_spmv_dot_peer(const wk_matrix* A, const double* p, double* q, wk_cg_state* state, void* workspace,
                         void* peer, const void* halo, wk_stream_t stream);

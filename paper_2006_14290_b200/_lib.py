@@ -53,7 +53,7 @@ class WkPeerHalo(ctypes.Structure):
     """Mirror of `wk_peer_halo` (include/wk_sparse.h)."""
 
     _fields_ = [("n", I32), ("peer", I32 * 8), ("lo", I64 * 8), ("hi", I64 * 8), ("dst_off", I64 * 8),
-                ("nrecv", I32), ("recv_peer", I32 * 8)]
+                ("nrecv", I32), ("recv_peer", I32 * 8), ("int_lo", I64), ("int_hi", I64)]
 
 
 class WkMatrix(ctypes.Structure):

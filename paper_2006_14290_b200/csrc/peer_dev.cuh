@@ -87,6 +87,7 @@ struct PeerHalo {
     long long dst_off[kHaloMax];
     int nrecv;
     int recv_peer[kHaloMax];
+    long long int_lo, int_hi;  // SELL-P slices [int_lo, int_hi) of the local matrix gather no halo column
 };
 
 __device__ __forceinline__ void halo_store(const PeerCtx* c, const PeerHalo* h, long long i, double v) {

@@ -158,11 +158,16 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     };
     seek();
     for (int st = 0; st < S && pvalid; ++st) issue(st);
-    if (kDot && dot.halo != nullptr) {
-        // the matrix stream is already in flight; the x gathers wait for the
-        // neighbours' halo stores (peer-memory distributed CG)
-        if (threadIdx.x == 0) halo_wait(dot.peer, dot.halo);
-        __syncthreads();
+    // peer-memory distributed CG: the neighbours push the halo of x while this
+    // kernel runs. Slices in [int_lo, int_hi) gather no halo column, so a warp
+    // waits for the halo flags only before its first slice outside that range:
+    // interior rows overlap the exchange, boundary rows run after arrival.
+    // The slice order (and so every sum) is the same as without a halo.
+    bool halo_pending = kDot && dot.halo != nullptr;
+    int64_t int_lo = 0, int_hi = 0;
+    if (halo_pending) {
+        int_lo = dot.halo->int_lo;
+        int_hi = dot.halo->int_hi;
     }
 
     int cst = 0;            // ring stage of the next chunk
@@ -183,6 +188,11 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         }
         const int64_t r0 = SP(s) * 64 + 2 * lane;
         const bool partial = kEll && (SP(s) + 1) * 64 > nrows;
+        if (kDot && halo_pending && (SP(s) < int_lo || SP(s) >= int_hi)) {
+            if (lane == 0) halo_wait(dot.peer, dot.halo);
+            __syncwarp();
+            halo_pending = false;
+        }
         int len0 = w, len1 = w;
         if (!finite0) {
             len0 = r0 < nrows ? row_lengths[r0] : 0;

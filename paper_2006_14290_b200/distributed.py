@@ -317,9 +317,32 @@ class DistOperator:
         h.nrecv = len(self._peer_recv)
         for j, q in enumerate(self._peer_recv):
             h.recv_peer[j] = q
+        h.int_lo, h.int_hi = self._interior_slices()
         t = torch.frombuffer(bytearray(bytes(h)), dtype=torch.uint8).to(self.ops.device)
         self._halo_keep = getattr(self, "_halo_keep", []) + [t]
         return t
+
+    def _interior_slices(self):
+        """Longest run [lo, hi) of local SELL-P slices with no halo column
+        (entries with column >= n_local); (0, 0) when unknown or empty. The
+        fused SpMV folds those before waiting for the halo."""
+        L = self.local
+        if getattr(L, "fmt", None) != "sellp" or L.nrows == 0:
+            return 0, 0
+        if getattr(self, "_int_range", None) is None:
+            ss = int(L.slice_size)
+            nsl = (L.nrows + ss - 1) // ss
+            idx = torch.nonzero(L.col_idx >= self.n_local).flatten()
+            if idx.numel() == 0:
+                self._int_range = (0, nsl)
+            else:
+                starts = L.slice_sets.to(torch.int64) * ss
+                sl = torch.searchsorted(starts, idx.to(torch.int64), right=True) - 1
+                pts = np.concatenate(([-1], torch.unique(sl).cpu().numpy(), [nsl]))
+                gaps = np.diff(pts) - 1
+                g = int(np.argmax(gaps))
+                self._int_range = (int(pts[g] + 1), int(pts[g + 1])) if gaps[g] > 0 else (0, 0)
+        return self._int_range
 
     def arena_mark(self):
         """Allocation mark of the peer arena (None without the peer path)."""

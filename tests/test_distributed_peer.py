@@ -61,6 +61,8 @@ def _worker(rank, world, port, out):
         opg = DI.stencil_slab_operator(12, 12, None, corpus.points_7pt(), dist, fmt="sellp", weak=False,
                                        nz=12).enable_peer()
         b = torch.ones(opg.n_local, dtype=torch.float64, device="cuda")
+        res["int_range"] = opg._interior_slices()
+        res["nslices"] = (opg.local.nrows + 63) // 64
         for graph in (False, True):
             xs, hist = DI.cg_solve(opg, b, 1e-12, 500, graph=graph)  # all-reduces fused into the CG kernels
             res[f"cg_x_{graph}"], res[f"cg_hist_{graph}"] = xs.cpu().numpy(), hist.cpu().numpy()
@@ -114,6 +116,15 @@ def test_peer_allreduce_rank_order(parts):
     want = (0.0 + (v * 1 + 0.125)) + (v * 2 + 0.125)
     for p in parts:
         assert p["allreduce"].tobytes() == want.tobytes()
+
+
+def test_peer_interior_slices(parts):
+    """Each rank of the 2-rank z-slab split has halo columns in one boundary
+    plane only: the interior-first range covers all other slices."""
+    for p in parts:
+        lo, hi = p["int_range"]
+        assert 0 <= lo < hi <= p["nslices"]
+        assert hi - lo >= p["nslices"] - (12 * 12 + 63) // 64 - 1
 
 
 def test_peer_cg_graph(parts):
