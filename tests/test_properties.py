@@ -107,3 +107,56 @@ def test_device_conversions_and_spmv(m, ss):
             assert np.array_equal(y, y_ref)
         else:
             assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= 1e-12
+
+
+@st.composite
+def spd_systems(draw):
+    """Random sparse symmetric strictly diagonally dominant (hence SPD) systems."""
+    n = draw(st.integers(1, 300))
+    m = draw(st.integers(0, 4 * n))
+    i = draw(st.lists(st.integers(0, n - 1), min_size=m, max_size=m))
+    j = draw(st.lists(st.integers(0, n - 1), min_size=m, max_size=m))
+    v = draw(st.lists(st.floats(-1.0, 1.0, allow_nan=False, width=64), min_size=m, max_size=m))
+    seed = draw(st.integers(0, 2**31 - 1))
+    return n, i, j, v, seed
+
+
+@pytest.mark.gpu
+@settings(max_examples=30, deadline=None, suppress_health_check=[HealthCheck.too_slow,
+                                                                 HealthCheck.function_scoped_fixture])
+@given(sys_=spd_systems(), fmt=st.sampled_from(["sellp", "csr", "ell"]))
+def test_cg_random_spd(sys_, fmt):
+    """CG (wk_cg_solve: device loop, CUDA graph, L2 ping-pong) on random SPD
+    systems against the oracle CG (kernels.py:283-331 update order): same
+    starting residual, converged to the tolerance, iteration counts within
+    one (dot summation orders differ), solutions within 1e-8."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2006_14290_b200 as wk
+    from oracle import krylov_ref
+
+    n, i, j, v, seed = sys_
+    rows = np.concatenate([np.asarray(i, np.int64), np.asarray(j, np.int64), np.arange(n)])
+    cols = np.concatenate([np.asarray(j, np.int64), np.asarray(i, np.int64), np.arange(n)])
+    vals = np.concatenate([np.asarray(v), np.asarray(v), np.zeros(n)])
+    off = np.zeros(n)
+    np.add.at(off, rows[: 2 * len(i)], np.abs(vals[: 2 * len(i)]))
+    vals[2 * len(i):] = off + 1.0  # strict diagonal dominance
+    ref_coo = sparse_ref.coo_from_entries(n, n, rows, cols, vals)
+    ref_csr = sparse_ref.coo_to_csr(ref_coo)
+    ex = wk.make_executor("b200", device=0)
+    coo = wk.CooMatrix(n, n, ref_coo.row_idx, ref_coo.col_idx, ref_coo.values)
+    A = {"sellp": lambda: wk.coo_to_sellp(coo, 64, ex), "csr": lambda: wk.coo_to_csr(coo, ex),
+         "ell": lambda: wk.csr_to_ell(wk.coo_to_csr(coo, ex), exec=ex)}[fmt]()
+    b = np.random.default_rng(seed).standard_normal(n)
+    tol = 1e-10
+    x, hist = wk.cg_solve(A, b, tol, 1000, ex)
+    xr, hr = krylov_ref.cg_solve(lambda z: sparse_ref.spmv(ref_csr, z), b, tol, 1000)
+    x = x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+    hist = hist.cpu().numpy() if hasattr(hist, "cpu") else np.asarray(hist)
+    assert abs(hist[0] - hr[0]) <= 1e-14 * hr[0]
+    assert abs(len(hist) - len(hr)) <= 1
+    bn = float(np.linalg.norm(b))
+    assert hist[-1] <= tol * bn or len(hist) - 1 == 1000
+    assert np.max(np.abs(x - xr)) <= 1e-8 * max(1.0, float(np.max(np.abs(xr))))
