@@ -53,7 +53,7 @@ ell_tma_kernel(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
     __syncthreads();
     const int64_t ntiles = (nrows + R - 1) / R;
     const int nchunks = int((width + J - 1) / J);
-    auto TL = [&](int64_t k) -> int64_t { return rev ? ntiles - 1 - k : k; };
+    auto TL = [&](int64_t k) -> int64_t { return (kDot && rev) ? ntiles - 1 - k : k; };
     double dacc = 0.0;
 
     if (tid >= T) {  // producer warp: lane 0 streams the (tile, chunk) sequence
