@@ -35,6 +35,11 @@ def lib():
         L.or_cg_sellp.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, ctypes.c_double, _I64, _P, _P,
                                   ctypes.c_int]
         L.or_cg_sellp.restype = _I64
+        L.or_bicgstab_csr.argtypes = [_I64, _P, _P, _P, _P, ctypes.c_double, _I64, _P, _P, ctypes.c_int]
+        L.or_bicgstab_csr.restype = _I64
+        L.or_gmres_csr.argtypes = [_I64, _P, _P, _P, _P, ctypes.c_double, _I64, _I64, _P, _P,
+                                   ctypes.c_int]
+        L.or_gmres_csr.restype = _I64
         _lib = L
     return _lib
 
@@ -98,6 +103,31 @@ class Prepared:
                                _p(self.lengths), _p(b), tol, max_iters, _p(x), _p(hist), nthreads)
         if it < 0:
             raise RuntimeError("CG breakdown")
+        return x, hist[: it + 1]
+
+
+    def bicgstab(self, b, tol, max_iters, nthreads=0):
+        """krylov_ref.bicgstab_solve in C (CSR operator)."""
+        assert self.kind == "csr"
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.nrows, dtype=np.float64)
+        hist = np.empty(max_iters + 1, dtype=np.float64)
+        it = lib().or_bicgstab_csr(self.nrows, _p(self.ptrs), _p(self.col), _p(self.val), _p(b), tol,
+                                   max_iters, _p(x), _p(hist), nthreads)
+        if it < 0:
+            raise RuntimeError(f"BiCGSTAB breakdown ({it})")
+        return x, hist[: it + 1]
+
+    def gmres(self, b, tol, max_iters, restart=30, nthreads=0):
+        """krylov_ref.gmres_solve in C (CSR operator)."""
+        assert self.kind == "csr"
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty(self.nrows, dtype=np.float64)
+        hist = np.empty(max_iters + 1, dtype=np.float64)
+        it = lib().or_gmres_csr(self.nrows, _p(self.ptrs), _p(self.col), _p(self.val), _p(b), tol,
+                                max_iters, restart, _p(x), _p(hist), nthreads)
+        if it < 0:
+            raise MemoryError("GMRES basis allocation failed")
         return x, hist[: it + 1]
 
 

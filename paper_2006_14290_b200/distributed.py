@@ -481,63 +481,77 @@ def partition_csr(m, comm, fmt="sellp", slice_size=64, ops=None, bounds=None, up
     return DistOperator(comm, bounds, plan, local, len(lv), ops, n)
 
 
-def stencil_slab_operator(nx, ny, nz_local, points, dist=None, fmt="sellp", slice_size=64, weak=True, nz=None):
-    """z-slab partition of a stencil matrix generated on the device.
+class SlabLayout:
+    """z-slab partition of an nx*ny*nzg stencil grid over P ranks (host index
+    logic only, shared by the device operator and the CPU tests).
 
-    weak=True: every rank owns nz_local planes of an nx*ny*(nz_local*P) grid
-    (weak scaling); weak=False: the global grid has `nz` planes split as
-    evenly as possible (strong scaling). Each rank generates only its planes
-    plus one halo plane on each side (the stencils here reach +-1 plane)."""
+    weak=True: every rank owns nz_local planes of an nx*ny*(nz_local*P) grid;
+    weak=False: the global grid has `nz` planes split as evenly as possible.
+    Rank g owns planes [z0, z1) plus one halo plane on each side that exists
+    (the stencils here reach +-1 plane); its extended slab is planes
+    [e0, e1)."""
+
+    def __init__(self, nx, ny, P, g, weak=True, nz_local=None, nz=None):
+        self.plane = plane = nx * ny
+        if weak:
+            self.nzg = nz_local * P
+            zb = [nz_local * q for q in range(P + 1)]
+        else:
+            self.nzg = nz
+            zb = [nz * q // P for q in range(P + 1)]
+        z0, z1 = zb[g], zb[g + 1]
+        self.z0, self.z1 = z0, z1
+        self.has_lo, self.has_hi = z0 > 0, z1 < self.nzg
+        self.e0, self.e1 = z0 - int(self.has_lo), z1 + int(self.has_hi)
+        self.n_local = (z1 - z0) * plane
+        self.lo_rows = int(self.has_lo) * plane     # rows of the extended slab before the owned ones
+        self.n_halo = (int(self.has_lo) + int(self.has_hi)) * plane
+        self.bounds = [z * plane for z in zb]
+        halo_cols, recv, send = [], {}, {}
+        if self.has_lo:
+            halo_cols.append(np.arange((z0 - 1) * plane, z0 * plane, dtype=np.int64))
+            recv[g - 1] = (0, plane)
+            send[g - 1] = np.arange(0, plane, dtype=np.int64)
+        if self.has_hi:
+            halo_cols.append(np.arange(z1 * plane, (z1 + 1) * plane, dtype=np.int64))
+            recv[g + 1] = (int(self.has_lo) * plane, plane)
+            send[g + 1] = np.arange(self.n_local - plane, self.n_local, dtype=np.int64)
+        hc = np.concatenate(halo_cols) if halo_cols else np.zeros(0, np.int64)
+        self.plan = HaloPlan(self.n_local, hc, send, recv)
+
+    def localize(self, col):
+        """Extended-slab column ids (torch int64, any device) -> [owned |
+        halo lo plane | halo hi plane] local ids."""
+        owned_lo, owned_hi, n_local = self.lo_rows, self.lo_rows + self.n_local, self.n_local
+        lcol = col - owned_lo
+        if self.has_lo:
+            lcol = torch.where(col < owned_lo, n_local + col, lcol)
+        if self.has_hi:
+            lcol = torch.where(col >= owned_hi, n_local + self.lo_rows + (col - owned_hi), lcol)
+        return lcol
+
+
+def stencil_slab_operator(nx, ny, nz_local, points, dist=None, fmt="sellp", slice_size=64, weak=True, nz=None):
+    """z-slab partition of a stencil matrix generated on the device (see
+    SlabLayout): each rank generates only its planes plus one halo plane on
+    each side."""
     from . import corpus
 
     comm = Comm(dist)
-    P, g = comm.world, comm.rank
-    plane = nx * ny
-    if weak:
-        nzg = nz_local * P
-        zb = [nz_local * q for q in range(P + 1)]
-    else:
-        nzg = nz
-        zb = [nzg * q // P for q in range(P + 1)]
-    z0, z1 = zb[g], zb[g + 1]
-    has_lo, has_hi = z0 > 0, z1 < nzg
-    e0, e1 = z0 - int(has_lo), z1 + int(has_hi)
-    ext = corpus.stencil(nx, ny, e1 - e0, points)          # device CSR of the extended slab
-    n_local = (z1 - z0) * plane
-    lo_rows = int(has_lo) * plane
-    ptrs = ext.row_ptrs[lo_rows: lo_rows + n_local + 1]
+    lay = SlabLayout(nx, ny, comm.world, comm.rank, weak, nz_local, nz)
+    ext = corpus.stencil(nx, ny, lay.e1 - lay.e0, points)          # device CSR of the extended slab
+    n_local = lay.n_local
+    ptrs = ext.row_ptrs[lay.lo_rows: lay.lo_rows + n_local + 1]
     base = int(ptrs[0].item())
     nnz = int(ptrs[-1].item()) - base
     col = ext.col_idx[base: base + nnz].to(torch.int64)
     val = ext.values[base: base + nnz]
-    # extended-slab column -> [owned | halo lo plane | halo hi plane]
-    owned_lo, owned_hi = lo_rows, lo_rows + n_local
-    lcol = col - owned_lo
-    if has_lo:
-        m = col < owned_lo
-        lcol = torch.where(m, n_local + col, lcol)
-    if has_hi:
-        m = col >= owned_hi
-        lcol = torch.where(m, n_local + lo_rows + (col - owned_hi), lcol)
-    n_halo = (int(has_lo) + int(has_hi)) * plane
-    dcsr = D.DeviceCsr(n_local, n_local + n_halo, (ptrs - base).contiguous(), lcol.to(torch.int32).contiguous(),
+    lcol = lay.localize(col)
+    dcsr = D.DeviceCsr(n_local, n_local + lay.n_halo, (ptrs - base).contiguous(), lcol.to(torch.int32).contiguous(),
                        val.contiguous())
     del ext
     local = _convert_local(dcsr, fmt, slice_size)
-    bounds = [z * plane for z in zb]
-    halo_cols = []
-    recv, send = {}, {}
-    if has_lo:
-        halo_cols.append(np.arange((z0 - 1) * plane, z0 * plane, dtype=np.int64))
-        recv[g - 1] = (0, plane)
-        send[g - 1] = np.arange(0, plane, dtype=np.int64)
-    if has_hi:
-        halo_cols.append(np.arange(z1 * plane, (z1 + 1) * plane, dtype=np.int64))
-        recv[g + 1] = (int(has_lo) * plane, plane)
-        send[g + 1] = np.arange(n_local - plane, n_local, dtype=np.int64)
-    hc = np.concatenate(halo_cols) if halo_cols else np.zeros(0, np.int64)
-    plan = HaloPlan(n_local, hc, send, recv)
-    return DistOperator(comm, bounds, plan, local, nnz, DeviceOps(), nzg * plane)
+    return DistOperator(comm, lay.bounds, lay.plan, local, nnz, DeviceOps(), lay.nzg * lay.plane)
 
 
 # ---- distributed CG -------------------------------------------------------------------------------
