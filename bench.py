@@ -41,7 +41,6 @@ SLICE = 64
 CG_GRID = 256       # config 4
 CG_ITERS = 1000
 RMAT_SCALE = 24     # config 3
-CPU_SAMPLE_PLANES = 25
 
 
 def peaks():
@@ -185,17 +184,38 @@ def load_traffic(name):
 # ---- CPU baseline (oracle C port, all host threads) ---------------------------------------------
 
 
-def cpu_sample(budget_s=10.0, steps=None):
-    """Middle z-slab of the 27-point 200^3 matrix (25 planes, 1M rows, full x),
-    SELL-P(64), folded by oracle/csrc/oracle.c on every host thread."""
-    from oracle import corpus_ref, native, sparse_ref
+def workload_config(rows, nnz, stored, nbytes, world=1):
+    """`config` of the N=1 headline, shared verbatim by the reference arm."""
+    return {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 per GPU (BASELINE config 2)",
+            "rows_per_gpu": int(rows), "nnz_per_gpu": int(nnz), "stored_per_gpu": int(stored),
+            "bytes_per_spmv": int(nbytes),
+            "l2": "operands 2.7 GB/step >> 126 MB L2: no flush needed between steps",
+            "parallelism": f"rowblock{world}"}
 
-    plane = GRID * GRID
-    z0 = GRID // 2 - CPU_SAMPLE_PLANES // 2
-    m = corpus_ref.stencil(GRID, GRID, GRID, corpus_ref.points_27pt(), z0 * plane, (z0 + CPU_SAMPLE_PLANES) * plane)
-    sp = sparse_ref.csr_to_sellp(m, SLICE)
+
+def cpu_matrix():
+    """The whole config-2 matrix (27-point 200^3, SELL-P(64)) built on the
+    host by the oracle's C builders (oracle.native.stencil_csr /
+    csr_to_sellp, equal to the numpy restatements, tests/test_oracle_golden.py)."""
+    from oracle import corpus_ref, native
+
+    m = native.stencil_csr(GRID, GRID, GRID, corpus_ref.points_27pt())
+    sp = native.csr_to_sellp(m, SLICE)
+    nnz = int(m.row_ptrs[-1])
+    del m
+    return sp, nnz
+
+
+def cpu_sample(budget_s=10.0, steps=None, matrix=None):
+    """The reference fold (oracle/csrc/oracle.c or_spmv_sellp: per row
+    acc = 0.0; acc += v * x[c], sparse.py:397-417) of the WHOLE config-2
+    matrix on every host thread; x = default_rng(42).random(n) as the
+    reference's bench (bench.py:233-234)."""
+    from oracle import native
+
+    sp, nnz = matrix if matrix is not None else cpu_matrix()
     prep = native.Prepared(sp)
-    x = np.random.default_rng(42).random(m.ncols)
+    x = np.random.default_rng(42).random(sp.ncols)
     threads = native.max_threads()
     y = prep.spmv(x, nthreads=threads)  # warm-up
     times = []
@@ -208,13 +228,14 @@ def cpu_sample(budget_s=10.0, steps=None):
             break
         if steps is None and time.perf_counter() - t_start > budget_s:
             break
-    nnz = int(m.row_ptrs[-1])
     mean = sum(times) / len(times)
-    sample = (f"rows of z-planes {z0}..{z0 + CPU_SAMPLE_PLANES - 1} of the 27-pt {GRID}^3 matrix "
-              f"({m.nrows} rows, {nnz} nnz, full x), SELL-P({SLICE}), {len(times)} reps")
+    stored = len(sp.values)
+    nbytes = 12 * stored + 8 * (len(sp.slice_sets)) + 8 * sp.ncols + 8 * sp.nrows
+    sample = (f"the whole config-2 matrix ({sp.nrows} rows, {nnz} nnz, {stored} stored), SELL-P({SLICE}), "
+              f"{len(times)} reps")
     return {"value": round(2 * nnz / mean / 1e9, 4), "unit": "GFLOP/s", "cores": threads, "kind": "port",
             "sample": sample, "ms_per_rep": round(mean * 1e3, 3), "impl": "oracle/csrc/oracle.c or_spmv_sellp",
-            "nnz": nnz, "host": host_info()}, times
+            "nnz": nnz, "stored": stored, "bytes_per_spmv": nbytes, "rows": sp.nrows, "host": host_info()}, times
 
 
 def host_info():
@@ -330,8 +351,7 @@ def run_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GFLOP/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 (bounded sample, see cpu_baseline)",
-                   "cpu_threads": base["cores"]},
+        "config": workload_config(base["rows"], base["nnz"], base["stored"], base["bytes_per_spmv"]),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -427,18 +447,14 @@ def run_gpu(args, rank, world, dist):
         else:
             e2e = part.e2e(x, args, timed)
 
+    if world > 1:
+        comm_how = 'NVLink peer stores' if comm_mode == 'peer' else comm_mode.upper()
+        part_desc = f", z-slab partitioned {GRID}x{GRID}x{GRID * world}, halo over {comm_how}"
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"SELL-P({SLICE}) SpMV, 27-point stencil {GRID}^3 per GPU (BASELINE config 2)"
-                               + (f", z-slab partitioned {GRID}x{GRID}x{GRID * world}, halo over "
-                                  f"{'NVLink peer stores' if comm_mode == 'peer' else comm_mode.upper()}"
-                                  if world > 1 else ""),
-                   "rows_per_gpu": n_local, "nnz_per_gpu": int(nnz), "stored_per_gpu": int(A.stored),
-                   "bytes_per_spmv": int(bytes_launch),
-                   "l2": "operands 2.7 GB/step >> 126 MB L2: no flush needed between steps",
-                   "parallelism": f"rowblock{world}"},
+        "config": workload_config(n_local, nnz, A.stored, bytes_launch, world),
         "hbm_gbs": round(bytes_launch * args.steps * world / (total_ms * 1e-3) / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000.0, 4),
@@ -447,7 +463,11 @@ def run_gpu(args, rank, world, dist):
                      "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": int(bytes_launch)},
         "e2e": e2e,
         "gpu_launches": args.steps * (1 if world == 1 else part.launches_per_spmv),
+        **({"partition": part_desc.lstrip(", ")} if world > 1 else {}),
         "clocks": clocks,
+        "comm": {"nranks": world, "backend": str(dist.get_backend()).lower() if dist is not None else None,
+                 "data_path": comm_mode if world > 1 else "none (1 GPU)",
+                 "halo_bytes_per_spmv": int(part.plan.bytes_per_exchange) if world > 1 else 0},
     }
     # extra sections
     if world == 1 and not args.quick:
@@ -462,7 +482,20 @@ def run_gpu(args, rank, world, dist):
         if not args.no_cpu:
             out["cpu_baselines"] = _safe(lambda: cpu_per_config(wk, corpus, D))
     elif world > 1 and not args.quick:
+        # strong scaling of CG 256^3 (north_star: >= 6x at 8 GPUs): the same
+        # solve on rank 0's GPU alone first (the other ranks wait), then
+        # partitioned over all ranks
+        single = None
+        if rank == 0:
+            single = _safe(lambda: bench_cg(args, wk, corpus, D))
+            torch.cuda.empty_cache()
+        barrier(dist)
         out["cg"] = _safe(lambda: part_cg(args, dist, world))
+        if rank == 0 and "it_per_s" in out["cg"] and single and "it_per_s" in single:
+            out["cg"]["single_gpu_it_per_s"] = single["it_per_s"]
+            out["cg"]["speedup_vs_1gpu"] = round(out["cg"]["it_per_s"] / single["it_per_s"], 3)
+            line["cg_strong_it_per_s"] = out["cg"]["it_per_s"]
+            line["cg_strong_speedup_vs_1gpu"] = out["cg"]["speedup_vs_1gpu"]
         torch.cuda.empty_cache()
         out["nonsymmetric"] = _safe(lambda: part_nonsym(args, dist, world))
     line.update(out)
@@ -531,10 +564,23 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
     for strat in ("load_balance", "merge", "stream"):
         Rc.with_strategy(strat, 0)
         rec(f"csr_{strat}_rmat24", Rc, xr)
+    # Hybrid: Ginkgo's minimal-storage width (0 on R-MAT: 56% of the rows are
+    # empty, any ELL slot costs more than the COO entry it replaces) and a
+    # real split, ELL width k = 8 (12kn + 16 rem + 16n)
     H = D.csr_to_hybrid(Rc)
     rec("hybrid_rmat24", H, xr, nnz=R.nnz)
-    res["hybrid_rmat24"]["ell_width"] = H.ell.width
-    res["hybrid_rmat24"]["coo_nnz"] = H.coo.nnz
+    res["hybrid_rmat24"].update(ell_width=H.ell.width, coo_nnz=H.coo.nnz, strategy="minimal_storage")
+    del H
+    torch.cuda.empty_cache()
+    _, per = timed(lambda: D.csr_to_hybrid(Rc, width=8), 3, 1, None)
+    H = D.csr_to_hybrid(Rc, width=8)
+    ms = statistics.mean(per)
+    b = 12 * Rc.nnz + 4 * (Rc.nrows + 1) + 12 * 8 * Rc.nrows + 4 * Rc.nrows + 16 * H.coo.nnz + 8 * (Rc.nrows + 1)
+    res["csr_to_hybrid_k8_rmat24"] = {"ms": round(ms, 3), "GB/s": round(b / (ms * 1e-3) / 1e9, 1), "bytes": int(b),
+                                      "note": "read CSR, write ELL(8) + lengths, COO offsets + remainder; "
+                                              "includes the host sync reading the remainder size"}
+    rec("hybrid_k8_rmat24", H, xr, nnz=R.nnz)
+    res["hybrid_k8_rmat24"].update(ell_width=H.ell.width, ell_real_nnz=int(H.ell.nnz), coo_nnz=H.coo.nnz)
     del R, Rc, H, flush_buf
     torch.cuda.empty_cache()
     return res
@@ -628,6 +674,23 @@ def part_cg(args, dist, world):
     return DI.bench_cg(CG_GRID, CG_ITERS, dist, timed)
 
 
+def _free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a torchrun environment: relaunch
+    this script under torch.distributed.run with N ranks (one per GPU,
+    rendezvous on 127.0.0.1) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -642,8 +705,13 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
+        # host-only arm: rank 0 times the CPU restatement, other ranks exit
         run_reference(args, rank)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus and os.environ.get("WK_DIST_BACKEND", "nccl") == "nccl":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} ranks")
     import torch
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -657,6 +725,9 @@ def main():
         import torch.distributed as tdist
 
         if backend == "nccl":
+            # communicator init lines (rank / nRanks) for the launcher's rank check
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             tdist.init_process_group(backend)

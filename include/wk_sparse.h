@@ -206,6 +206,13 @@ int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs,
 int wk_hybrid_coo_fill(int64_t nrows, int64_t width, const int32_t* row_ptrs, const int32_t* col_idx,
                        const double* values, const int64_t* offsets, int32_t* c_row, int32_t* c_col,
                        double* c_val, wk_stream_t stream);
+/* Host-uploaded SELL-P / ELL: rewrite every slot past row_lengths[r] (and
+ * the rows past nrows of the last slice / of the stride) as the reference
+ * padding (col 0, val 0.0; sparse.py:230-232), in place. */
+int wk_sellp_zero_padding(int64_t nrows, int64_t slice_size, const int64_t* slice_sets, const int32_t* row_lengths,
+                          int32_t* col_idx, double* values, wk_stream_t stream);
+int wk_ell_zero_padding(int64_t nrows, int64_t width, int64_t stride, const int32_t* row_lengths, int32_t* col_idx,
+                        double* values, wk_stream_t stream);
 /* sorted COO -> CSR row_ptrs (sparse.py:212-216) */
 int wk_coo_to_csr_ptrs(int64_t nrows, int64_t nnz, const int32_t* row_idx, int32_t* row_ptrs, wk_stream_t stream);
 /* CSR -> COO row indices */

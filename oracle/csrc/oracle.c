@@ -334,3 +334,87 @@ int64_t or_gmres_csr(int64_t n, const int64_t* ptrs, const int32_t* col, const d
     free(V); free(w); free(r); free(H); free(cs); free(sn); free(g); free(h); free(y);
     return it;
 }
+
+/* ---- matrix construction for the full-size CPU baseline ----------------------------------
+ * corpus_ref.stencil (rows of a constant-coefficient stencil on an
+ * nx*ny*nz grid, points already sorted by linear offset so columns ascend)
+ * and sparse_ref.csr_to_sellp (sparse.py:219-242) in C, so the reference arm
+ * builds BASELINE config 2 (214M entries) in seconds. Checked against the
+ * numpy restatements by tests/test_oracle_golden.py. */
+
+/* pass 1: row lengths of rows [row_lo, row_hi) into ptrs[1..], ptrs[0] = 0;
+ * returns nnz (ptrs becomes the prefix sum). */
+int64_t or_stencil_ptrs(int64_t nx, int64_t ny, int64_t nz, int npts, const int32_t* pts, int64_t row_lo,
+                        int64_t row_hi, int64_t* ptrs, int nthreads) {
+    set_threads(nthreads);
+    int64_t n = row_hi - row_lo;
+    ptrs[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < n; ++q) {
+        int64_t r = row_lo + q, i = r % nx, j = (r / nx) % ny, k = r / (nx * ny), c = 0;
+        for (int p = 0; p < npts; ++p) {
+            int64_t a = i + pts[3 * p], b = j + pts[3 * p + 1], d = k + pts[3 * p + 2];
+            c += (a >= 0 && a < nx && b >= 0 && b < ny && d >= 0 && d < nz);
+        }
+        ptrs[q + 1] = c;
+    }
+    for (int64_t q = 0; q < n; ++q) ptrs[q + 1] += ptrs[q];
+    return ptrs[n];
+}
+
+void or_stencil_fill(int64_t nx, int64_t ny, int64_t nz, int npts, const int32_t* pts, const double* vals,
+                     int64_t row_lo, int64_t row_hi, const int64_t* ptrs, int32_t* col, double* val,
+                     int nthreads) {
+    set_threads(nthreads);
+    int64_t n = row_hi - row_lo;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < n; ++q) {
+        int64_t r = row_lo + q, i = r % nx, j = (r / nx) % ny, k = r / (nx * ny), e = ptrs[q];
+        for (int p = 0; p < npts; ++p) {
+            int64_t a = i + pts[3 * p], b = j + pts[3 * p + 1], d = k + pts[3 * p + 2];
+            if (a >= 0 && a < nx && b >= 0 && b < ny && d >= 0 && d < nz) {
+                col[e] = (int32_t)(r + (int64_t)pts[3 * p + 2] * nx * ny + (int64_t)pts[3 * p + 1] * nx + pts[3 * p]);
+                val[e] = vals[p];
+                ++e;
+            }
+        }
+    }
+}
+
+/* slice_sets (nslices + 1) and row lengths; returns the stored slot count */
+int64_t or_sellp_sets(int64_t nrows, int64_t ss, const int64_t* ptrs, int64_t* sets, int64_t* lengths,
+                      int nthreads) {
+    set_threads(nthreads);
+    int64_t nslices = (nrows + ss - 1) / ss;
+    sets[0] = 0;
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < nslices; ++s) {
+        int64_t w = 0, hi = (s + 1) * ss < nrows ? (s + 1) * ss : nrows;
+        for (int64_t r = s * ss; r < hi; ++r) {
+            lengths[r] = ptrs[r + 1] - ptrs[r];
+            if (lengths[r] > w) w = lengths[r];
+        }
+        sets[s + 1] = w;
+    }
+    for (int64_t s = 0; s < nslices; ++s) sets[s + 1] += sets[s];
+    return sets[nslices] * ss;
+}
+
+/* zero-filled storage, entry j of row r at sets[s]*ss + j*ss + (r - s*ss) */
+void or_sellp_fill(int64_t nrows, int64_t ss, const int64_t* ptrs, const int32_t* ccol, const double* cval,
+                   const int64_t* sets, int32_t* col, double* val, int nthreads) {
+    set_threads(nthreads);
+    int64_t nslices = (nrows + ss - 1) / ss;
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < nslices; ++s) {
+        int64_t base = sets[s] * ss, w = sets[s + 1] - sets[s];
+        memset(col + base, 0, sizeof(int32_t) * (size_t)(w * ss));
+        memset(val + base, 0, sizeof(double) * (size_t)(w * ss));
+        int64_t hi = (s + 1) * ss < nrows ? (s + 1) * ss : nrows;
+        for (int64_t r = s * ss; r < hi; ++r)
+            for (int64_t e = ptrs[r], j = 0; e < ptrs[r + 1]; ++e, ++j) {
+                col[base + j * ss + (r - s * ss)] = ccol[e];
+                val[base + j * ss + (r - s * ss)] = cval[e];
+            }
+    }
+}

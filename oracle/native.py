@@ -40,6 +40,12 @@ def lib():
         L.or_gmres_csr.argtypes = [_I64, _P, _P, _P, _P, ctypes.c_double, _I64, _I64, _P, _P,
                                    ctypes.c_int]
         L.or_gmres_csr.restype = _I64
+        L.or_stencil_ptrs.argtypes = [_I64, _I64, _I64, ctypes.c_int, _P, _I64, _I64, _P, ctypes.c_int]
+        L.or_stencil_ptrs.restype = _I64
+        L.or_stencil_fill.argtypes = [_I64, _I64, _I64, ctypes.c_int, _P, _P, _I64, _I64, _P, _P, _P, ctypes.c_int]
+        L.or_sellp_sets.argtypes = [_I64, _I64, _P, _P, _P, ctypes.c_int]
+        L.or_sellp_sets.restype = _I64
+        L.or_sellp_fill.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -135,3 +141,43 @@ def dot(a, b, nthreads=0):
     a = np.ascontiguousarray(a, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     return lib().or_dot(len(a), _p(a), _p(b), nthreads)
+
+
+def stencil_csr(nx, ny, nz, points, row_lo=0, row_hi=None, nthreads=0):
+    """corpus_ref.stencil in C (int32 columns, int64 row pointers)."""
+    from types import SimpleNamespace
+
+    from .corpus_ref import _sorted_points
+
+    pts = _sorted_points(points, nx, ny)
+    off = np.ascontiguousarray([[p[0], p[1], p[2]] for p in pts], dtype=np.int32)
+    vals = np.ascontiguousarray([p[3] for p in pts], dtype=np.float64)
+    row_hi = nx * ny * nz if row_hi is None else row_hi
+    n = row_hi - row_lo
+    ptrs = np.empty(n + 1, dtype=np.int64)
+    L = lib()
+    nnz = L.or_stencil_ptrs(nx, ny, nz, len(pts), _p(off), row_lo, row_hi, _p(ptrs), nthreads)
+    col = np.empty(nnz, dtype=np.int32)
+    val = np.empty(nnz, dtype=np.float64)
+    L.or_stencil_fill(nx, ny, nz, len(pts), _p(off), _p(vals), row_lo, row_hi, _p(ptrs), _p(col), _p(val), nthreads)
+    return SimpleNamespace(nrows=n, ncols=nx * ny * nz, row_ptrs=ptrs, col_idx=col, values=val)
+
+
+def csr_to_sellp(m, slice_size=64, nthreads=0):
+    """sparse_ref.csr_to_sellp in C (sparse.py:219-242)."""
+    from types import SimpleNamespace
+
+    n, ss = int(m.nrows), int(slice_size)
+    ptrs = np.ascontiguousarray(m.row_ptrs, dtype=np.int64)
+    ccol = np.ascontiguousarray(m.col_idx, dtype=np.int32)
+    cval = np.ascontiguousarray(m.values, dtype=np.float64)
+    nslices = (n + ss - 1) // ss
+    sets = np.empty(nslices + 1, dtype=np.int64)
+    lengths = np.empty(n, dtype=np.int64)
+    L = lib()
+    total = L.or_sellp_sets(n, ss, _p(ptrs), _p(sets), _p(lengths), nthreads)
+    col = np.empty(total, dtype=np.int32)
+    val = np.empty(total, dtype=np.float64)
+    L.or_sellp_fill(n, ss, _p(ptrs), _p(ccol), _p(cval), _p(sets), _p(col), _p(val), nthreads)
+    return SimpleNamespace(nrows=n, ncols=m.ncols, slice_size=ss, slice_sets=sets, col_idx=col, values=val,
+                           row_lengths=lengths)

@@ -54,6 +54,7 @@ from .kernels import (
     spmv_sellp,
 )
 from .pipeline import SpmvPipeline
+from .device import release
 from .mmio import read_matrix_market, read_matrix_market_entries, write_matrix_market
 from .solvers import (Bicgstab, Cg, Gmres, Iteration, Jacobi, ResidualNorm, bicgstab_solve, cg_solve, diagonal,
                       gmres_solve, pcg_solve, reduce_microbench)
@@ -70,5 +71,5 @@ __all__ = [
     "norm2", "spmv", "spmv_coo", "spmv_csr", "spmv_ell", "spmv_hybrid", "spmv_sellp",
     "read_matrix_market", "read_matrix_market_entries", "write_matrix_market", "SpmvPipeline",
     "Bicgstab", "Cg", "Gmres", "Iteration", "Jacobi", "ResidualNorm", "bicgstab_solve", "cg_solve", "diagonal",
-    "gmres_solve", "pcg_solve", "reduce_microbench",
+    "gmres_solve", "pcg_solve", "reduce_microbench", "release",
 ]

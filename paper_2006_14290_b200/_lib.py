@@ -139,6 +139,8 @@ _SIGS = {
     "wk_csr_to_sellp_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P]),
     "wk_csr_to_ell_fill": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, P, P]),
     "wk_hybrid_coo_offsets": (ctypes.c_int, [I64, I64, P, P, P, P]),
+    "wk_sellp_zero_padding": (ctypes.c_int, [I64, I64, P, P, P, P, P]),
+    "wk_ell_zero_padding": (ctypes.c_int, [I64, I64, I64, P, P, P, P]),
     "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
     "wk_coo_to_csr_ptrs": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_csr_to_coo_rows": (ctypes.c_int, [I64, P, P, P]),

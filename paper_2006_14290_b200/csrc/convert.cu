@@ -373,13 +373,64 @@ __global__ void __launch_bounds__(256) max_len_kernel(int64_t nrows, const int* 
     if ((threadIdx.x & 31) == 0) atomicMax(result, m);
 }
 
-__global__ void __launch_bounds__(256) len_hist_kernel(int64_t nrows, int64_t nbins, const int* __restrict__ ptrs,
+// Row-length histogram: bins below kHistSmem are counted in shared memory
+// with warp-aggregated increments (one atomic per distinct length per warp:
+// R-MAT has 56% empty rows, so per-row global atomics serialised on bin 0 —
+// 7 ms for 16.7M rows), flushed with one global atomic per non-empty bin per
+// block; longer rows (rare) go straight to global memory.
+constexpr int kHistSmem = 4096;
+
+__global__ void __launch_bounds__(512) len_hist_kernel(int64_t nrows, int64_t nbins, const int* __restrict__ ptrs,
                                                        unsigned long long* __restrict__ hist) {
+    __shared__ unsigned sh[kHistSmem];
+    const int nb_s = nbins < kHistSmem ? int(nbins) : kHistSmem;
+    for (int i = threadIdx.x; i < nb_s; i += blockDim.x) sh[i] = 0u;
+    __syncthreads();
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += stride) {
-        int64_t len = ptrs[r + 1] - ptrs[r];
+        int64_t len = __ldcs(ptrs + r + 1) - __ldcs(ptrs + r);
         if (len > nbins - 1) len = nbins - 1;
-        atomicAdd(hist + len, 1ull);
+        if (len < nb_s) {
+            const unsigned peers = __match_any_sync(__activemask(), int(len));
+            if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(sh + len, unsigned(__popc(peers)));
+        } else {
+            atomicAdd(hist + len, 1ull);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb_s; i += blockDim.x)
+        if (sh[i]) atomicAdd(hist + i, (unsigned long long)sh[i]);
+}
+
+// Host-uploaded SELL-P / ELL: every slot past a row's length becomes the
+// reference padding (col 0, val 0.0, sparse.py:230-232), whatever the
+// caller's arrays held there (the SpMV kernels fold full slices).
+__global__ void __launch_bounds__(256) sellp_zero_padding_kernel(int64_t nrows, int64_t ss, int64_t nslices,
+                                                                 const int64_t* __restrict__ sets,
+                                                                 const int* __restrict__ lens, int* __restrict__ col,
+                                                                 double* __restrict__ val) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nslices * ss; t += stride) {
+        const int64_t s = t / ss, local = t - s * ss;
+        const int64_t base = sets[s] * ss, w = sets[s + 1] - sets[s];
+        const int64_t len = t < nrows ? lens[t] : 0;
+        for (int64_t j = len; j < w; ++j) {
+            col[base + j * ss + local] = 0;
+            val[base + j * ss + local] = 0.0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) ell_zero_padding_kernel(int64_t nrows, int64_t width, int64_t stride_,
+                                                               const int* __restrict__ lens, int* __restrict__ col,
+                                                               double* __restrict__ val) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < stride_; r += stride) {
+        const int64_t len = r < nrows ? lens[r] : 0;
+        for (int64_t j = len; j < width; ++j) {
+            col[j * stride_ + r] = 0;
+            val[j * stride_ + r] = 0.0;
+        }
     }
 }
 
@@ -416,10 +467,35 @@ int wk_csr_row_length_histogram(int64_t nrows, const int32_t* row_ptrs, int64_t 
     cudaStream_t st = as_stream(stream);
     WK_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * size_t(nbins), st));
     if (nrows == 0) return 0;
-    int64_t blocks = ceil_div(nrows, 256);
-    if (blocks > int64_t(sm_count()) * 8) blocks = int64_t(sm_count()) * 8;
-    len_hist_kernel<<<(unsigned)blocks, 256, 0, st>>>(nrows, nbins, row_ptrs,
+    int64_t blocks = ceil_div(nrows, 512);
+    if (blocks > int64_t(sm_count()) * 4) blocks = int64_t(sm_count()) * 4;
+    len_hist_kernel<<<(unsigned)blocks, 512, 0, st>>>(nrows, nbins, row_ptrs,
                                                       reinterpret_cast<unsigned long long*>(hist));
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_sellp_zero_padding(int64_t nrows, int64_t slice_size, const int64_t* slice_sets, const int32_t* row_lengths,
+                          int32_t* col_idx, double* values, wk_stream_t stream) {
+    clear_error();
+    const int64_t nslices = ceil_div(nrows, slice_size);
+    if (nslices == 0) return 0;
+    int64_t blocks = ceil_div(nslices * slice_size, 256);
+    if (blocks > int64_t(sm_count()) * 16) blocks = int64_t(sm_count()) * 16;
+    sellp_zero_padding_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(nrows, slice_size, nslices, slice_sets,
+                                                                               row_lengths, col_idx, values);
+    WK_LAUNCH_CHECK();
+    return 0;
+}
+
+int wk_ell_zero_padding(int64_t nrows, int64_t width, int64_t stride, const int32_t* row_lengths, int32_t* col_idx,
+                        double* values, wk_stream_t stream) {
+    clear_error();
+    if (stride == 0 || width == 0) return 0;
+    int64_t blocks = ceil_div(stride, 256);
+    if (blocks > int64_t(sm_count()) * 16) blocks = int64_t(sm_count()) * 16;
+    ell_zero_padding_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(nrows, width, stride, row_lengths,
+                                                                             col_idx, values);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -29,7 +29,10 @@ struct SellpTmaCfg {
 // kGuard (ELL's last, partial 64-row block): rows past nrows hold stale
 // shared memory and must not gather.
 // kColStride: distance between the staged columns (64 = one SELL-P slice).
-template <int J, bool kLen, bool kGuard = false, int kColStride = 64>
+// kCoh: gather x with ld.global.cg (coherent at L2, no L1 line) — the peer
+// CG variant, whose x halo is written by the neighbours DURING the kernel:
+// the non-coherent __ldg path is outside the memory model for such data.
+template <int J, bool kLen, bool kGuard = false, int kColStride = 64, bool kCoh = false>
 __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const int* __restrict__ c, int nj,
                                             int j0, int len0, int len1, const double* __restrict__ x, double& a0,
                                             double& a1, bool ok0 = true, bool ok1 = true) {
@@ -40,8 +43,8 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
         if (jj < nj) {
             vv[jj] = *reinterpret_cast<const double2*>(v + jj * kColStride);
             const int2 cc = *reinterpret_cast<const int2*>(c + jj * kColStride);
-            x0[jj] = (!kGuard || ok0) ? ld_x(x, cc.x) : 0.0;
-            x1[jj] = (!kGuard || ok1) ? ld_x(x, cc.y) : 0.0;
+            x0[jj] = (!kGuard || ok0) ? (kCoh ? __ldcg(x + cc.x) : ld_x(x, cc.x)) : 0.0;
+            x1[jj] = (!kGuard || ok1) ? (kCoh ? __ldcg(x + cc.y) : ld_x(x, cc.y)) : 0.0;
         }
     }
 #pragma unroll
@@ -57,7 +60,7 @@ __device__ __forceinline__ void sellp_chunk(const double* __restrict__ v, const 
 // x = p, y = q) and publish it through DotEpilogue (last-arriving CTA).
 // kEll: ELL(width, stride) — one "slice" per 64-row block, column j of block
 // b at j*stride + 64b (stride % 4 == 0): J bulk copies per chunk instead of 2.
-template <class Cfg, bool kDot = false, bool kEll = false>
+template <class Cfg, bool kDot = false, bool kEll = false, bool kCoh = false>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
 sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
                    const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
@@ -206,11 +209,11 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             const double* v = sval + st * CH + 2 * lane;
             const int* c = scol + st * CH + 2 * lane;
             if (kEll && partial)
-                sellp_chunk<J, true, true>(v, c, nj, j0, len0, len1, x, a0, a1, r0 < nrows, r0 + 1 < nrows);
+                sellp_chunk<J, true, true, 64, kCoh>(v, c, nj, j0, len0, len1, x, a0, a1, r0 < nrows, r0 + 1 < nrows);
             else if (finite0)
-                sellp_chunk<J, false>(v, c, nj, j0, len0, len1, x, a0, a1);
+                sellp_chunk<J, false, false, 64, kCoh>(v, c, nj, j0, len0, len1, x, a0, a1);
             else
-                sellp_chunk<J, true>(v, c, nj, j0, len0, len1, x, a0, a1);
+                sellp_chunk<J, true, false, 64, kCoh>(v, c, nj, j0, len0, len1, x, a0, a1);
             __syncwarp();
             if (pvalid) {
                 if (lane == 0) fence_proxy_async_smem();
@@ -249,7 +252,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
 
 // Launch one configuration (persistent grid: one CTA per SM). kEll: sets is
 // unused, the operand is ELL(ell_width, ell_stride).
-template <class Cfg, bool kDot = false, bool kEll = false>
+template <class Cfg, bool kDot = false, bool kEll = false, bool kCoh = false>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
                        DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int64_t ell_width = 0,
@@ -258,7 +261,7 @@ int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const 
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot, kEll>,
+        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot, kEll, kCoh>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
@@ -266,7 +269,7 @@ int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const 
     int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
     const int64_t need = ceil_div(nslices, Cfg::kWarps);
     if (grid > need) grid = need;
-    sellp64_tma_kernel<Cfg, kDot, kEll><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
+    sellp64_tma_kernel<Cfg, kDot, kEll, kCoh><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
         nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, ell_width, ell_stride, rev);
     WK_LAUNCH_CHECK();
     return 0;

@@ -293,6 +293,10 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
     DotEpilogue dot{reinterpret_cast<double*>(w),
                     reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
                     reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo)};
+    if (halo != nullptr)  // peer CG: the halo of p lands during the kernel (coherent gathers)
+        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true, false, true>(
+            A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values, A->row_lengths, p, q, &s->done, st, dot, 0, 0,
+            rev);
     return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
                                                              A->values, A->row_lengths, p, q, &s->done, st, dot,
                                                              0, 0, rev);

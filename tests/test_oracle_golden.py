@@ -125,3 +125,24 @@ def test_rmat_generator_statistics():
     counts = np.bincount(m.row_idx, minlength=m.nrows)
     # skew: quadrant a=0.57 concentrates edges on low row indices
     assert counts[:256].sum() > counts[768:].sum() * 4
+
+
+def test_c_generators_equal_numpy_restatements():
+    """oracle.native.stencil_csr / csr_to_sellp (the C builders of the
+    full-size CPU baseline) equal corpus_ref.stencil / sparse_ref.csr_to_sellp
+    (sparse.py:219-242) exactly."""
+    from oracle import corpus_ref, native, sparse_ref
+
+    cases = [(7, 5, 6, corpus_ref.points_27pt(), 0, None),
+             (9, 8, 7, corpus_ref.points_7pt(beta=(1.0, 0.5, 0.25)), 50, 300),
+             (30, 1, 1, corpus_ref.points_5pt(), 0, None)]
+    for nx, ny, nz, pts, lo, hi in cases:
+        a = native.stencil_csr(nx, ny, nz, pts, lo, hi)
+        b = corpus_ref.stencil(nx, ny, nz, pts, lo, hi)
+        assert np.array_equal(a.row_ptrs, b.row_ptrs) and np.array_equal(a.col_idx, b.col_idx)
+        assert a.values.tobytes() == b.values.tobytes()
+        for ss in (1, 4, 64):
+            sa, sb = native.csr_to_sellp(a, ss), sparse_ref.csr_to_sellp(b, ss)
+            for k in ("slice_sets", "col_idx", "row_lengths"):
+                assert np.array_equal(getattr(sa, k), getattr(sb, k)), k
+            assert sa.values.tobytes() == sb.values.tobytes()

@@ -92,3 +92,34 @@ def test_reference_harness_on_b200(installed, tmp_path):
     assert rows, "no b200 records"
     bad = [(r.matrix, r.kernel, r.max_rel_err) for r in rows if not r.correct]
     assert not bad, bad
+
+
+def test_plugin_raises_warpkit_errors(installed):
+    """With the b200 slot installed, warpkit's own entry points still raise
+    warpkit.errors classes (the checks run before any device work)."""
+    from warpkit.corpus import poisson2d_matrix
+    from warpkit.kernels import spmv_coo, spmv_csr, spmv_sellp
+    from warpkit.sparse import coo_to_csr, coo_to_sellp
+
+    ex = warpkit.make_executor("b200")
+    m = poisson2d_matrix(4)
+    for fn, mm in ((spmv_coo, m), (spmv_csr, coo_to_csr(m)), (spmv_sellp, coo_to_sellp(m, 4))):
+        with pytest.raises(warpkit.errors.DimensionMismatch):
+            fn(mm, np.ones(m.ncols + 1), ex)
+    with pytest.raises(warpkit.errors.DimensionMismatch):
+        warpkit.dispatch("cg", ex, coo_to_sellp(m, 4), np.ones(3), 1e-8, 10)
+    with pytest.raises(ValueError):
+        warpkit.dispatch("cg", ex, coo_to_sellp(m, 4), np.ones(m.nrows), 0.0, 10)
+
+
+@pytest.mark.gpu
+def test_plugin_breakdown_is_warpkit_breakdown(installed):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from warpkit.sparse import CooMatrix, coo_to_sellp
+
+    # indefinite: p.Ap < 0 at the first iteration (kernels.py:317-318)
+    m = CooMatrix.from_entries(2, 2, [0, 1], [0, 1], [-1.0, -2.0])
+    with pytest.raises(warpkit.errors.BreakdownError):
+        warpkit.dispatch("cg", warpkit.make_executor("b200"), coo_to_sellp(m, 2), np.ones(2), 1e-8, 10)
