@@ -202,10 +202,14 @@ int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32
 /* Hybrid COO part, pass 1: offsets[0..nrows] = exclusive scan of max(len-width, 0) */
 int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs, int64_t* offsets, void* scan_ws,
                           wk_stream_t stream);
-/* Hybrid COO part, pass 2 */
+/* Hybrid COO part, pass 2: short rows in 32-row flattened runs, rows with
+ * more than 256 overflow entries as 4096-entry segments spread over the grid.
+ * work: 16-byte aligned device scratch of wk_hybrid_coo_fill_workspace(rem)
+ * bytes, rem = offsets[nrows]. */
+int64_t wk_hybrid_coo_fill_workspace(int64_t rem);
 int wk_hybrid_coo_fill(int64_t nrows, int64_t width, const int32_t* row_ptrs, const int32_t* col_idx,
                        const double* values, const int64_t* offsets, int32_t* c_row, int32_t* c_col,
-                       double* c_val, wk_stream_t stream);
+                       double* c_val, void* work, int64_t work_bytes, wk_stream_t stream);
 /* Host-uploaded SELL-P / ELL: rewrite every slot past row_lengths[r] (and
  * the rows past nrows of the last slice / of the stride) as the reference
  * padding (col 0, val 0.0; sparse.py:230-232), in place. */

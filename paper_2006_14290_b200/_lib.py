@@ -141,7 +141,8 @@ _SIGS = {
     "wk_hybrid_coo_offsets": (ctypes.c_int, [I64, I64, P, P, P, P]),
     "wk_sellp_zero_padding": (ctypes.c_int, [I64, I64, P, P, P, P, P]),
     "wk_ell_zero_padding": (ctypes.c_int, [I64, I64, I64, P, P, P, P]),
-    "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P]),
+    "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P, I64, P]),
+    "wk_hybrid_coo_fill_workspace": (ctypes.c_int64, [I64]),
     "wk_coo_to_csr_ptrs": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_csr_to_coo_rows": (ctypes.c_int, [I64, P, P, P]),
     "wk_scan_workspace_bytes": (I64, [I64]),

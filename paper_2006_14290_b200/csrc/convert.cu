@@ -316,19 +316,131 @@ ell_fill_kernel(int64_t nrows, int64_t width, int64_t stride, int64_t rpb, const
     scatter_block(nrows, r0, nslots, width, r0, stride, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
 }
 
-__global__ void hybrid_coo_fill_kernel(int64_t nrows, int64_t width, const int* __restrict__ ptrs,
-                                       const int* __restrict__ col, const double* __restrict__ val,
-                                       const int64_t* __restrict__ offsets, int* __restrict__ crow,
-                                       int* __restrict__ ccol, double* __restrict__ cval) {
+// COO remainder of CSR->Hybrid, in two kernels.
+//
+// hybrid_coo_fill_kernel: a warp takes 32 consecutive rows (one row-pointer
+// pair per lane), scans their overflow counts (entries past `width`) and
+// copies the group's overflow as ONE flattened run: the destination is
+// contiguous (offsets[r0] ..), so every pass writes 32 consecutive COO entries
+// and each lane finds its row by a 5-step binary search over the scanned
+// counts in registers. Rows with no overflow (56% of R-MAT rows are empty)
+// cost one lane of one load. A row with more than kHybLong overflow entries is
+// not copied here: its segments of kHybSeg entries are appended to a work list
+// (one atomic per long row), so no single warp walks R-MAT's
+// heaviest rows (238k entries) or their 32-row group (~1M entries) alone.
+// hybrid_coo_long_kernel: the warps of the whole grid take the listed
+// segments round-robin, one contiguous copy of <= kHybSeg entries each.
+// (The first version, a warp per row: 4.9 ms on R-MAT scale 24, width 8.)
+constexpr int kHybLong = 256;
+constexpr int kHybSeg = 4096;
+
+__global__ void __launch_bounds__(256)
+hybrid_coo_fill_kernel(int64_t nrows, int64_t width, const int* __restrict__ ptrs, const int* __restrict__ col,
+                       const double* __restrict__ val, const int64_t* __restrict__ offsets, int* __restrict__ crow,
+                       int* __restrict__ ccol, double* __restrict__ cval, unsigned long long* __restrict__ nseg,
+                       int2* __restrict__ segs) {
+    const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < nrows; r += warps) {
-        const int64_t lo = int64_t(ptrs[r]) + width, hi = ptrs[r + 1];
-        const int64_t o = offsets[r];
-        for (int64_t k = lo + lane; k < hi; k += 32) {
-            crow[o + k - lo] = int(r);
-            ccol[o + k - lo] = col[k];
-            cval[o + k - lo] = val[k];
+    constexpr int kU = 4;
+    for (int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; r0 < nrows; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        int lo = 0, cnt = 0;
+        if (r < nrows) {
+            const int p0 = __ldcs(ptrs + r), p1 = __ldcs(ptrs + r + 1);
+            lo = p0 + int(width < p1 - p0 ? width : p1 - p0);
+            cnt = p1 - lo;
+        }
+        if (cnt > kHybLong) {  // long row: list its segments for the second kernel
+            const int ns = (cnt + kHybSeg - 1) / kHybSeg;
+            const unsigned long long at = atomicAdd(nseg, (unsigned long long)ns);
+            for (int q = 0; q < ns; ++q) segs[at + q] = make_int2(int(r), q);
+            cnt = 0;
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += o;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) continue;
+        const int excl = incl - cnt;
+        for (int d0 = 0; d0 < total; d0 += 32 * kU) {
+            int src[kU], row[kU];
+            int64_t dst[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int d = d0 + u * 32 + lane;
+                int j = 0;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) {
+                    const int e = __shfl_sync(FULL, excl, j + s);
+                    if (e <= d) j += s;
+                }
+                const int off = d - __shfl_sync(FULL, excl, j);
+                src[u] = __shfl_sync(FULL, lo, j) + off;
+                row[u] = int(r0) + j;
+                dst[u] = off;  // destination = offsets[row] + off (rows of a group need not be adjacent
+                               // in the remainder: a long row between them is copied elsewhere)
+            }
+            int c[kU];
+            double v[kU];
+            int64_t o[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const bool ok = d0 + u * 32 + lane < total;
+                c[u] = ok ? __ldcs(col + src[u]) : 0;
+                v[u] = ok ? __ldcs(val + src[u]) : 0.0;
+                o[u] = ok ? __ldg(offsets + row[u]) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (d0 + u * 32 + lane < total) {
+                    const int64_t at = o[u] + dst[u];
+                    __stcs(crow + at, row[u]);
+                    __stcs(ccol + at, c[u]);
+                    __stcs(cval + at, v[u]);
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+hybrid_coo_long_kernel(int64_t width, const int* __restrict__ ptrs, const int* __restrict__ col,
+                       const double* __restrict__ val, const int64_t* __restrict__ offsets, int* __restrict__ crow,
+                       int* __restrict__ ccol, double* __restrict__ cval, const unsigned long long* __restrict__ nseg,
+                       const int2* __restrict__ segs) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t n = int64_t(*nseg);
+    constexpr int kU = 4;
+    for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        const int2 sg = segs[i];
+        const int p0 = ptrs[sg.x], p1 = ptrs[sg.x + 1];
+        const int lo = p0 + int(width), cnt = p1 - lo;
+        const int s0 = sg.y * kHybSeg;
+        const int s1 = (cnt - s0 < kHybSeg) ? cnt : s0 + kHybSeg;
+        const int64_t base = offsets[sg.x];
+        for (int k0 = s0; k0 < s1; k0 += 32 * kU) {
+            int c[kU];
+            double v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int k = k0 + u * 32 + lane;
+                c[u] = k < s1 ? __ldcs(col + lo + k) : 0;
+                v[u] = k < s1 ? __ldcs(val + lo + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int k = k0 + u * 32 + lane;
+                if (k < s1) {
+                    __stcs(crow + base + k, sg.x);
+                    __stcs(ccol + base + k, c[u]);
+                    __stcs(cval + base + k, v[u]);
+                }
+            }
         }
     }
 }
@@ -571,13 +683,31 @@ int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs,
     return exclusive_scan(nrows, rem, offsets, scan_ws, as_stream(stream));
 }
 
+int64_t wk_hybrid_coo_fill_workspace(int64_t rem) {
+    // list length <= rem / kHybSeg + (rows with > kHybLong overflow) <= rem / kHybSeg + rem / kHybLong
+    return 16 + 8 * (rem / kHybSeg + rem / kHybLong + 1);
+}
+
 int wk_hybrid_coo_fill(int64_t nrows, int64_t width, const int32_t* row_ptrs, const int32_t* col_idx,
                        const double* values, const int64_t* offsets, int32_t* c_row, int32_t* c_col,
-                       double* c_val, wk_stream_t stream) {
+                       double* c_val, void* work, int64_t work_bytes, wk_stream_t stream) {
     clear_error();
     if (nrows == 0) return 0;
-    hybrid_coo_fill_kernel<<<warp_grid(nrows), 256, 0, as_stream(stream)>>>(nrows, width, row_ptrs, col_idx, values,
-                                                                            offsets, c_row, c_col, c_val);
+    WK_REQUIRE(work != nullptr && (reinterpret_cast<uintptr_t>(work) & 15) == 0, WK_ERR_INVALID,
+               "hybrid fill workspace must be 16-byte aligned");
+    cudaStream_t st = as_stream(stream);
+    auto* nseg = reinterpret_cast<unsigned long long*>(work);
+    auto* segs = reinterpret_cast<int2*>(reinterpret_cast<char*>(work) + 16);
+    (void)work_bytes;  // sized by wk_hybrid_coo_fill_workspace(offsets[nrows])
+    WK_CUDA(cudaMemsetAsync(nseg, 0, 8, st));
+    int64_t blocks = ceil_div(nrows, 256);  // 8 warps x 32 rows
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (blocks > cap) blocks = cap;
+    hybrid_coo_fill_kernel<<<unsigned(blocks), 256, 0, st>>>(nrows, width, row_ptrs, col_idx, values, offsets,
+                                                            c_row, c_col, c_val, nseg, segs);
+    WK_LAUNCH_CHECK();
+    hybrid_coo_long_kernel<<<unsigned(cap), 256, 0, st>>>(width, row_ptrs, col_idx, values, offsets, c_row, c_col,
+                                                         c_val, nseg, segs);
     WK_LAUNCH_CHECK();
     return 0;
 }

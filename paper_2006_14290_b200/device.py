@@ -661,8 +661,10 @@ def csr_to_hybrid(m, width=None, strategy="minimal_storage", percent=0.8, stride
     ccol = torch.empty(rem, dtype=torch.int32, device=d.device)
     cval = torch.empty(rem, dtype=torch.float64, device=d.device)
     if rem:
+        nwork = int(_lib.load().wk_hybrid_coo_fill_workspace(rem))
+        work = torch.empty((nwork + 15) // 16 * 2, dtype=torch.int64, device=d.device)
         _lib.call("wk_hybrid_coo_fill", d.nrows, width, _ptr(d.row_ptrs), _ptr(d.col_idx), _ptr(d.values),
-                  _ptr(offsets), _ptr(crow), _ptr(ccol), _ptr(cval), st)
+                  _ptr(offsets), _ptr(crow), _ptr(ccol), _ptr(cval), _ptr(work), nwork, st)
     return DeviceHybrid(ell, DeviceCoo(d.nrows, d.ncols, crow, ccol, cval))
 
 

@@ -14,6 +14,8 @@
 #include <thrust/device_ptr.h>
 #include <thrust/sort.h>
 #include <thrust/unique.h>
+#include <thrust/sequence.h>
+#include <thrust/functional.h>
 
 #include <cstdio>
 #include <cstdint>
@@ -124,6 +126,93 @@ float run(int64_t nnz, const int* row, const int* col, const double* val, const 
     return ms / reps;
 }
 
+
+// Hot-column cache: the K most frequent columns' x values are packed (hx,
+// one gather pass per launch) and copied into shared memory by every CTA of a
+// persistent grid; col2[k] = ~slot for a cached column, col otherwise.
+__global__ void pack_hot(int K, const int* __restrict__ hot, const double* __restrict__ x, double* __restrict__ hx) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < K) hx[i] = __ldg(x + hot[i]);
+}
+
+template <int K>
+__global__ void __launch_bounds__(1024, 1)
+fold_hot(int64_t nnz, const int* __restrict__ row, const int* __restrict__ col2, const double* __restrict__ val,
+         const double* __restrict__ x, const double* __restrict__ hxg, double* __restrict__ out) {
+    extern __shared__ double hx[];
+    for (int i = threadIdx.x; i < K; i += blockDim.x) hx[i] = hxg[i];
+    __syncthreads();
+    const int64_t T = int64_t(gridDim.x) * blockDim.x;
+    double acc = 0.0;
+    int rsum = 0;
+    for (int64_t kb = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 8; kb + 8 <= nnz; kb += T * 8) {
+        const int4 c0 = __ldcs(reinterpret_cast<const int4*>(col2 + kb));
+        const int4 c1 = __ldcs(reinterpret_cast<const int4*>(col2 + kb + 4));
+        const int4 r0 = __ldcs(reinterpret_cast<const int4*>(row + kb));
+        const int4 r1 = __ldcs(reinterpret_cast<const int4*>(row + kb + 4));
+        int c[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            double2 t = __ldcs(reinterpret_cast<const double2*>(val + kb + u));
+            v[u] = t.x;
+            v[u + 1] = t.y;
+        }
+        double g[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) g[u] = c[u] < 0 ? hx[~c[u]] : __ldg(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], g[u]));
+        rsum += r0.x ^ r1.w;
+    }
+    if (acc == 12345.0 || rsum == 7) out[0] = acc;
+    out[1 + (blockIdx.x * 1024 + threadIdx.x) % 1024] = acc;
+}
+
+__global__ void col_hist(int64_t nnz, const int* __restrict__ col, int* __restrict__ cnt) {
+    int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < nnz) atomicAdd(cnt + col[e], 1);
+}
+__global__ void make_slot(int K, const int* __restrict__ hot, int* __restrict__ slot) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < K) slot[hot[i]] = i;
+}
+__global__ void remap(int64_t nnz, const int* __restrict__ col, const int* __restrict__ slot, int* __restrict__ col2) {
+    int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < nnz) {
+        int s = slot[col[e]];
+        col2[e] = s >= 0 ? ~s : col[e];
+    }
+}
+
+template <int K>
+int run_hot(int64_t n, int64_t nnz, const int* row, const int* col, const double* val, const double* x, double* out,
+            int sms, int* cnt_sorted_cols, int* slot, int* col2, double* hx, const char* tag) {
+    CK(cudaMemset(slot, 0xff, n * 4));
+    make_slot<<<(K + 255) / 256, 256>>>(K, cnt_sorted_cols, slot);
+    remap<<<(nnz + 255) / 256, 256>>>(nnz, col, slot, col2);
+    CK(cudaFuncSetAttribute(fold_hot<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K * 8));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto go = [&] {
+        pack_hot<<<(K + 255) / 256, 256>>>(K, cnt_sorted_cols, x, hx);
+        fold_hot<K><<<sms, 1024, K * 8>>>(nnz, row, col2, val, x, hx, out);
+    };
+    for (int i = 0; i < 3; ++i) go();
+    cudaEventRecord(a);
+    for (int i = 0; i < 10; ++i) go();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    ms /= 10;
+    cudaError_t e = cudaGetLastError();
+    const double bytes = 16.0 * nnz + 8.0 * n;
+    printf("hot K=%d %s: %.4f ms  %.1f GB/s  %s\n", K, tag, ms, bytes / ms / 1e6, e == cudaSuccess ? "" : cudaGetErrorString(e));
+    return 0;
+}
+
 int main() {
     const int scale = 24;
     const int64_t n = int64_t(1) << scale, m = n * 16;
@@ -167,5 +256,31 @@ int main() {
     R(0, 1, 4) R(0, 1, 8) R(0, 4, 4) R(0, 4, 8)
     R(1, 4, 8) R(2, 4, 8) R(3, 4, 8) R(4, 4, 8) R(5, 4, 8)
     R(2, 4, 4) R(3, 4, 4) R(1, 4, 4)
+    {
+        int *cnt, *ids, *slot, *col2;
+        double* hx;
+        CK(cudaMalloc(&cnt, n * 4));
+        CK(cudaMalloc(&ids, n * 4));
+        CK(cudaMalloc(&slot, n * 4));
+        CK(cudaMalloc(&col2, nnz * 4));
+        CK(cudaMalloc(&hx, 32768 * 8));
+        CK(cudaMemset(cnt, 0, n * 4));
+        col_hist<<<(nnz + 255) / 256, 256>>>(nnz, col, cnt);
+        thrust::sequence(thrust::device_ptr<int>(ids), thrust::device_ptr<int>(ids + n));
+        thrust::sort_by_key(thrust::device_ptr<int>(cnt), thrust::device_ptr<int>(cnt + n), thrust::device_ptr<int>(ids),
+                            thrust::greater<int>());
+        std::vector<int> hc(65536);
+        CK(cudaMemcpy(hc.data(), cnt, 65536 * 4, cudaMemcpyDeviceToHost));
+        long long s = 0;
+        for (int k = 0; k < 65536; ++k) {
+            s += hc[k];
+            if (k + 1 == 4096 || k + 1 == 8192 || k + 1 == 16384 || k + 1 == 24576 || k + 1 == 32768 || k + 1 == 65536)
+                printf("top %d columns: %.4f of entries\n", k + 1, double(s) / nnz);
+        }
+        run_hot<8192>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+        run_hot<16384>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+        run_hot<24576>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+        run_hot<27000>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+    }
     return 0;
 }
