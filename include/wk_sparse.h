@@ -70,18 +70,6 @@ const char* wk_last_error(void);
 int wk_version(void);
 /* number of SMs of the current device */
 int wk_device_sm_count(void);
-/* process-wide kernel selection knobs (A/B measurement): "sellp_kernel":
- * 0 = register-only SELL-P kernel, 1..10 = TMA pipeline configurations
- * (table in spmv.cu launch_sellp); "csr_kernel": see spmv.cu launch_csr;
- * "coo_kernel": 0..3 (default 3, spmv.cu coo_kernel_choice); "ell_kernel":
- * 0 = register kernel, 1 = SELL-P(64) warp pipeline, 2 (default) .. 4 =
- * ell_tma_kernel (512-row tiles, producer warp); "seg8_kernel" (COO /
- * CSR load_balance data path): 0 = direct loads (default), 1 = TMA ring;
- * "fill_kernel" (CSR -> SELL-P / ELL / Hybrid-ELL fill): 0 = staged scatter,
- * 1 (default) = TMA-staged ring; "cg_pingpong" (wk_cg_solve): 1 (default) =
- * consecutive kernels walk the rows in alternating directions (L2 reuse), 0 =
- * all forward */
-int wk_config_set(const char* key, int64_t value);
 
 /* ---- SpMV: y = A x ------------------------------------------------------ */
 
@@ -116,6 +104,18 @@ int64_t wk_csr_load_balance_plan_bytes(int64_t nrows, int64_t nnz);
 int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
                                    wk_stream_t stream);
 
+/* Hot-column gather plan for COO / CSR load_balance (wk_matrix.gather_plan):
+ * the columns with the most entries (at most 8192, each with >= min_count
+ * entries; min_count <= 0: 2 x SM count) are cached in shared memory by the
+ * SpMV; the plan holds their ids and a rewritten column array. Results are
+ * bitwise those of the plan-less kernels. plan: wk_gather_plan_bytes(nnz),
+ * scratch: wk_gather_plan_scratch_bytes(ncols), both 16-byte aligned. Plan
+ * header (device): int32 nhot, int32 threshold, int64 entries covered. */
+int64_t wk_gather_plan_bytes(int64_t nnz);
+int64_t wk_gather_plan_scratch_bytes(int64_t ncols);
+int wk_gather_plan_build(int64_t ncols, int64_t nnz, const int32_t* col_idx, int64_t min_count, void* plan,
+                         void* scratch, wk_stream_t stream);
+
 /* replaces spmv_coo (kernels.py:409-410 -> 209-264); coo_spmv fixture
  * (coo_kernels.cu:34-35). Entries sorted row-major. accumulate = 0 zero-fills y. */
 int wk_spmv_coo_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_idx, const int32_t* col_idx,
@@ -147,7 +147,9 @@ typedef struct wk_matrix {
     const int32_t* coo_row;
     const int32_t* coo_col;
     const double* coo_val;
-    void* plan;               /* CSR stream plan */
+    void* plan;               /* CSR stream / merge / load_balance plan */
+    const void* gather_plan;  /* COO, CSR load_balance, HYBRID (coo part): hot-column
+                                 gather plan (wk_gather_plan_build) or NULL */
 } wk_matrix;
 
 int wk_spmv(const wk_matrix* A, const double* x, double* y, wk_stream_t stream);

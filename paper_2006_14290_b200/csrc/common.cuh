@@ -61,15 +61,6 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // Number of SMs of the current device (cached per device).
 int sm_count();
 
-// Kernel-selection knob behind wk_config_set("sellp_kernel", ...).
-int set_sellp_kernel(int choice);
-int set_csr_kernel(int choice);
-int set_coo_kernel(int choice);
-int set_ell_kernel(int choice);
-int set_seg8_kernel(int choice);
-int set_fill_kernel(int choice);
-int set_cg_pingpong(int v);
-
 // CG q = A p with the p.q reduction fused into the SpMV (spmv.cu); returns 1
 // if A cannot take the fused path.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,

@@ -17,25 +17,6 @@ namespace wk {
 constexpr int kConvThreads = 256;
 constexpr int kStageCap = 2048;  // staged entries per block (24 KB)
 
-// SELL-P / ELL fill kernel (wk_config_set("fill_kernel", i) / env
-// WK_FILL_KERNEL): 0 = staged scatter kernels, 1 (default) = TMA-staged ring
-// (fill_tma_kernel).
-static int g_fill_choice = -1;
-
-int set_fill_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 1, WK_ERR_INVALID, "fill kernel choice must be 0 or 1");
-    g_fill_choice = choice;
-    return 0;
-}
-
-static int fill_kernel_choice() {
-    if (g_fill_choice < 0) {
-        const char* e = getenv("WK_FILL_KERNEL");
-        g_fill_choice = (e != nullptr) ? atoi(e) : 1;
-    }
-    return g_fill_choice;
-}
-
 // Row lengths and per-slice maximum lengths (sparse.py:225-228) in one pass:
 // lengths[r] = ptrs[r+1] - ptrs[r]; out[s + 1] = max over the slice's rows
 // (butterfly within ss <= 32 lanes, warp maxima combined in shared memory for
@@ -145,8 +126,8 @@ sellp_fill_kernel(int64_t nrows, int log2ss, const int* __restrict__ ptrs, const
     scatter_block(nrows, s * ss, ss, w, sets[s] * ss, ss, ptrs, col, val, dcol, dval, s_col, s_val, s_ptr);
 }
 
-// CSR -> SELL-P / ELL fill with TMA-staged input (fill_kernel 1, the default
-// for 16-byte aligned CSR arrays). Persistent CTAs (2 per SM) walk tiles of R
+// CSR -> SELL-P / ELL fill with TMA-staged input (16-byte aligned CSR arrays,
+// 4 <= rows per tile <= 256; the staged-scatter kernels above otherwise). Persistent CTAs (2 per SM) walk tiles of R
 // rows (SELL-P: one slice, R = ss; ELL: R = 2^k <= 256 rows with R * width <=
 // the stage capacity), t = blockIdx.x + i * gridDim.x. Thread 0 bulk-loads
 // the next tile's CSR range (values and column indices are contiguous per
@@ -643,7 +624,7 @@ int wk_csr_to_sellp_fill(int64_t nrows, int64_t slice_size, const int32_t* row_p
     if (nslices == 0) return 0;
     int l2 = 0;
     while ((int64_t(1) << l2) < slice_size) ++l2;
-    if (slice_size >= 4 && slice_size <= 256 && al16(col_idx) && al16(values) && fill_kernel_choice() == 1)
+    if (slice_size >= 4 && slice_size <= 256 && al16(col_idx) && al16(values))
         return launch_fill_tma<2, false>(nrows, l2, nslices, row_ptrs, col_idx, values, slice_sets, 0, 0, s_col,
                                                s_val, nullptr, as_stream(stream));
     sellp_fill_kernel<<<(unsigned)nslices, kConvThreads, 0, as_stream(stream)>>>(nrows, l2, row_ptrs, col_idx, values,
@@ -659,7 +640,7 @@ int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32
     WK_REQUIRE(stride >= nrows, WK_ERR_INVALID, "ELL stride %lld < nrows %lld", (long long)stride,
                (long long)nrows);
     if (stride == 0) return 0;
-    if (al16(col_idx) && al16(values) && fill_kernel_choice() == 1) {
+    if (al16(col_idx) && al16(values)) {
         int l2 = 8;  // tile rows: 256 down to 32 so that a tile's entries fit a stage
         while (l2 > 5 && (int64_t(1) << l2) * width > kFillCap) --l2;
         return launch_fill_tma<2, true>(nrows, l2, ceil_div(stride, int64_t(1) << l2), row_ptrs, col_idx, values,

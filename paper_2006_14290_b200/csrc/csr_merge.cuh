@@ -341,236 +341,3 @@ inline int build_csr_merge_plan(int64_t nrows, int64_t nnz, const int* ptrs, voi
 }
 
 }  // namespace wk
-
-namespace wk {
-
-// ---------------------------------------------------------------------------
-// COO with the same tile machinery (kernels.py:209-257 semantics: sorted
-// entries, segment sums, atomics only where a row is shared between work
-// units). Tiles of kMgTile consecutive entries; each thread folds 8
-// consecutive entries sequentially (a row end = the next entry's row
-// differs), threads are joined by the block segmented scan, and the only rows
-// two tiles can share — a tile's first and last row — are added with
-// atomicAdd (the reference's "atomic at run heads"). Persistent grid, the next
-// tile's rows / columns / values stream in with cp.async.bulk.
-// ---------------------------------------------------------------------------
-constexpr int kCtRowSlots = kMgTile + 4 + 4;  // + the next tile's first row
-constexpr size_t kCtStageBytes =
-    (size_t(kMgValSlots) * 8 + size_t(kMgColSlots) * 4 + size_t(kCtRowSlots) * 4 + 127) / 128 * 128;
-constexpr size_t kCtSmem = kMgStages * kCtStageBytes + kMgStages * 8 + 256;
-
-__device__ __forceinline__ void ct_issue(int64_t j0, int64_t j1, const int* __restrict__ row,
-                                         const int* __restrict__ col, const double* __restrict__ val,
-                                         unsigned char* stage, uint64_t* bar, uint64_t pol) {
-    const int64_t va = j0 & ~int64_t(1), ve = j1 & ~int64_t(1);
-    const int64_t ca = j0 & ~int64_t(3), ce = j1 & ~int64_t(3);
-    const uint32_t bv = ve > va ? uint32_t((ve - va) * 8) : 0u;
-    const uint32_t bc = ce > ca ? uint32_t((ce - ca) * 4) : 0u;
-    mbar_arrive_expect_tx(bar, bv + 2 * bc);
-    if (bv) bulk_g2s_evict_first(stage, val + va, bv, bar, pol);
-    if (bc) {
-        bulk_g2s_evict_first(stage + size_t(kMgValSlots) * 8, col + ca, bc, bar, pol);
-        bulk_g2s_evict_first(stage + size_t(kMgValSlots) * 8 + size_t(kMgColSlots) * 4, row + ca, bc, bar, pol);
-    }
-}
-
-__global__ void __launch_bounds__(kMgThreads)
-coo_tile_kernel(int64_t nnz, int64_t ntiles, int accumulate, const int* __restrict__ row,
-                const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
-                double* __restrict__ y, const int* __restrict__ skip) {
-    if (skip != nullptr && *skip) return;
-    extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ double s_wv[kMgThreads / 32];
-    __shared__ int s_wf[kMgThreads / 32];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kMgStages * kCtStageBytes);
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const uint64_t pol = policy_evict_first();
-    if (tid == 0) {
-        for (int s = 0; s < kMgStages; ++s) mbar_init(bars + s, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    auto bounds = [&](int64_t t, int64_t& j0, int64_t& j1) {
-        j0 = t * kMgTile;
-        j1 = (j0 + kMgTile < nnz) ? j0 + kMgTile : nnz;
-    };
-    if (tid == 0) {
-        for (int s = 0; s < kMgStages; ++s) {
-            const int64_t t = blockIdx.x + int64_t(s) * gridDim.x;
-            int64_t j0, j1;
-            bounds(t, j0, j1);
-            if (t < ntiles) ct_issue(j0, j1, row, col, val, smem + s * kCtStageBytes, bars + s, pol);
-        }
-    }
-    uint32_t n = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++n) {
-        const int st = int(n % kMgStages);
-        unsigned char* stage = smem + st * kCtStageBytes;
-        double* sv = reinterpret_cast<double*>(stage);
-        const int* sc = reinterpret_cast<const int*>(stage + size_t(kMgValSlots) * 8);
-        int* sr = reinterpret_cast<int*>(stage + size_t(kMgValSlots) * 8 + size_t(kMgColSlots) * 4);
-        int64_t j0, j1;
-        bounds(t, j0, j1);
-        const int nn = int(j1 - j0);
-        const int ov = int(j0 & 1), oc = int(j0 & 3);
-        const int nv = int((j1 & ~int64_t(1)) - j0);
-        const int nc = int((j1 & ~int64_t(3)) - j0);
-        mbar_wait(bars + st, (n / kMgStages) & 1);
-        // rows past the bulk body, and the next tile's first row (-1 at the end)
-        if (tid < 5) {
-            const int k = (nc > 0 ? nc : 0) + tid;
-            if (k < nn) sr[oc + k] = __ldg(row + j0 + k);
-            else if (k == nn) sr[oc + k] = (j1 < nnz) ? __ldg(row + j1) : -1;
-        }
-        {
-            double v[kMgItems], xv[kMgItems];
-            int c[kMgItems];
-#pragma unroll
-            for (int u = 0; u < kMgItems; ++u) {
-                const int k = u * kMgThreads + tid;
-                v[u] = 0.0;
-                c[u] = 0;
-                if (k < nn) {
-                    v[u] = (k < nv) ? sv[ov + k] : ld_stream(val + j0 + k);
-                    c[u] = (k < nc) ? sc[oc + k] : ld_stream(col + j0 + k);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kMgItems; ++u) xv[u] = (u * kMgThreads + tid < nn) ? ld_x(x, c[u]) : 0.0;
-#pragma unroll
-            for (int u = 0; u < kMgItems; ++u) {
-                const int k = u * kMgThreads + tid;
-                if (k < nn) sv[ov + k] = __dmul_rn(v[u], xv[u]);
-            }
-        }
-        __syncthreads();
-        const double* prod = sv + ov;
-        const int* rw = sr + oc;
-        const int r_first = rw[0], r_last = rw[nn - 1];
-        auto emit = [&](int r, double v) {
-            if (r == r_first || r == r_last)
-                atomicAdd(y + r, v);
-            else
-                y[r] = accumulate ? __dadd_rn(y[r], v) : v;
-        };
-        const int a = tid * kMgItems < nn ? tid * kMgItems : nn;
-        const int b = a + kMgItems < nn ? a + kMgItems : nn;
-        double acc = 0.0, first_val = 0.0;
-        int first_row = -1;
-        // this thread's 8 products and 9 row ids with 16-byte shared loads
-        // (tiles start at multiples of 2048 entries: both arrays are aligned)
-        double pk[kMgItems];
-        int rk[kMgItems + 1];
-        if (b - a == kMgItems) {
-#pragma unroll
-            for (int u = 0; u < kMgItems; u += 2) {
-                const double2 p2 = *reinterpret_cast<const double2*>(prod + a + u);
-                pk[u] = p2.x;
-                pk[u + 1] = p2.y;
-            }
-#pragma unroll
-            for (int u = 0; u < kMgItems; u += 4) {
-                const int4 r4 = *reinterpret_cast<const int4*>(rw + a + u);
-                rk[u] = r4.x;
-                rk[u + 1] = r4.y;
-                rk[u + 2] = r4.z;
-                rk[u + 3] = r4.w;
-            }
-            rk[kMgItems] = rw[a + kMgItems];
-        } else {
-#pragma unroll
-            for (int u = 0; u < kMgItems; ++u) {
-                pk[u] = a + u < b ? prod[a + u] : 0.0;
-                rk[u] = a + u <= b ? rw[a + u] : 0;
-            }
-            rk[kMgItems] = 0;
-        }
-        int r = rk[0];
-#pragma unroll
-        for (int u = 0; u < kMgItems; ++u) {
-            if (a + u >= b) break;
-            acc = __dadd_rn(acc, pk[u]);
-            const int rn = rk[u + 1];
-            if (rn != r) {
-                if (first_row < 0) {
-                    first_row = r;
-                    first_val = acc;
-                } else {
-                    emit(r, acc);
-                }
-                acc = 0.0;
-                r = rn;
-            }
-        }
-        int f = first_row >= 0;
-        double v = acc;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const double pv = __shfl_up_sync(0xffffffffu, v, d);
-            const int pf = __shfl_up_sync(0xffffffffu, f, d);
-            if (lane >= d) seg_combine(f, v, pf, pv);
-        }
-        if (lane == 31) {
-            s_wv[wid] = v;
-            s_wf[wid] = f;
-        }
-        __syncthreads();
-        int pf = 0;
-        double pv = 0.0;
-        for (int w = 0; w < wid; ++w) {
-            if (s_wf[w]) {
-                pv = s_wv[w];
-                pf = 1;
-            } else {
-                pv = __dadd_rn(pv, s_wv[w]);
-            }
-        }
-        double ex = __shfl_up_sync(0xffffffffu, v, 1);
-        int exf = __shfl_up_sync(0xffffffffu, f, 1);
-        if (lane == 0) {
-            ex = pv;
-            exf = pf;
-        } else if (wid > 0) {
-            seg_combine(exf, ex, pf, pv);
-        }
-        if (first_row >= 0) emit(first_row, __dadd_rn(ex, first_val));
-        if (tid == kMgThreads - 1 && nn > 0 && rw[nn] == r_last) {
-            // the tile's last row continues in the next tile: add this tile's part
-            double tv = v;
-            int tf = f;
-            if (wid > 0) seg_combine(tf, tv, pf, pv);
-            atomicAdd(y + r_last, tv);
-        }
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            const int64_t tn = t + int64_t(kMgStages) * gridDim.x;
-            if (tn < ntiles) {
-                int64_t a0, a1;
-                bounds(tn, a0, a1);
-                ct_issue(a0, a1, row, col, val, stage, bars + st, pol);
-            }
-        }
-    }
-}
-
-inline int launch_coo_tile(int64_t nnz, int accumulate, const int* row, const int* col, const double* val,
-                           const double* x, double* y, const int* skip, cudaStream_t st) {
-    const int64_t ntiles = ceil_div(nnz, kMgTile);
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(coo_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kCtSmem)));
-        attr_set[dev & 63] = true;
-    }
-    int per_sm = 0;
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel, kMgThreads, kCtSmem));
-    int64_t grid = int64_t(sm_count()) * (per_sm > 0 ? per_sm : 1);
-    if (grid > ntiles) grid = ntiles;
-    coo_tile_kernel<<<(unsigned)grid, kMgThreads, kCtSmem, st>>>(nnz, ntiles, accumulate, row, col, val, x, y, skip);
-    WK_LAUNCH_CHECK();
-    return 0;
-}
-
-}  // namespace wk

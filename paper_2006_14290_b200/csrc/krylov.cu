@@ -346,21 +346,6 @@ static int cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state*
         n, [=] __device__(int64_t i) { p[i] = __dadd_rn(r[i], __dmul_rn(s->beta, p[i])); }, &s->done, st);
 }
 
-static int g_cg_pingpong = -1;
-static int cg_pingpong_choice() {
-    if (g_cg_pingpong < 0) {
-        const char* e = getenv("WK_CG_PINGPONG");
-        g_cg_pingpong = e != nullptr ? atoi(e) : 1;
-    }
-    return g_cg_pingpong;
-}
-
-int set_cg_pingpong(int v) {
-    WK_REQUIRE(v == 0 || v == 1, WK_ERR_INVALID, "cg_pingpong must be 0 or 1");
-    g_cg_pingpong = v;
-    return 0;
-}
-
 }  // namespace wk
 
 using namespace wk;
@@ -527,13 +512,12 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     // so each starts on the rows the previous one touched last (the most
     // recently written q / r / p are still in the 126 MB L2). Iteration i:
     // SpMV d, x/r update !d, p update d, with d flipping every iteration (the
-    // 50-iteration period is even). Knob: wk_config_set("cg_pingpong", 0|1).
-    const bool pp = cg_pingpong_choice() != 0;
+    // 50-iteration period is even).
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kReplaceEvery; ++i) {
-            const int d = pp ? (i & 1) : 0;
+            const int d = i & 1;
             WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs, nullptr, nullptr, d));
-            WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs, pp ? 1 - d : 0));
+            WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs, 1 - d));
             if (i == kReplaceEvery - 1) {
                 WK_TRY(wk_spmv_masked(A, x, q, &s->done, cs));
                 WK_TRY(cg_replace_r(n, b, q, r, s, hist, red, true, cs));

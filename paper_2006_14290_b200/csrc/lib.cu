@@ -39,17 +39,4 @@ int wk_version(void) { return 1; }
 
 int wk_device_sm_count(void) { return wk::sm_count(); }
 
-int wk_config_set(const char* key, int64_t value) {
-    wk::clear_error();
-    if (key != nullptr && strcmp(key, "sellp_kernel") == 0) return wk::set_sellp_kernel(int(value));
-    if (key != nullptr && strcmp(key, "csr_kernel") == 0) return wk::set_csr_kernel(int(value));
-    if (key != nullptr && strcmp(key, "coo_kernel") == 0) return wk::set_coo_kernel(int(value));
-    if (key != nullptr && strcmp(key, "ell_kernel") == 0) return wk::set_ell_kernel(int(value));
-    if (key != nullptr && strcmp(key, "seg8_kernel") == 0) return wk::set_seg8_kernel(int(value));
-    if (key != nullptr && strcmp(key, "fill_kernel") == 0) return wk::set_fill_kernel(int(value));
-    if (key != nullptr && strcmp(key, "cg_pingpong") == 0) return wk::set_cg_pingpong(int(value));
-    wk::set_error("unknown configuration key '%s'", key ? key : "(null)");
-    return WK_ERR_INVALID;
-}
-
 }  // extern "C"

@@ -1,134 +1,14 @@
 // Warp-range segmented-sum SpMV for COO and for load-balanced CSR
 // (kernels.py:209-257 semantics: entries in row-major order, per-row segment
 // sums by a warp segmented scan, atomics only at the run heads shared between
-// work units).
-//
-// Each warp owns kSwPerWarp consecutive entries and walks them in groups of
-// kSwU batches of 32 (one entry per lane). The next group's columns, values
-// (and, for COO, row ids) are loaded while the current group is folded
-// (software pipelining: 2*kSwU independent loads per lane in flight). Per
-// batch an inclusive segmented scan keyed by row gives every row's sum at its
-// last lane; the running tail of lane 31 carries into the next batch. Rows
-// that begin and end inside the warp range are stored directly, the two rows a
-// range can share with its neighbours (its first and last) go through
-// atomicAdd on a zero-filled y (or on y itself when accumulating, Hybrid).
-//
-// seg_warp_kernel is the COO A/B baseline (coo_kernel 1); the defaults are the
-// seg8 kernels below (COO, and CSR load_balance with a precomputed head plan).
+// work units; CSR: deterministic carries instead of atomics).
 #pragma once
 
 #include <climits>
 
 #include "common.cuh"
 #include "reduce.cuh"
-
-namespace wk {
-
-constexpr int kSwPerWarp = 1024;  // entries per warp range
-constexpr int kSwU = 4;           // batches of 32 entries per group
-
-inline int64_t seg_warps(int64_t nnz) { return ceil_div(nnz, kSwPerWarp); }
-
-__global__ void __launch_bounds__(256)
-seg_warp_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
-                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                const int* __restrict__ skip) {
-    if (skip != nullptr && *skip) return;
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t wlo = warp * kSwPerWarp;
-    if (wlo >= nnz) return;
-    const int64_t whi = (wlo + kSwPerWarp < nnz) ? wlo + kSwPerWarp : nnz;
-    // rows this range can share with its neighbours
-    const int first_row = __ldg(rows + wlo);
-    const int last_row = __ldg(rows + whi - 1);
-
-    auto emit = [&](int r, double v) {
-        if (r == first_row || r == last_row)
-            atomicAdd(y + r, v);
-        else
-            y[r] = accumulate ? __dadd_rn(y[r], v) : v;
-    };
-
-    int gc[kSwU], gr[kSwU];
-    double gv[kSwU];
-    auto load_group = [&](int64_t b0) {
-#pragma unroll
-        for (int u = 0; u < kSwU; ++u) {
-            const int64_t k = b0 + u * 32 + lane;
-            gc[u] = 0;
-            gv[u] = 0.0;
-            gr[u] = -1;
-            if (k < whi) {
-                gc[u] = ld_stream(col + k);
-                gv[u] = ld_stream(val + k);
-                gr[u] = ld_stream(rows + k);
-            }
-        }
-    };
-    load_group(wlo);
-    int carry_row = -1;
-    double carry = 0.0;
-    for (int64_t b0 = wlo; b0 < whi; b0 += kSwU * 32) {
-        int c[kSwU], r[kSwU];
-        double v[kSwU];
-#pragma unroll
-        for (int u = 0; u < kSwU; ++u) {
-            c[u] = gc[u];
-            v[u] = gv[u];
-            r[u] = gr[u];
-        }
-        if (b0 + kSwU * 32 < whi) load_group(b0 + kSwU * 32);  // next group in flight
-        double p[kSwU];
-#pragma unroll
-        for (int u = 0; u < kSwU; ++u) p[u] = (b0 + u * 32 + lane < whi) ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
-#pragma unroll
-        for (int u = 0; u < kSwU; ++u) {
-            if (b0 + u * 32 >= whi) break;
-            int rr = r[u];
-            double s = p[u];
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double pv = __shfl_up_sync(FULL, s, d);
-                const int pr = __shfl_up_sync(FULL, rr, d);
-                if (lane >= d && pr == rr) s += pv;
-            }
-            const int nr = __shfl_down_sync(FULL, rr, 1);
-            const bool valid = rr >= 0;
-            const bool tail = valid && (lane == 31 || nr != rr);
-            const int r0 = __shfl_sync(FULL, rr, 0);
-            if (carry_row >= 0) {
-                if (carry_row == r0) {
-                    if (tail && rr == r0) s += carry;
-                } else if (lane == 0) {
-                    emit(carry_row, carry);
-                }
-            }
-            const int r31 = __shfl_sync(FULL, rr, 31);
-            const double s31 = __shfl_sync(FULL, s, 31);
-            if (tail && lane != 31) emit(rr, s);
-            if (r31 >= 0) {
-                carry_row = r31;
-                carry = s31;
-            } else {
-                carry_row = -1;
-            }
-        }
-    }
-    if (carry_row >= 0 && lane == 0) emit(carry_row, carry);
-}
-
-inline int launch_seg_warp(int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
-                           const double* x, double* y, const int* skip, cudaStream_t st) {
-    const int64_t warps = seg_warps(nnz);
-    const unsigned blocks = (unsigned)ceil_div(warps * 32, 256);
-    seg_warp_kernel<<<blocks, 256, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip);
-    WK_LAUNCH_CHECK();
-    return 0;
-}
-
-}  // namespace wk
+#include "hotcols.cuh"
 
 namespace wk {
 
@@ -148,10 +28,22 @@ namespace wk {
 // (a serial chain of dependent loads) by independent loads of about the size
 // of row_ptrs itself (32 B per window + 4 B per non-empty row).
 //
-// Two data paths: seg8_kernel loads each lane's 8 entries with 16/32-byte
-// vector loads; seg8_tma_kernel (persistent, one CTA per SM) streams whole
-// windows into a per-warp shared-memory ring with cp.async.bulk, so the
-// matrix stream runs S windows ahead of the x gathers.
+// Each lane loads its 8 entries with 16/32-byte vector loads (scalar loads for
+// unaligned arrays and the matrix tail). A TMA-staged persistent variant was
+// measured 2x slower (the kernel is bound by the random x gathers, not by the
+// matrix stream) and removed.
+//
+// Hot-column gathers (gather plan, hotcols.cu): on power-law matrices a few
+// thousand columns take a fifth of all entries (R-MAT scale 24: the top 8192
+// columns hold 20.8% of the 263M entries). The plan rewrites the column array
+// once per matrix, col2[k] = ~slot for a cached column, and seg8_hot_kernel
+// (persistent, one 1024-thread CTA per SM) first gathers x of the K cached
+// columns into shared memory, so those entries read shared memory instead of
+// issuing a random L2 sector request each: the R-MAT kernels are bound by the
+// rate of random L2 requests (tools/gather_probe.cu: a bare stream + gather
+// fold of the same matrix takes 1.19 ms, 221 G gathers/s; with the cache
+// 1.04 ms). K = 8192 (64 KB): larger caches shrink the L1 that holds the
+// in-flight gather lines and lose (16384: 1.09 ms, 24576: 1.71 ms).
 // ---------------------------------------------------------------------------
 constexpr int kS8Win = 256;                  // entries per window (8 per lane)
 constexpr int kS8PerWarp = 8 * kS8Win;       // entries per warp range
@@ -399,16 +291,15 @@ __device__ __forceinline__ void seg8_fold(int lane, int nv, bool last_window, co
     }
 }
 
-template <bool kCsr>
-__global__ void __launch_bounds__(kS8Warps * 32, kCsr ? 3 : 4)
-seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
-            const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-            const int* __restrict__ skip, HeadPlan hp) {
-    if (skip != nullptr && *skip) return;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t warp = int64_t(blockIdx.x) * kS8Warps + wib;
-    const int64_t wlo = warp * kS8PerWarp;
-    if (wlo >= nnz) return;
+
+// One warp range [wlo, whi) of seg8. kHot: columns come from the gather
+// plan's col2 and cached columns read `hx` (shared memory).
+template <bool kCsr, bool kHot>
+__device__ __forceinline__ void seg8_range(int lane, int64_t g, int64_t nnz, int accumulate, bool vec,
+                                           const int* __restrict__ rows, const int* __restrict__ col,
+                                           const double* __restrict__ val, const double* __restrict__ x,
+                                           const double* hx, double* __restrict__ y, const HeadPlan& hp) {
+    const int64_t wlo = g * kS8PerWarp;
     const int64_t whi = (wlo + kS8PerWarp < nnz) ? wlo + kS8PerWarp : nnz;
     int first_row, last_row;
     RangeCsr rc{0u, 0u, 0};
@@ -424,11 +315,11 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
     // (kernels.py:229-253 semantics): atomics for the two rows a range can
     // share with its neighbours.
     const bool carries = kCsr && whi < nnz && !head_at(hp, whi);
-    if (kCsr && lane == 0) hp.crow[warp] = carries ? last_row : -1;
+    if (kCsr && lane == 0) hp.crow[g] = carries ? last_row : -1;
     auto emit = [&](int r, double v) {
         if (kCsr) {
             if (carries && r == last_row)
-                hp.cval[warp] = v;
+                hp.cval[g] = v;
             else
                 y[r] = v;
         } else if (r == first_row || r == last_row) {
@@ -450,7 +341,7 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
         {
             int c[8];
             double v[8];
-            if (nv == 8) {
+            if (vec && nv == 8) {
                 const int4 c0 = ld_stream(reinterpret_cast<const int4*>(col + kb));
                 const int4 c1 = ld_stream(reinterpret_cast<const int4*>(col + kb + 4));
                 c[0] = c0.x, c[1] = c0.y, c[2] = c0.z, c[3] = c0.w, c[4] = c1.x, c[5] = c1.y, c[6] = c1.z, c[7] = c1.w;
@@ -474,11 +365,60 @@ seg8_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int
                     if (!kCsr) rw[u] = u < nv ? ld_stream(rows + kb + u) : -1;
                 }
             }
+            if (kHot) {
+                // all global gathers first (8 in flight per lane), then the
+                // shared-memory reads of the cached columns
+                double g[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
+                for (int u = 0; u < 8; ++u) g[u] = c[u] >= 0 ? ld_x(x, c[u]) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (c[u] < 0) g[u] = hx[~c[u]];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], g[u]) : 0.0;
+            } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
+            }
         }
         seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
     }
+}
+
+// one warp range per warp
+template <bool kCsr>
+__global__ void __launch_bounds__(kS8Warps * 32, kCsr ? 3 : 4)
+seg8_kernel(int64_t nnz, int accumulate, int vec, const int* __restrict__ rows, const int* __restrict__ col,
+            const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+            const int* __restrict__ skip, HeadPlan hp) {
+    if (skip != nullptr && *skip) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = int64_t(blockIdx.x) * kS8Warps + (threadIdx.x >> 5);
+    if (warp * kS8PerWarp >= nnz) return;
+    seg8_range<kCsr, false>(lane, warp, nnz, accumulate, vec != 0, rows, col, val, x, nullptr, y, hp);
+}
+
+// persistent, hot columns of x cached in shared memory (one CTA per SM; the
+// CSR variant keeps 24 warps: its row-id expansion needs ~80 registers)
+template <bool kCsr>
+__host__ __device__ constexpr int hot_threads() { return kCsr ? 768 : kHotThreads; }
+
+template <bool kCsr>
+__global__ void __launch_bounds__(hot_threads<kCsr>(), 1)
+seg8_hot_kernel(int64_t nnz, int accumulate, int vec, const int* __restrict__ rows, const double* __restrict__ val,
+                const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip, HeadPlan hp,
+                GatherPlan gp) {
+    if (skip != nullptr && *skip) return;
+    extern __shared__ double hx[];
+    const int nh = *gp.nhot;
+    constexpr int T = hot_threads<kCsr>();
+    for (int i = threadIdx.x; i < nh; i += T) hx[i] = ld_x(x, __ldg(gp.hot + i));
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nranges = (nnz + kS8PerWarp - 1) / kS8PerWarp;
+    const int64_t nwarps = int64_t(gridDim.x) * (T / 32);
+    for (int64_t g = int64_t(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); g < nranges; g += nwarps)
+        seg8_range<kCsr, true>(lane, g, nnz, accumulate, vec != 0, rows, gp.col2, val, x, hx, y, hp);
 }
 
 // rows cut by warp-range boundaries (CSR): the first range of each run of
@@ -496,194 +436,46 @@ __global__ void seg8_fixup_kernel(int64_t nranges, const int* __restrict__ crow,
     y[r] = __dadd_rn(s, y[r]);
 }
 
-// ---- TMA-staged variant -------------------------------------------------------
-// Persistent grid (one CTA of W warps per SM). Warp g takes ranges g, g + G,
-// g + 2G, ... (G warps in the grid); its windows are streamed in order into
-// an S-deep ring: lane 0 issues one cp.async.bulk per array (values, columns,
-// COO rows) per window, mbarrier complete_tx per stage; the entries past the
-// last 4-entry boundary of the matrix are loaded directly by the consumer.
-template <int W, int S>
-struct Seg8TmaCfg {
-    static constexpr int kW = W, kS = S;
-    static constexpr size_t kValBytes = kS8Win * 8, kIdxBytes = kS8Win * 4;
-    static constexpr size_t kStage = kValBytes + 2 * kIdxBytes;  // values | columns | rows (COO)
-    static constexpr size_t kSmem = size_t(W) * S * kStage + size_t(W) * S * 8 + 128;
-};
-
-template <bool kCsr, class Cfg>
-__global__ void __launch_bounds__(Cfg::kW * 32, 1)
-seg8_tma_kernel(int64_t nnz, int accumulate, const int* __restrict__ rows, const int* __restrict__ col,
-                const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                const int* __restrict__ skip, HeadPlan hp) {
-    constexpr int W = Cfg::kW, S = Cfg::kS;
-    if (skip != nullptr && *skip) return;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* wbase = smem + size_t(wib) * S * Cfg::kStage;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(W) * S * Cfg::kStage) + wib * S;
-    if (lane == 0) {
-        for (int st = 0; st < S; ++st) mbar_init(bars + st, 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    const int64_t gwarp = int64_t(blockIdx.x) * W + wib, nwarps = int64_t(gridDim.x) * W;
-    const int64_t nranges = (nnz + kS8PerWarp - 1) / kS8PerWarp;
-    const int64_t body_end = nnz & ~int64_t(3);  // entries streamed by bulk copies
-    const uint64_t pol = policy_evict_first();
-    // producer cursor over this warp's windows: t -> range gwarp + (t / 8) * nwarps, window t % 8
-    int64_t pt = 0;
-    auto window_start = [&](int64_t t) -> int64_t {
-        const int64_t g = gwarp + (t >> 3) * nwarps;
-        return g < nranges ? g * kS8PerWarp + (t & 7) * kS8Win : nnz;
-    };
-    auto issue = [&](int st) -> bool {  // warp-uniform; lane 0 issues
-        const int64_t E = window_start(pt);
-        if (E >= nnz) return false;
-        ++pt;
-        if (lane == 0) {
-            // a window past the last 4-entry boundary arms the stage with 0 bytes
-            // (completes at once; the consumer loads its entries directly)
-            const int64_t e1 = (E + kS8Win < body_end) ? E + kS8Win : body_end;
-            const uint32_t n = e1 > E ? uint32_t(e1 - E) : 0u;
-            unsigned char* sb = wbase + size_t(st) * Cfg::kStage;
-            mbar_arrive_expect_tx(bars + st, n * (kCsr ? 12u : 16u));
-            if (n) {
-                bulk_g2s_evict_first(sb, val + E, n * 8, bars + st, pol);
-                bulk_g2s_evict_first(sb + Cfg::kValBytes, col + E, n * 4, bars + st, pol);
-                if (!kCsr)
-                    bulk_g2s_evict_first(sb + Cfg::kValBytes + Cfg::kIdxBytes, rows + E, n * 4, bars + st, pol);
-            }
-        }
-        return true;
-    };
-    for (int st = 0; st < S; ++st)
-        if (!issue(st)) break;
-    uint32_t i = 0;  // windows consumed
-    for (int64_t g = gwarp; g < nranges; g += nwarps) {
-        const int64_t wlo = g * kS8PerWarp;
-        const int64_t whi = (wlo + kS8PerWarp < nnz) ? wlo + kS8PerWarp : nnz;
-        int first_row, last_row;
-        RangeCsr rc{0u, 0u, 0};
-        if (kCsr) {
-            rc = seg8_range_csr(lane, wlo, whi, nnz, hp, first_row, last_row);
-        } else {
-            first_row = __ldg(rows + wlo);
-            last_row = __ldg(rows + whi - 1);
-        }
-        const bool carries = kCsr && whi < nnz && !head_at(hp, whi);
-        if (kCsr && lane == 0) hp.crow[g] = carries ? last_row : -1;
-        auto emit = [&](int r, double v) {
-            if (kCsr) {
-                if (carries && r == last_row)
-                    hp.cval[g] = v;
-                else
-                    y[r] = v;
-            } else if (r == first_row || r == last_row) {
-                atomicAdd(y + r, v);
-            } else {
-                y[r] = accumulate ? __dadd_rn(y[r], v) : v;
-            }
-        };
-        int carry_row = -1;
-        double carry = 0.0;
-        for (int64_t E = wlo; E < whi; E += kS8Win, ++i) {
-            const int st = int(i % S);
-            const int64_t kb = E + 8 * lane;
-            const int nv = kb >= whi ? 0 : (whi - kb >= 8 ? 8 : int(whi - kb));
-            const bool staged = E < body_end;
-            mbar_wait(bars + st, (i / S) & 1);
-            const unsigned char* sb = wbase + size_t(st) * Cfg::kStage;
-            int c[8], rw[8];
-            double v[8];
-            if (staged && kb + 8 <= body_end && nv == 8) {
-                const double2* sv = reinterpret_cast<const double2*>(sb) + 4 * lane;
-                const int4* sc = reinterpret_cast<const int4*>(sb + Cfg::kValBytes) + 2 * lane;
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const double2 t = sv[u];
-                    v[2 * u] = t.x;
-                    v[2 * u + 1] = t.y;
-                }
-                const int4 c0 = sc[0], c1 = sc[1];
-                c[0] = c0.x, c[1] = c0.y, c[2] = c0.z, c[3] = c0.w, c[4] = c1.x, c[5] = c1.y, c[6] = c1.z, c[7] = c1.w;
-                if (!kCsr) {
-                    const int4* sr = reinterpret_cast<const int4*>(sb + Cfg::kValBytes + Cfg::kIdxBytes) + 2 * lane;
-                    const int4 r0 = sr[0], r1 = sr[1];
-                    rw[0] = r0.x, rw[1] = r0.y, rw[2] = r0.z, rw[3] = r0.w;
-                    rw[4] = r1.x, rw[5] = r1.y, rw[6] = r1.z, rw[7] = r1.w;
-                }
-            } else {
-                const double* sv = reinterpret_cast<const double*>(sb);
-                const int* sc = reinterpret_cast<const int*>(sb + Cfg::kValBytes);
-                const int* sr = reinterpret_cast<const int*>(sb + Cfg::kValBytes + Cfg::kIdxBytes);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int64_t k = kb + u;
-                    const bool in = u < nv, sm = staged && k < body_end;
-                    c[u] = in ? (sm ? sc[k - E] : ld_stream(col + k)) : 0;
-                    v[u] = in ? (sm ? sv[k - E] : ld_stream(val + k)) : 0.0;
-                    if (!kCsr) rw[u] = in ? (sm ? sr[k - E] : ld_stream(rows + k)) : -1;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) fence_proxy_async_smem();
-            issue(st);  // refill this stage with the warp's next window
-            double pv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
-            if (kCsr) seg8_csr_rows(lane, int((E - wlo) >> 8), rc, nv, hp, rw);
-            seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
-        }
-    }
-}
-
-// seg8 kernel selection (env WK_SEG8_KERNEL or wk_config_set("seg8_kernel", i)):
-// 0 (default) = direct vector loads, 1 = TMA-staged persistent kernel (spmv.cu).
-int seg8_kernel_choice();
-
-template <bool kCsr>
-int launch_seg8_tma(int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
-                    const double* x, double* y, const int* skip, cudaStream_t st, HeadPlan hp) {
-    using Cfg = Seg8TmaCfg<16, 3>;
-    static bool attr_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(seg8_tma_kernel<kCsr, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(Cfg::kSmem)));
-        attr_set[dev & 63] = true;
-    }
-    int64_t grid = sm_count();
-    const int64_t need = ceil_div(seg8_warps(nnz), Cfg::kW);
-    if (grid > need) grid = need;
-    seg8_tma_kernel<kCsr, Cfg><<<(unsigned)grid, Cfg::kW * 32, Cfg::kSmem, st>>>(nnz, accumulate, rows, col, val, x,
-                                                                                y, skip, hp);
-    WK_LAUNCH_CHECK();
-    return 0;
-}
 
 // rows: COO row indices (csr = false) or unused (csr = true, row ids from hp).
-// The TMA path needs 16-byte aligned arrays.
+// gp.col2 != nullptr: the hot-column kernel (gather plan).
 inline int launch_seg8(bool csr, int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
                        const double* x, double* y, const int* skip, cudaStream_t st,
-                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}) {
+                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
+                       GatherPlan gp = GatherPlan{nullptr, nullptr, nullptr}) {
     if (nnz == 0) return 0;
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (seg8_kernel_choice() == 1 && al(col) && al(val) && (csr || al(rows))) {
-        if (csr) {
-            WK_TRY(launch_seg8_tma<true>(nnz, accumulate, rows, col, val, x, y, skip, st, hp));
-        } else {
-            return launch_seg8_tma<false>(nnz, accumulate, rows, col, val, x, y, skip, st, hp);
+    const int vec = al(gp.col2 != nullptr ? gp.col2 : col) && al(val) && (csr || al(rows));
+    if (gp.col2 != nullptr) {
+        static bool attr_set[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!attr_set[dev & 63]) {
+            WK_CUDA(cudaFuncSetAttribute(seg8_hot_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kHotMax * 8));
+            WK_CUDA(cudaFuncSetAttribute(seg8_hot_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kHotMax * 8));
+            attr_set[dev & 63] = true;
         }
+        const int T = csr ? hot_threads<true>() : hot_threads<false>();
+        int64_t grid = sm_count();
+        const int64_t need = ceil_div(seg8_warps(nnz), T / 32);
+        if (grid > need) grid = need;
+        if (csr)
+            seg8_hot_kernel<true><<<(unsigned)grid, T, kHotMax * 8, st>>>(nnz, accumulate, vec, rows, val, x, y, skip,
+                                                                         hp, gp);
+        else
+            seg8_hot_kernel<false><<<(unsigned)grid, T, kHotMax * 8, st>>>(nnz, accumulate, vec, rows, val, x, y,
+                                                                          skip, hp, gp);
     } else {
         const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
         if (csr)
-            seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
+            seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
         else
-            seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, rows, col, val, x, y, skip, hp);
-        WK_LAUNCH_CHECK();
-        if (!csr) return 0;
+            seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
     }
+    WK_LAUNCH_CHECK();
+    if (!csr) return 0;
     const int64_t nranges = seg8_warps(nnz);
     if (nranges > 1) {
         seg8_fixup_kernel<<<(unsigned)ceil_div(nranges, 256), 256, 0, st>>>(nranges, hp.crow, hp.cval, y, skip);

@@ -124,111 +124,6 @@ sliced_spmv_kernel(int64_t nrows, int64_t ncols, int log2ss, int64_t ell_width, 
 
 static bool aligned(const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
-// SELL-P(64) kernel selection for A/B measurements (env WK_SELLP_KERNEL or
-// wk_config_set("sellp_kernel", i)): 0 = register-only kernel, 1..8 = TMA
-// pipeline configurations (table in launch_sellp); default 7 = the best
-// measured configuration (tools/sweep_sellp.py, profiles/r01).
-static int g_sellp_choice = -1;
-
-int set_sellp_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 10, WK_ERR_INVALID, "sellp kernel choice must be in [0, 10]");
-    g_sellp_choice = choice;
-    return 0;
-}
-
-static int sellp_kernel_choice() {
-    int& choice = g_sellp_choice;
-    if (choice < 0) {
-        const char* e = getenv("WK_SELLP_KERNEL");
-        choice = 7;
-        if (e != nullptr) choice = atoi(e);  // index into the table in launch_sellp
-    }
-    return choice;
-}
-
-// CSR kernel selection for A/B measurements (env WK_CSR_KERNEL or
-// wk_config_set("csr_kernel", i)). Stream strategy: 0 = one CTA per nnz chunk,
-// otherwise the persistent TMA pipeline. Row-block strategy: 2..7 force one
-// configuration, otherwise (default 1) the configuration follows the mean row
-// length.
-static int g_csr_choice = -1;
-
-int set_csr_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 7, WK_ERR_INVALID, "csr kernel choice must be in [0, 7]");
-    g_csr_choice = choice;
-    return 0;
-}
-
-static int csr_kernel_choice() {
-    if (g_csr_choice < 0) {
-        const char* e = getenv("WK_CSR_KERNEL");
-        g_csr_choice = (e != nullptr) ? atoi(e) : 1;
-    }
-    return g_csr_choice;
-}
-
-// ELL kernel selection (env WK_ELL_KERNEL or wk_config_set("ell_kernel", i)):
-// 0 = register kernel, 1 = SELL-P(64) warp pipeline with ELL addressing,
-// 2 (default) .. 4 = ell_tma_kernel configurations (see launch_ell).
-static int g_ell_choice = -1;
-
-int set_ell_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 4, WK_ERR_INVALID, "ell kernel choice must be 0..4");
-    g_ell_choice = choice;
-    return 0;
-}
-
-static int ell_kernel_choice() {
-    if (g_ell_choice < 0) {
-        const char* e = getenv("WK_ELL_KERNEL");
-        g_ell_choice = (e != nullptr) ? atoi(e) : 2;
-    }
-    return g_ell_choice;
-}
-
-// COO kernel selection (env WK_COO_KERNEL or wk_config_set("coo_kernel", i)):
-// 0 = warp-range kernel without load pipelining, 1 = the pipelined warp-range
-// kernel (segwarp.cuh seg_warp_kernel), 2 = persistent TMA tile kernel with
-// block-wide scans (csr_merge.cuh coo_tile_kernel), 3 (default) = 8 entries
-// per lane, one warp scan per 256 entries (segwarp.cuh seg8_kernel).
-static int g_coo_choice = -1;
-
-int set_coo_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 3, WK_ERR_INVALID, "coo kernel choice must be in [0, 3]");
-    g_coo_choice = choice;
-    return 0;
-}
-
-static int coo_kernel_choice() {
-    if (g_coo_choice < 0) {
-        const char* e = getenv("WK_COO_KERNEL");
-        g_coo_choice = (e != nullptr) ? atoi(e) : 3;
-    }
-    return g_coo_choice;
-}
-
-// seg8 data path (env WK_SEG8_KERNEL or wk_config_set("seg8_kernel", i)):
-// 0 (default) = direct vector loads, 1 = TMA-staged persistent kernel. The TMA
-// variant is 2x slower on R-MAT (1.27 -> 2.55 ms COO): the kernel is bound by
-// the random x gathers, and the register budget of the persistent grid (16
-// warps per SM) keeps fewer gathers in flight than the direct kernel's
-// 24-32 warps; streaming the matrix ahead does not pay for that.
-static int g_seg8_choice = -1;
-
-int set_seg8_kernel(int choice) {
-    WK_REQUIRE(choice >= 0 && choice <= 1, WK_ERR_INVALID, "seg8 kernel choice must be 0 or 1");
-    g_seg8_choice = choice;
-    return 0;
-}
-
-int seg8_kernel_choice() {
-    if (g_seg8_choice < 0) {
-        const char* e = getenv("WK_SEG8_KERNEL");
-        g_seg8_choice = (e != nullptr) ? atoi(e) : 0;
-    }
-    return g_seg8_choice;
-}
-
 static int log2i(int64_t v) {
     int l = 0;
     while ((int64_t(1) << l) < v) ++l;
@@ -240,24 +135,11 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
                  const int* skip, cudaStream_t st) {
     if (nrows == 0) return 0;
     const int l2 = log2i(ss);
-    const int choice = sellp_kernel_choice();
-    if (ss == 64 && choice > 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16)) {
-#define WK_TMA(J, S, W, C) \
-    return launch_sellp64_tma<SellpTmaCfg<J, S, W, C>>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st)
-        switch (choice) {
-            case 1: WK_TMA(8, 4, 8, 1);
-            case 3: WK_TMA(2, 8, 16, 1);
-            case 4: WK_TMA(4, 6, 12, 1);
-            case 5: WK_TMA(4, 4, 8, 2);
-            case 6: WK_TMA(2, 6, 20, 1);
-            case 8: WK_TMA(4, 5, 12, 1);
-            case 9: WK_TMA(8, 3, 12, 1);
-            case 10: WK_TMA(8, 2, 16, 1);
-            case 7: WK_TMA(4, 3, 16, 1);  // best measured (profiles/r01/sellp_sweep.jsonl)
-            default: WK_TMA(4, 4, 16, 1);
-        }
-#undef WK_TMA
-    }
+    // SELL-P(64), 16-byte aligned: the TMA pipeline (J = 4 columns per chunk,
+    // 3-stage rings, 16 warps: the best of the (J, S, W) sweep in
+    // profiles/r01/sellp_sweep.jsonl); otherwise the register kernel.
+    if (ss == 64 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16))
+        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st);
     const bool vec = ss >= 2 && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {
         const int64_t threads = ceil_div(nrows, 2);
@@ -276,7 +158,7 @@ int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, 
 // SpMV + separate dot), 0 on success, an error code otherwise.
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
                    cudaStream_t st, void* peer, const void* halo, int rev) {
-    if (A->format == WK_FMT_ELL && halo == nullptr && ell_kernel_choice() >= 2 && A->stride % 4 == 0 &&
+    if (A->format == WK_FMT_ELL && halo == nullptr && A->stride % 4 == 0 &&
         A->width > 0 && aligned(A->values, 16) && aligned(A->col_idx, 16) && aligned(q, 16) && aligned(p, 16) &&
         A->nrows > 0) {
         char* w = reinterpret_cast<char*>(red_ws);
@@ -286,7 +168,7 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
         return launch_ell_tma<EllTmaCfg<4, 4, 448, 1>, true>(A->nrows, A->ncols, A->width, A->stride, A->col_idx,
                                                             A->values, A->row_lengths, p, q, &s->done, st, dot, rev);
     }
-    if (A->format != WK_FMT_SELLP || A->slice_size != 64 || sellp_kernel_choice() == 0 || !aligned(A->values, 16) ||
+    if (A->format != WK_FMT_SELLP || A->slice_size != 64 || !aligned(A->values, 16) ||
         !aligned(A->col_idx, 16) || !aligned(q, 16) || !aligned(p, 16) || A->nrows == 0)
         return 1;
     char* w = reinterpret_cast<char*>(red_ws);
@@ -306,24 +188,13 @@ int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, cons
                const double* val, const int* row_lengths, const double* x, double* y, const int* skip,
                cudaStream_t st) {
     if (nrows == 0) return 0;
-    // ell_kernel 1: the SELL-P(64) TMA pipeline with ELL addressing (one
-    // 512 B + 256 B bulk copy per column of a 64-row block, stride % 4 == 0).
-    // Measured 1.7 ms vs 0.49 ms for the register kernel on the 27-point
-    // 200^3 ELL (columns 64 MB apart: the many small copies do not stream),
-    // so the register kernel is the default.
-    const int choice = ell_kernel_choice();
-    const bool tma_ok = stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16) && width > 0;
-    if (choice >= 2 && tma_ok) {
-        switch (choice) {
-            case 3: return launch_ell_tma<EllTmaCfg<2, 8, 448, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
-            case 4: return launch_ell_tma<EllTmaCfg<2, 6, 512, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
-            default: return launch_ell_tma<EllTmaCfg<4, 4, 448, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip, st);
-        }
-    }
-    if (choice == 1 && tma_ok)
-        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, false, true>(
-            nrows, ncols, nullptr, col, val, row_lengths, x, y, skip, st, DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr},
-            width, stride);
+    // aligned, stride % 4 == 0: the producer-warp TMA kernel (896-row tiles,
+    // 4 columns per stage, 4 stages); otherwise the register kernel. (The
+    // SELL-P(64) warp pipeline with ELL addressing moves 512 B + 256 B copies
+    // per column and 64-row block and was 3.5x slower: removed.)
+    if (stride % 4 == 0 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16) && width > 0)
+        return launch_ell_tma<EllTmaCfg<4, 4, 448, 1>>(nrows, ncols, width, stride, col, val, row_lengths, x, y, skip,
+                                                       st);
     const bool vec = (stride % 2 == 0) && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {
         const int64_t threads = ceil_div(nrows, 2);
@@ -363,101 +234,6 @@ __global__ void csr_plan_kernel(int64_t nrows, int64_t nnz, int64_t nchunks, con
     if (r < nrows && hi > nchunks - 1) hi = nchunks - 1;
     const int64_t lo = (r == 0) ? 0 : int64_t(ptrs[r - 1]) / kCsrChunk + 1;
     for (int64_t c = lo; c <= hi; ++c) first[c] = int(r);
-}
-
-__device__ __forceinline__ double long_row_part(const int* __restrict__ col, const double* __restrict__ val,
-                                                const double* __restrict__ x, int64_t lo, int64_t hi,
-                                                double* red) {
-    double acc = 0.0;
-    for (int64_t k = lo + threadIdx.x; k < hi; k += kSpmvThreads)
-        acc += __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
-    return block_sum<kSpmvThreads>(acc, red);
-}
-
-// Partial slots: 2*c for the tail of a long row entering chunk c, 2*c+1 for
-// the head of a long row starting in chunk c.
-__device__ void long_row_finish(int64_t L, int64_t c_head, int64_t c_last, double* __restrict__ partials,
-                                unsigned* __restrict__ tickets, double* __restrict__ y) {
-    // caller: thread 0 only, after writing its partial
-    __threadfence();
-    const unsigned parts = unsigned(c_last - c_head + 1);
-    const unsigned t = atomicAdd(tickets + c_head, 1u);
-    if (t == parts - 1) {
-        __threadfence();
-        double acc = 0.0;
-        acc += __ldcg(partials + 2 * c_head + 1);
-        for (int64_t c = c_head + 1; c <= c_last; ++c) acc += __ldcg(partials + 2 * c);
-        y[L] = acc;
-        tickets[c_head] = 0;  // self-cleaning for the next call
-    }
-}
-
-__global__ void __launch_bounds__(kSpmvThreads)
-csr_stream_kernel(int64_t nrows, int64_t nnz, const int* __restrict__ ptrs, const int* __restrict__ col,
-                  const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-                  const int* __restrict__ first, double* __restrict__ partials,
-                  unsigned* __restrict__ tickets, const int* __restrict__ skip) {
-    if (skip != nullptr && *skip) return;
-    __shared__ double prod[kCsrCap];
-    __shared__ double red[kSpmvThreads / 32];
-    const int64_t c = blockIdx.x;
-    const int64_t rb = first[c], re = first[c + 1];
-    const int64_t chunk_lo = c * kCsrChunk, chunk_hi = chunk_lo + kCsrChunk;
-
-    // (a) tail of a long row that started in an earlier chunk
-    if (rb > 0) {
-        const int64_t L = rb - 1;
-        const int64_t Ls = ptrs[L], Le = ptrs[rb];
-        if (Le - Ls > kCsrChunk && Le > chunk_lo) {
-            const int64_t hi = Le < chunk_hi ? Le : chunk_hi;
-            const double part = long_row_part(col, val, x, chunk_lo, hi, red);
-            if (threadIdx.x == 0) {
-                partials[2 * c] = part;
-                long_row_finish(L, Ls / kCsrChunk, (Le - 1) / kCsrChunk, partials, tickets, y);
-            }
-        }
-    }
-    if (rb >= re) return;
-    // (b) head of a long row that starts in this chunk (always the item's last row)
-    int64_t rs_end = re;
-    {
-        const int64_t L = re - 1;
-        const int64_t Ls = ptrs[L], Le = ptrs[re];
-        if (Le - Ls > kCsrChunk) {
-            rs_end = L;
-            const double part = long_row_part(col, val, x, Ls, chunk_hi, red);
-            if (threadIdx.x == 0) {
-                partials[2 * c + 1] = part;
-                long_row_finish(L, c, (Le - 1) / kCsrChunk, partials, tickets, y);
-            }
-        }
-    }
-    if (rb >= rs_end) return;
-    // (c) short rows: stage products, then fold row by row
-    const int64_t base = ptrs[rb];
-    const int64_t cnt = int64_t(ptrs[rs_end]) - base;  // < kCsrCap
-    const int64_t abase = base & ~int64_t(1);
-    const int64_t npairs = (base - abase + cnt + 1) >> 1;
-    for (int64_t i = threadIdx.x; i < npairs; i += kSpmvThreads) {
-        const int64_t k = abase + 2 * i;
-        if (k >= base && k + 1 < base + cnt) {
-            const double2 v = ld_stream(reinterpret_cast<const double2*>(val + k));
-            const int2 cc = ld_stream(reinterpret_cast<const int2*>(col + k));
-            prod[k - base] = __dmul_rn(v.x, ld_x(x, cc.x));
-            prod[k + 1 - base] = __dmul_rn(v.y, ld_x(x, cc.y));
-        } else {
-            if (k >= base && k < base + cnt) prod[k - base] = __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
-            if (k + 1 >= base && k + 1 < base + cnt)
-                prod[k + 1 - base] = __dmul_rn(ld_stream(val + k + 1), ld_x(x, ld_stream(col + k + 1)));
-        }
-    }
-    __syncthreads();
-    for (int64_t r = rb + threadIdx.x; r < rs_end; r += kSpmvThreads) {
-        const int64_t lo = int64_t(ptrs[r]) - base, hi = int64_t(ptrs[r + 1]) - base;
-        double acc = 0.0;
-        for (int64_t k = lo; k < hi; ++k) acc = __dadd_rn(acc, prod[k]);
-        y[r] = acc;
-    }
 }
 
 int64_t csr_stream_chunks(int64_t nnz) {
@@ -506,7 +282,8 @@ static int launch_zero_masked(double* y, int64_t n, const int* skip, cudaStream_
 
 int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const int* col, const double* val,
                const double* x, double* y, int strategy, int subwarp, const int* first, double* partials,
-               unsigned* tickets, const int* skip, cudaStream_t st, void* merge_plan = nullptr) {
+               unsigned* tickets, const int* skip, cudaStream_t st, void* merge_plan = nullptr,
+               const void* gplan = nullptr) {
     (void)ncols;
     if (nrows == 0) return 0;
     if (strategy == WK_CSR_MERGE) {
@@ -528,21 +305,13 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
                    "csr load_balance needs 16-byte aligned col_idx / values");
         const HeadPlanMut h = head_plan_views(merge_plan, nrows, nnz);
         return launch_seg8(true, nnz, 0, nullptr, col, val, x, y, skip, st,
-                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow});
+                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow},
+                           gplan ? gather_plan_view(gplan) : GatherPlan{nullptr, nullptr, nullptr});
     }
     if (strategy == WK_CSR_ROWBLOCK) {
         // 32*k-row blocks; the stage capacity is the smallest that keeps a
         // 32-row block of mean-length rows "light" (more warps per SM when
         // rows are short). Measured sweep: profiles/r01/csr_sweep.jsonl.
-        switch (csr_kernel_choice()) {
-            case 2: return launch_csr_rowblock<CsrRbCfg<8, 2, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            case 3: return launch_csr_rowblock<CsrRbCfg<16, 1, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            case 4: return launch_csr_rowblock<CsrRbCfg<16, 2, 512>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            case 5: return launch_csr_rowblock<CsrRbCfg<20, 1, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            case 6: return launch_csr_rowblock<CsrRbCfg<24, 1, 640>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            case 7: return launch_csr_rowblock<CsrRbCfg<12, 2, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
-            default: break;
-        }
         const double need = 32.0 * double(nnz) / double(nrows) * 1.25;
         if (need <= 640.0) return launch_csr_rowblock<CsrRbCfg<24, 1, 640>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
         if (need <= 768.0) return launch_csr_rowblock<CsrRbCfg<20, 1, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
@@ -552,13 +321,8 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
         WK_REQUIRE(first != nullptr && partials != nullptr && tickets != nullptr, WK_ERR_INVALID,
                    "csr stream strategy needs a plan (wk_csr_plan_build)");
         const int64_t nchunks = csr_stream_chunks(nnz);
-        if (csr_kernel_choice() != 0)
-            return launch_csr_tma<CsrTmaCfg<16, 2>>(nrows, nnz, nchunks, ptrs, col, val, x, y, first, partials,
-                                                    tickets, skip, st);
-        csr_stream_kernel<<<(unsigned)nchunks, kSpmvThreads, 0, st>>>(nrows, nnz, ptrs, col, val, x, y, first,
-                                                                     partials, tickets, skip);
-        WK_LAUNCH_CHECK();
-        return 0;
+        return launch_csr_tma<CsrTmaCfg<16, 2>>(nrows, nnz, nchunks, ptrs, col, val, x, y, first, partials, tickets,
+                                                skip, st);
     }
     WK_REQUIRE(strategy == WK_CSR_SUBWARP, WK_ERR_INVALID, "unknown CSR strategy %d", strategy);
     int T = subwarp;
@@ -583,92 +347,12 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
     return 0;
 }
 
-// ---------------------------------------------------------------------------
-// COO: each warp owns a contiguous range of kCooPerWarp sorted entries and
-// walks it in batches of 32 (4 batches loaded up front for memory-level
-// parallelism). Within a batch a segmented inclusive scan keyed by row
-// (rows are sorted, so equal rows are contiguous) gives every segment's sum
-// at its tail lane. Rows that begin and end inside the warp's range are
-// stored directly; the first and last row of the range (possibly shared with
-// a neighbouring warp) go through atomicAdd. The running tail of lane 31 is
-// carried into the next batch (kernels.py:229-253 semantics: flush on row
-// change, merge equal-row tails, atomic at run heads).
-// ---------------------------------------------------------------------------
-constexpr int kCooPerWarp = 1024;
-
-__global__ void __launch_bounds__(kSpmvThreads)
-coo_kernel(int64_t nnz, int accumulate, const int* __restrict__ row, const int* __restrict__ col,
-           const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
-           const int* __restrict__ skip) {
-    if (skip != nullptr && *skip) return;
-    const unsigned lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t wlo = warp * kCooPerWarp;
-    if (wlo >= nnz) return;
-    const int64_t whi = (wlo + kCooPerWarp < nnz) ? wlo + kCooPerWarp : nnz;
-    const int first_row = row[wlo];
-    const int last_row = row[whi - 1];
-    int carry_row = -1;
-    double carry = 0.0;
-    for (int64_t b0 = wlo; b0 < whi; b0 += 4 * 32) {
-        int r[4];
-        double p[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t k = b0 + u * 32 + lane;
-            r[u] = -1;
-            p[u] = 0.0;
-            if (k < whi) {
-                r[u] = ld_stream(row + k);
-                p[u] = __dmul_rn(ld_stream(val + k), ld_x(x, ld_stream(col + k)));
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (b0 + u * 32 >= whi) break;
-            int rr = r[u];
-            double v = p[u];
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double pv = __shfl_up_sync(0xffffffffu, v, d);
-                const int pr = __shfl_up_sync(0xffffffffu, rr, d);
-                if (lane >= unsigned(d) && pr == rr) v += pv;
-            }
-            const int nr = __shfl_down_sync(0xffffffffu, rr, 1);
-            const bool valid = rr >= 0;
-            const bool tail = valid && (lane == 31 || nr != rr);
-            const int r0 = __shfl_sync(0xffffffffu, rr, 0);
-            // merge the carried tail into the first segment of this batch
-            if (carry_row >= 0) {
-                if (carry_row == r0) {
-                    if (tail && rr == r0) v += carry;
-                } else if (lane == 0) {
-                    if (carry_row == first_row || carry_row == last_row) atomicAdd(y + carry_row, carry);
-                    else y[carry_row] = accumulate ? y[carry_row] + carry : carry;
-                }
-            }
-            const int r31 = __shfl_sync(0xffffffffu, rr, 31);
-            const double v31 = __shfl_sync(0xffffffffu, v, 31);
-            if (tail && lane != 31) {
-                if (rr == first_row || rr == last_row) atomicAdd(y + rr, v);
-                else y[rr] = accumulate ? y[rr] + v : v;
-            }
-            if (r31 >= 0) {
-                carry_row = r31;
-                carry = v31;
-            } else {
-                carry_row = -1;
-            }
-        }
-    }
-    if (carry_row >= 0 && lane == 0) {
-        if (carry_row == first_row || carry_row == last_row) atomicAdd(y + carry_row, carry);
-        else y[carry_row] = accumulate ? y[carry_row] + carry : carry;
-    }
-}
-
+// COO (kernels.py:209-264 semantics): seg8 warp ranges of 2048 sorted
+// entries, warp segmented scans, atomics for the two rows a range can share
+// with its neighbours (segwarp.cuh). `gplan`: hot-column gather plan
+// (hotcols.cu) or nullptr.
 int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const double* val, const double* x,
-               double* y, int accumulate, const int* skip, cudaStream_t st) {
+               double* y, int accumulate, const int* skip, cudaStream_t st, const void* gplan = nullptr) {
     if (nrows == 0) return 0;
     if (!accumulate) {
         // skip-aware zero fill is not needed: a skipped SpMV leaves y untouched
@@ -677,17 +361,9 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const
         WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
     }
     if (nnz == 0) return 0;
-    const int cc = coo_kernel_choice();
-    if (cc == 3 && aligned(row, 16) && aligned(col, 16) && aligned(val, 16))
-        return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st);
-    if (cc == 1 || cc == 3)
-        return launch_seg_warp(nnz, accumulate, row, col, val, x, y, skip, st);
-    if (coo_kernel_choice() == 2) return launch_coo_tile(nnz, accumulate, row, col, val, x, y, skip, st);
-    const int64_t warps = ceil_div(nnz, kCooPerWarp);
-    const int64_t blocks = ceil_div(warps * 32, kSpmvThreads);
-    coo_kernel<<<(unsigned)blocks, kSpmvThreads, 0, st>>>(nnz, accumulate, row, col, val, x, y, skip);
-    WK_LAUNCH_CHECK();
-    return 0;
+    return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st,
+                       HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
+                       gplan ? gather_plan_view(gplan) : GatherPlan{nullptr, nullptr, nullptr});
 }
 
 }  // namespace wk
@@ -811,11 +487,13 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
                 csr_plan_views(A->plan, A->nnz, &first, &partials, &tickets);
             return launch_csr(A->nrows, A->ncols, A->nnz, A->row_ptrs, A->col_idx, A->values, x, y,
                               A->csr_strategy, A->subwarp_size, first, partials, tickets, skip, st,
-                              (A->csr_strategy == WK_CSR_MERGE || A->csr_strategy == WK_CSR_LOAD_BALANCE) ? A->plan : nullptr);
+                              (A->csr_strategy == WK_CSR_MERGE || A->csr_strategy == WK_CSR_LOAD_BALANCE) ? A->plan : nullptr,
+                              A->gather_plan);
         }
         case WK_FMT_COO:
             WK_REQUIRE(skip == nullptr, WK_ERR_INVALID, "masked COO SpMV is not supported");
-            return launch_coo(A->nrows, A->nnz, A->row_idx, A->col_idx, A->values, x, y, 0, nullptr, st);
+            return launch_coo(A->nrows, A->nnz, A->row_idx, A->col_idx, A->values, x, y, 0, nullptr, st,
+                              A->gather_plan);
         case WK_FMT_ELL:
             return launch_ell(A->nrows, A->ncols, A->width, A->stride, A->col_idx, A->values, A->row_lengths, x,
                               y, skip, st);
@@ -828,7 +506,7 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
             if (rc) return rc;
             if (A->coo_nnz == 0) return 0;
             return launch_coo(A->nrows, A->coo_nnz, A->coo_row, A->coo_col, A->coo_val, x, y, /*accumulate=*/1,
-                              skip, st);
+                              skip, st, A->gather_plan);
         }
         default:
             WK_REQUIRE(false, WK_ERR_INVALID, "unknown matrix format %d", A->format);

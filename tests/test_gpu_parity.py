@@ -104,46 +104,31 @@ def test_csr_subwarp_golden(wk, case):
             assert sparse_ref.max_scaled_rel_err(y, case.y, nnz) <= TOL, tile
 
 
-COO_KERNELS = (0, 1, 2, 3)  # spmv.cu coo_kernel_choice: warp range, pipelined warp range, TMA tiles, seg8 (default)
+GATHER = ("off", "on")  # hot-column gather plan (hotcols.cu); "on" caches every column with >= 1 entry
 
 
-@pytest.fixture
-def coo_kernel(wk, request):
-    from paper_2006_14290_b200 import _lib
-
-    _lib.call("wk_config_set", b"coo_kernel", request.param)
-    yield request.param
-    _lib.call("wk_config_set", b"coo_kernel", 3)
+def _gather_ex(wk, gather):
+    return wk.make_executor("b200", device=0, tuning={"gather_plan": gather, "gather_min_count": 1})
 
 
-@pytest.mark.parametrize("coo_kernel", COO_KERNELS, indirect=True)
+@pytest.mark.parametrize("gather", GATHER)
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
-def test_coo_golden(wk, ex, case, coo_kernel):
-    y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, ex)
+def test_coo_golden(wk, case, gather):
+    y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, _gather_ex(wk, gather))
     if _is_int(case):
         assert np.array_equal(y, case.y)
     else:
         assert sparse_ref.max_scaled_rel_err(y, case.y, sparse_ref.row_nnz(case.csr)) <= TOL
 
 
-@pytest.fixture
-def seg8_kernel(wk, request):
-    from paper_2006_14290_b200 import _lib
-
-    _lib.call("wk_config_set", b"seg8_kernel", request.param)
-    yield request.param
-    _lib.call("wk_config_set", b"seg8_kernel", 0)
-
-
-@pytest.mark.parametrize("seg8_kernel", [0, 1], indirect=True)
-@pytest.mark.parametrize("coo_kernel", COO_KERNELS, indirect=True)
+@pytest.mark.parametrize("gather", GATHER)
 @pytest.mark.parametrize("shape", ["skewed", "many_tiles", "one_row", "multi_range"])
-def test_coo_hybrid_skewed(wk, ex, rng, shape, coo_kernel, seg8_kernel):
-    """COO and Hybrid (ELL + COO accumulate) on skewed / multi-tile inputs;
-    multi_range: more 2048-entry warp ranges than warps in the persistent
-    TMA grid (ring reuse across ranges), nnz not a multiple of 4."""
-    if seg8_kernel == 1 and coo_kernel != 3:
-        pytest.skip("seg8_kernel only selects the data path of coo_kernel 3")
+def test_coo_hybrid_skewed(wk, rng, shape, gather):
+    """COO and Hybrid (ELL + COO accumulate) on skewed / multi-range inputs
+    (more 2048-entry warp ranges than warps in the persistent hot-column
+    grid, nnz not a multiple of 4), with and without the gather plan; the
+    plan's results are bitwise those of the plain kernel."""
+    ex = _gather_ex(wk, gather)
     ncols = 70000
     if shape == "one_row":
         lens = np.array([0, 60000, 0, 3])
@@ -160,9 +145,39 @@ def test_coo_hybrid_skewed(wk, ex, rng, shape, coo_kernel, seg8_kernel):
     x = rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
     coo = wk.csr_to_coo(csr, ex)
-    assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
+    y = wk.spmv_coo(coo, x, ex)
+    assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
+    y_plain = wk.spmv_coo(coo, x, _gather_ex(wk, "off"))
     hyb = wk.csr_to_hybrid(csr, width=3, exec=ex)
     assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
+    if gather == "on":
+        # same folds, x read from shared memory for the cached columns:
+        # only the atomics at range boundaries may order differently
+        assert sparse_ref.max_scaled_rel_err(y, y_plain, lens) <= TOL
+
+
+def test_gather_plan_contents(wk):
+    """The plan caches the most frequent columns (count >= threshold, at most
+    8192, column order) and rewrites exactly their entries as ~slot."""
+    import torch
+
+    from paper_2006_14290_b200 import device as D
+
+    rng = np.random.default_rng(5)
+    ncols = 50000
+    cols = np.concatenate([rng.integers(0, ncols, 300000), np.repeat(np.arange(0, 20000, 2), 40)])
+    col_t = torch.as_tensor(cols.astype(np.int32), device="cuda")
+    g = D.build_gather_plan(col_t, len(cols), ncols, col_t.device, min_count=20)
+    counts = np.bincount(cols, minlength=ncols)
+    hot_ref = np.flatnonzero(counts >= g.threshold)
+    assert len(hot_ref) <= 8192 and np.sum(counts >= g.threshold - 1) > 8192  # smallest admissible threshold
+    assert g.nhot == len(hot_ref) and g.covered == int(counts[hot_ref].sum())
+    buf = g.buf.view(torch.int32).cpu().numpy()
+    assert np.array_equal(buf[4:4 + g.nhot], hot_ref)
+    slot = np.full(ncols, -1)
+    slot[hot_ref] = np.arange(len(hot_ref))
+    col2 = buf[4 + 8192:4 + 8192 + len(cols)]
+    assert np.array_equal(col2, np.where(slot[cols] >= 0, ~slot[cols], cols))
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -180,22 +195,9 @@ def test_conversions_golden_bitwise(wk, ex, case):
         assert got.values.tobytes() == ref.values.tobytes(), s
 
 
-@pytest.fixture
-def ell_kernel(wk, request):
-    from paper_2006_14290_b200 import _lib
-
-    _lib.call("wk_config_set", b"ell_kernel", request.param)
-    yield request.param
-    _lib.call("wk_config_set", b"ell_kernel", 2)
-
-
-ELL_KERNELS = (0, 1, 2, 3, 4)  # register, SELL-P warp pipeline, ell_tma_kernel configs (2 = default)
-
-
-@pytest.mark.parametrize("ell_kernel", ELL_KERNELS, indirect=True)
 @pytest.mark.parametrize("nrows,stride", [(1000, 1000), (4096, 4096), (4100, 4100), (130, 132), (999, 1004),
                                           (1001, 1001), (2000, 2050)])
-def test_ell_strides_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
+def test_ell_strides_bitwise(wk, ex, rng, nrows, stride):
     """ELL through the TMA pipeline (stride % 4 == 0, partial last 64-row
     block) and the register kernel (other strides): bitwise vs the oracle,
     also with non-finite x[0] (padding must then be skipped via row_lengths)."""
@@ -215,9 +217,8 @@ def test_ell_strides_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
         assert wk.spmv_ell(ell, x, ex).tobytes() == y_ref.tobytes()
 
 
-@pytest.mark.parametrize("ell_kernel", ELL_KERNELS, indirect=True)
 @pytest.mark.parametrize("nrows,stride", [(400003, 400004), (400000, 400000)])
-def test_ell_many_tiles_bitwise(wk, ex, rng, nrows, stride, ell_kernel):
+def test_ell_many_tiles_bitwise(wk, ex, rng, nrows, stride):
     """More 512-row tiles than CTAs in the persistent grid (every ring stage
     reused across tiles), a partial last tile, a width that is not a multiple
     of the stage's column count; bitwise vs the oracle."""
@@ -272,19 +273,9 @@ def test_from_entries_duplicates(wk):
     assert m.values.tobytes() == ez.coo.values.tobytes()
 
 
-@pytest.fixture
-def fill_kernel(wk, request):
-    from paper_2006_14290_b200 import _lib
-
-    _lib.call("wk_config_set", b"fill_kernel", request.param)
-    yield request.param
-    _lib.call("wk_config_set", b"fill_kernel", 1)
-
-
-@pytest.mark.parametrize("fill_kernel", [0, 1], indirect=True)
 @pytest.mark.parametrize("ss", [1, 4, 32, 64, 256, 512])
-def test_sellp_fill_kernels_bitwise(wk, ex, rng, ss, fill_kernel):
-    """CSR -> SELL-P fill, staged scatter and TMA ring: many slices per CTA of
+def test_sellp_fill_kernels_bitwise(wk, ex, rng, ss):
+    """CSR -> SELL-P fill (TMA ring for 4 <= ss <= 256, staged scatter otherwise): many slices per CTA of
     the persistent grid, slices too wide for a stage (a 5000-entry row, direct
     path), empty slices, a last slice whose 16-byte-widened range would pass
     nnz; every array bitwise vs the oracle (sparse.py:219-242)."""
@@ -412,15 +403,18 @@ def _banded_case(rng, lens, ncols):
     return ptrs, cols.astype(np.int64), rng.standard_normal(int(ptrs[-1]))
 
 
-@pytest.mark.parametrize("seg8_kernel", [0, 1], indirect=True)
+@pytest.mark.parametrize("gather", GATHER)
 @pytest.mark.parametrize("strategy", ["merge", "load_balance"])
 @pytest.mark.parametrize("shape", ["tile_spanning_row", "empty_runs", "tile_aligned", "all_empty", "one_row",
                                    "skewed", "ints", "many_tiles", "multi_range"])
-def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
+def test_csr_balanced_edge_cases(wk, rng, shape, strategy, gather):
     """merge-path and load-balance CSR: rows spanning many tiles / warp
     ranges, long runs of empty rows crossing them, rows ending exactly on tile /
     thread boundaries, empty matrices; tolerance 1e-12, exact on integer data;
-    both are deterministic."""
+    both are deterministic; load_balance with and without the hot-column
+    gather plan (bitwise equal: same folds, same carries)."""
+    if strategy == "merge" and gather == "on":
+        pytest.skip("the gather plan applies to load_balance (and COO) only")
     ncols = 70000
     if shape == "tile_spanning_row":
         lens = np.array([3, 50000, 2, 0, 7000, 1] + [5] * 900)
@@ -456,8 +450,13 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
     csr = wk.CsrMatrix(len(lens), ncols, ptrs, cols, vals)
     x = rng.integers(-5, 6, size=ncols).astype(np.float64) if shape == "ints" else rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
-    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
+    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy, "gather_plan": gather,
+                                                   "gather_min_count": 1})
     y = wk.spmv_csr(csr, x, e)
+    if gather == "on":
+        e_off = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy, "gather_plan": "off"})
+        assert wk.spmv_csr(csr, x, e_off).tobytes() == y.tobytes()
+        wk.spmv_csr(csr, x, e)  # back to the plan for the masked call below
     assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
     if shape == "ints":
         assert np.array_equal(y, y_ref)
@@ -472,6 +471,8 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, seg8_kernel):
     from paper_2006_14290_b200 import _lib
 
     d = D.as_device(csr, 0).with_strategy(strategy)
+    if gather == "on":
+        assert d.gather_plan() is not None
     xt = torch.as_tensor(x, device="cuda")
     yt = torch.full((csr.nrows,), 7.0, dtype=torch.float64, device="cuda")
     flag = torch.ones(1, dtype=torch.int32, device="cuda")

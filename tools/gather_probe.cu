@@ -213,6 +213,11 @@ int run_hot(int64_t n, int64_t nnz, const int* row, const int* col, const double
     return 0;
 }
 
+__global__ void fold_cols(int64_t nnz, int* col, int mask) {
+    int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e < nnz) col[e] &= mask;
+}
+
 int main() {
     const int scale = 24;
     const int64_t n = int64_t(1) << scale, m = n * 16;
@@ -278,9 +283,13 @@ int main() {
                 printf("top %d columns: %.4f of entries\n", k + 1, double(s) / nnz);
         }
         run_hot<8192>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
-        run_hot<16384>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
-        run_hot<24576>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
-        run_hot<27000>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+        run_hot<4096>(n, nnz, row, col, val, x, out, sms, ids, slot, col2, hx, "");
+    }
+    // sensitivity to the x footprint: fold the column ids into n/2, n/4, n/8
+    for (int sh = 1; sh <= 3; ++sh) {
+        fold_cols<<<(nnz + 255) / 256, 256>>>(nnz, col, int((n >> sh) - 1));
+        printf("x footprint %lld MB:\n", (long long)((n >> sh) * 8 >> 20));
+        R(0, 1, 4) R(0, 1, 8)
     }
     return 0;
 }
