@@ -104,17 +104,6 @@ int64_t wk_csr_load_balance_plan_bytes(int64_t nrows, int64_t nnz);
 int wk_csr_load_balance_plan_build(int64_t nrows, int64_t nnz, const int32_t* row_ptrs, void* plan,
                                    wk_stream_t stream);
 
-/* Hot-column gather plan for COO / CSR load_balance (wk_matrix.gather_plan):
- * the columns with the most entries (at most 8192, each with >= min_count
- * entries; min_count <= 0: 2 x SM count) are cached in shared memory by the
- * SpMV; the plan holds their ids and a rewritten column array. Results are
- * bitwise those of the plan-less kernels. plan: wk_gather_plan_bytes(nnz),
- * scratch: wk_gather_plan_scratch_bytes(ncols), both 16-byte aligned. Plan
- * header (device): int32 nhot, int32 threshold, int64 entries covered. */
-int64_t wk_gather_plan_bytes(int64_t nnz);
-int64_t wk_gather_plan_scratch_bytes(int64_t ncols);
-int wk_gather_plan_build(int64_t ncols, int64_t nnz, const int32_t* col_idx, int64_t min_count, void* plan,
-                         void* scratch, wk_stream_t stream);
 
 /* replaces spmv_coo (kernels.py:409-410 -> 209-264); coo_spmv fixture
  * (coo_kernels.cu:34-35). Entries sorted row-major. accumulate = 0 zero-fills y. */
@@ -148,8 +137,6 @@ typedef struct wk_matrix {
     const int32_t* coo_col;
     const double* coo_val;
     void* plan;               /* CSR stream / merge / load_balance plan */
-    const void* gather_plan;  /* COO, CSR load_balance, HYBRID (coo part): hot-column
-                                 gather plan (wk_gather_plan_build) or NULL */
 } wk_matrix;
 
 int wk_spmv(const wk_matrix* A, const double* x, double* y, wk_stream_t stream);

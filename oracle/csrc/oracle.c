@@ -6,9 +6,10 @@
  * (warpkit/kernels.py:283-331) in C so the CPU baseline can use every host
  * core. Built with -ffp-contract=off: each product and each sum is rounded
  * separately, so every row result is bitwise identical to the reference no
- * matter how rows are split across OpenMP threads. Dot products use an
- * OpenMP reduction (summation order depends on the thread count, exactly as
- * the reference's OpenBLAS ddot does, see SURVEY.md §7 "Solver parity").
+ * matter how rows are split across OpenMP threads. Dot products sum
+ * per-thread blocks in thread order (the order depends on the thread count,
+ * as the reference's OpenBLAS ddot does, see SURVEY.md §7 "Solver parity",
+ * but not on thread timing).
  *
  * Index layout follows the device formats: int32 column indices, int64
  * row pointers / slice sets.
@@ -101,11 +102,34 @@ void or_spmv_coo(int64_t nrows, int64_t nnz, const int32_t* row, const int32_t* 
     }
 }
 
+/* Deterministic for a given thread count: thread t sums the contiguous block
+ * [n t / T, n (t + 1) / T) in index order and the T partials are added in
+ * thread order (an OpenMP `reduction(+)` combines them in arrival order, so
+ * repeated runs of a chaotic solver -- BiCGSTAB on a nonsymmetric operator --
+ * could take different iteration counts). */
+#define OR_MAX_THREADS 1024
 double or_dot(int64_t n, const double* a, const double* b, int nthreads) {
     set_threads(nthreads);
+    double part[OR_MAX_THREADS];
+    int used = 1;
+#pragma omp parallel
+    {
+        int nt = 1, t = 0;
+#ifdef _OPENMP
+        nt = omp_get_num_threads();
+        t = omp_get_thread_num();
+#endif
+        if (nt > OR_MAX_THREADS) nt = OR_MAX_THREADS;
+        if (t < nt) {
+            const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+            double s = 0.0;
+            for (int64_t i = lo; i < hi; ++i) s += a[i] * b[i];
+            part[t] = s;
+        }
+        if (t == 0) used = nt;
+    }
     double s = 0.0;
-#pragma omp parallel for reduction(+ : s) schedule(static)
-    for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+    for (int t = 0; t < used; ++t) s += part[t];
     return s;
 }
 

@@ -66,7 +66,7 @@ class WkMatrix(ctypes.Structure):
         ("slice_size", I64), ("slice_sets", P),
         ("width", I64), ("stride", I64), ("row_lengths", P),
         ("coo_nnz", I64), ("coo_row", P), ("coo_col", P), ("coo_val", P),
-        ("plan", P), ("gather_plan", P),
+        ("plan", P),
     ]
 
 
@@ -142,9 +142,6 @@ _SIGS = {
     "wk_ell_zero_padding": (ctypes.c_int, [I64, I64, I64, P, P, P, P]),
     "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P, I64, P]),
     "wk_hybrid_coo_fill_workspace": (ctypes.c_int64, [I64]),
-    "wk_gather_plan_bytes": (ctypes.c_int64, [I64]),
-    "wk_gather_plan_scratch_bytes": (ctypes.c_int64, [I64]),
-    "wk_gather_plan_build": (ctypes.c_int, [I64, I64, P, I64, P, P, P]),
     "wk_coo_to_csr_ptrs": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_csr_to_coo_rows": (ctypes.c_int, [I64, P, P, P]),
     "wk_scan_workspace_bytes": (I64, [I64]),

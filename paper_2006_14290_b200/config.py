@@ -16,7 +16,6 @@ MAX_TUNING_VALUE = 1024
 REQUIRED_TUNING_KEYS = ("block_size", "subwarps_per_block", "csr_subwarp_size")
 CSR_STRATEGIES = ("auto", "stream", "rowblock", "subwarp", "merge", "load_balance")
 HYBRID_STRATEGIES = ("minimal_storage", "imbalance_limit")
-GATHER_POLICIES = ("auto", "on", "off")
 
 
 def is_power_of_two(n) -> bool:
@@ -35,11 +34,6 @@ DEFAULT_TUNING = {
     "sellp_slice_size": 64,
     "hybrid_strategy": "minimal_storage",
     "hybrid_percent": 0.8,
-    # hot-column gather plan of COO / CSR load_balance / Hybrid-COO (device.py
-    # GATHER_PLAN_*): auto = large power-law operands only; gather_min_count:
-    # entries a column needs to be cached (<= 0: 2 x SM count)
-    "gather_plan": "auto",
-    "gather_min_count": 0,
 }
 
 
@@ -68,10 +62,6 @@ class B200Config:
             raise ValueError(f"tuning['csr_strategy'] must be one of {CSR_STRATEGIES}")
         if t["hybrid_strategy"] not in HYBRID_STRATEGIES:
             raise ValueError(f"tuning['hybrid_strategy'] must be one of {HYBRID_STRATEGIES}")
-        if t["gather_plan"] not in GATHER_POLICIES:
-            raise ValueError(f"tuning['gather_plan'] must be one of {GATHER_POLICIES}")
-        if not isinstance(t["gather_min_count"], int):
-            raise ValueError("tuning['gather_min_count'] must be an int")
         if not (0.0 < float(t["hybrid_percent"]) <= 1.0):
             raise ValueError("tuning['hybrid_percent'] must be in (0, 1]")
         object.__setattr__(self, "tuning", MappingProxyType(t))

@@ -8,7 +8,6 @@
 
 #include "common.cuh"
 #include "reduce.cuh"
-#include "hotcols.cuh"
 
 namespace wk {
 
@@ -33,17 +32,13 @@ namespace wk {
 // measured 2x slower (the kernel is bound by the random x gathers, not by the
 // matrix stream) and removed.
 //
-// Hot-column gathers (gather plan, hotcols.cu): on power-law matrices a few
-// thousand columns take a fifth of all entries (R-MAT scale 24: the top 8192
-// columns hold 20.8% of the 263M entries). The plan rewrites the column array
-// once per matrix, col2[k] = ~slot for a cached column, and seg8_hot_kernel
-// (persistent, one 1024-thread CTA per SM) first gathers x of the K cached
-// columns into shared memory, so those entries read shared memory instead of
-// issuing a random L2 sector request each: the R-MAT kernels are bound by the
-// rate of random L2 requests (tools/gather_probe.cu: a bare stream + gather
-// fold of the same matrix takes 1.19 ms, 221 G gathers/s; with the cache
-// 1.04 ms). K = 8192 (64 KB): larger caches shrink the L1 that holds the
-// in-flight gather lines and lose (16384: 1.09 ms, 24576: 1.71 ms).
+// The kernel is bound by the L1TEX data pipe, not by DRAM: every random x
+// gather is one wavefront (R-MAT rows share no x lines between lanes), and a
+// bare stream + gather fold of the same matrix (tools/gather_probe.cu) takes
+// 1.19 ms, 1.03 ms with x shrunk to 16 MB (all L2 hits) — the seg8 kernel runs
+// at 0.95-1.0 of that fold. A shared-memory cache of the 8192 hottest columns'
+// x (20.8% of R-MAT's entries) did not pay in the real kernel (the L1 already
+// serves those gathers: 28% L1 sector hit rate; profiles/r02) and was removed.
 // ---------------------------------------------------------------------------
 constexpr int kS8Win = 256;                  // entries per window (8 per lane)
 constexpr int kS8PerWarp = 8 * kS8Win;       // entries per warp range
@@ -292,13 +287,12 @@ __device__ __forceinline__ void seg8_fold(int lane, int nv, bool last_window, co
 }
 
 
-// One warp range [wlo, whi) of seg8. kHot: columns come from the gather
-// plan's col2 and cached columns read `hx` (shared memory).
-template <bool kCsr, bool kHot>
+// One warp range [wlo, whi) of seg8.
+template <bool kCsr>
 __device__ __forceinline__ void seg8_range(int lane, int64_t g, int64_t nnz, int accumulate, bool vec,
                                            const int* __restrict__ rows, const int* __restrict__ col,
                                            const double* __restrict__ val, const double* __restrict__ x,
-                                           const double* hx, double* __restrict__ y, const HeadPlan& hp) {
+                                           double* __restrict__ y, const HeadPlan& hp) {
     const int64_t wlo = g * kS8PerWarp;
     const int64_t whi = (wlo + kS8PerWarp < nnz) ? wlo + kS8PerWarp : nnz;
     int first_row, last_row;
@@ -365,21 +359,8 @@ __device__ __forceinline__ void seg8_range(int lane, int64_t g, int64_t nnz, int
                     if (!kCsr) rw[u] = u < nv ? ld_stream(rows + kb + u) : -1;
                 }
             }
-            if (kHot) {
-                // all global gathers first (8 in flight per lane), then the
-                // shared-memory reads of the cached columns
-                double g[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) g[u] = c[u] >= 0 ? ld_x(x, c[u]) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (c[u] < 0) g[u] = hx[~c[u]];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], g[u]) : 0.0;
-            } else {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
-            }
+            for (int u = 0; u < 8; ++u) pv[u] = u < nv ? __dmul_rn(v[u], ld_x(x, c[u])) : 0.0;
         }
         seg8_fold(lane, nv, E + kS8Win >= whi, pv, rw, carry_row, carry, emit);
     }
@@ -395,30 +376,7 @@ seg8_kernel(int64_t nnz, int accumulate, int vec, const int* __restrict__ rows, 
     const int lane = threadIdx.x & 31;
     const int64_t warp = int64_t(blockIdx.x) * kS8Warps + (threadIdx.x >> 5);
     if (warp * kS8PerWarp >= nnz) return;
-    seg8_range<kCsr, false>(lane, warp, nnz, accumulate, vec != 0, rows, col, val, x, nullptr, y, hp);
-}
-
-// persistent, hot columns of x cached in shared memory (one CTA per SM; the
-// CSR variant keeps 24 warps: its row-id expansion needs ~80 registers)
-template <bool kCsr>
-__host__ __device__ constexpr int hot_threads() { return kCsr ? 768 : kHotThreads; }
-
-template <bool kCsr>
-__global__ void __launch_bounds__(hot_threads<kCsr>(), 1)
-seg8_hot_kernel(int64_t nnz, int accumulate, int vec, const int* __restrict__ rows, const double* __restrict__ val,
-                const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip, HeadPlan hp,
-                GatherPlan gp) {
-    if (skip != nullptr && *skip) return;
-    extern __shared__ double hx[];
-    const int nh = *gp.nhot;
-    constexpr int T = hot_threads<kCsr>();
-    for (int i = threadIdx.x; i < nh; i += T) hx[i] = ld_x(x, __ldg(gp.hot + i));
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t nranges = (nnz + kS8PerWarp - 1) / kS8PerWarp;
-    const int64_t nwarps = int64_t(gridDim.x) * (T / 32);
-    for (int64_t g = int64_t(blockIdx.x) * (T / 32) + (threadIdx.x >> 5); g < nranges; g += nwarps)
-        seg8_range<kCsr, true>(lane, g, nnz, accumulate, vec != 0, rows, gp.col2, val, x, hx, y, hp);
+    seg8_range<kCsr>(lane, warp, nnz, accumulate, vec != 0, rows, col, val, x, y, hp);
 }
 
 // rows cut by warp-range boundaries (CSR): the first range of each run of
@@ -438,42 +396,17 @@ __global__ void seg8_fixup_kernel(int64_t nranges, const int* __restrict__ crow,
 
 
 // rows: COO row indices (csr = false) or unused (csr = true, row ids from hp).
-// gp.col2 != nullptr: the hot-column kernel (gather plan).
 inline int launch_seg8(bool csr, int64_t nnz, int accumulate, const int* rows, const int* col, const double* val,
                        const double* x, double* y, const int* skip, cudaStream_t st,
-                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
-                       GatherPlan gp = GatherPlan{nullptr, nullptr, nullptr}) {
+                       HeadPlan hp = HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr}) {
     if (nnz == 0) return 0;
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    const int vec = al(gp.col2 != nullptr ? gp.col2 : col) && al(val) && (csr || al(rows));
-    if (gp.col2 != nullptr) {
-        static bool attr_set[64] = {false};
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!attr_set[dev & 63]) {
-            WK_CUDA(cudaFuncSetAttribute(seg8_hot_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kHotMax * 8));
-            WK_CUDA(cudaFuncSetAttribute(seg8_hot_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kHotMax * 8));
-            attr_set[dev & 63] = true;
-        }
-        const int T = csr ? hot_threads<true>() : hot_threads<false>();
-        int64_t grid = sm_count();
-        const int64_t need = ceil_div(seg8_warps(nnz), T / 32);
-        if (grid > need) grid = need;
-        if (csr)
-            seg8_hot_kernel<true><<<(unsigned)grid, T, kHotMax * 8, st>>>(nnz, accumulate, vec, rows, val, x, y, skip,
-                                                                         hp, gp);
-        else
-            seg8_hot_kernel<false><<<(unsigned)grid, T, kHotMax * 8, st>>>(nnz, accumulate, vec, rows, val, x, y,
-                                                                          skip, hp, gp);
-    } else {
-        const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
-        if (csr)
-            seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
-        else
-            seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
-    }
+    const int vec = al(col) && al(val) && (csr || al(rows));  // 16/32-byte vector loads
+    const unsigned blocks = (unsigned)ceil_div(seg8_warps(nnz), kS8Warps);
+    if (csr)
+        seg8_kernel<true><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
+    else
+        seg8_kernel<false><<<blocks, kS8Warps * 32, 0, st>>>(nnz, accumulate, vec, rows, col, val, x, y, skip, hp);
     WK_LAUNCH_CHECK();
     if (!csr) return 0;
     const int64_t nranges = seg8_warps(nnz);

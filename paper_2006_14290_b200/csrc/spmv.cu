@@ -282,8 +282,7 @@ static int launch_zero_masked(double* y, int64_t n, const int* skip, cudaStream_
 
 int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const int* col, const double* val,
                const double* x, double* y, int strategy, int subwarp, const int* first, double* partials,
-               unsigned* tickets, const int* skip, cudaStream_t st, void* merge_plan = nullptr,
-               const void* gplan = nullptr) {
+               unsigned* tickets, const int* skip, cudaStream_t st, void* merge_plan = nullptr) {
     (void)ncols;
     if (nrows == 0) return 0;
     if (strategy == WK_CSR_MERGE) {
@@ -305,8 +304,7 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
                    "csr load_balance needs 16-byte aligned col_idx / values");
         const HeadPlanMut h = head_plan_views(merge_plan, nrows, nnz);
         return launch_seg8(true, nnz, 0, nullptr, col, val, x, y, skip, st,
-                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow},
-                           gplan ? gather_plan_view(gplan) : GatherPlan{nullptr, nullptr, nullptr});
+                           HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow});
     }
     if (strategy == WK_CSR_ROWBLOCK) {
         // 32*k-row blocks; the stage capacity is the smallest that keeps a
@@ -349,10 +347,9 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
 
 // COO (kernels.py:209-264 semantics): seg8 warp ranges of 2048 sorted
 // entries, warp segmented scans, atomics for the two rows a range can share
-// with its neighbours (segwarp.cuh). `gplan`: hot-column gather plan
-// (hotcols.cu) or nullptr.
+// with its neighbours (segwarp.cuh).
 int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const double* val, const double* x,
-               double* y, int accumulate, const int* skip, cudaStream_t st, const void* gplan = nullptr) {
+               double* y, int accumulate, const int* skip, cudaStream_t st) {
     if (nrows == 0) return 0;
     if (!accumulate) {
         // skip-aware zero fill is not needed: a skipped SpMV leaves y untouched
@@ -361,9 +358,7 @@ int launch_coo(int64_t nrows, int64_t nnz, const int* row, const int* col, const
         WK_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * size_t(nrows), st));
     }
     if (nnz == 0) return 0;
-    return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st,
-                       HeadPlan{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr},
-                       gplan ? gather_plan_view(gplan) : GatherPlan{nullptr, nullptr, nullptr});
+    return launch_seg8(false, nnz, accumulate, row, col, val, x, y, skip, st);
 }
 
 }  // namespace wk
@@ -487,13 +482,11 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
                 csr_plan_views(A->plan, A->nnz, &first, &partials, &tickets);
             return launch_csr(A->nrows, A->ncols, A->nnz, A->row_ptrs, A->col_idx, A->values, x, y,
                               A->csr_strategy, A->subwarp_size, first, partials, tickets, skip, st,
-                              (A->csr_strategy == WK_CSR_MERGE || A->csr_strategy == WK_CSR_LOAD_BALANCE) ? A->plan : nullptr,
-                              A->gather_plan);
+                              (A->csr_strategy == WK_CSR_MERGE || A->csr_strategy == WK_CSR_LOAD_BALANCE) ? A->plan : nullptr);
         }
         case WK_FMT_COO:
             WK_REQUIRE(skip == nullptr, WK_ERR_INVALID, "masked COO SpMV is not supported");
-            return launch_coo(A->nrows, A->nnz, A->row_idx, A->col_idx, A->values, x, y, 0, nullptr, st,
-                              A->gather_plan);
+            return launch_coo(A->nrows, A->nnz, A->row_idx, A->col_idx, A->values, x, y, 0, nullptr, st);
         case WK_FMT_ELL:
             return launch_ell(A->nrows, A->ncols, A->width, A->stride, A->col_idx, A->values, A->row_lengths, x,
                               y, skip, st);
@@ -506,7 +499,7 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
             if (rc) return rc;
             if (A->coo_nnz == 0) return 0;
             return launch_coo(A->nrows, A->coo_nnz, A->coo_row, A->coo_col, A->coo_val, x, y, /*accumulate=*/1,
-                              skip, st, A->gather_plan);
+                              skip, st);
         }
         default:
             WK_REQUIRE(false, WK_ERR_INVALID, "unknown matrix format %d", A->format);

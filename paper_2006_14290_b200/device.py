@@ -94,72 +94,6 @@ def workspace(device=None):
     return _Workspace.get(device)
 
 
-# ---- hot-column gather plan (hotcols.cu) ----------------------------------------
-
-# The plan is built automatically for COO / CSR load_balance / Hybrid-COO
-# operands with at least this many entries, and kept when its cached columns
-# hold at least GATHER_PLAN_MIN_COVER of the entries (power-law matrices:
-# R-MAT scale 24 -> 20.8%; a stencil -> no column qualifies, no plan).
-GATHER_PLAN_MIN_NNZ = 1 << 22
-GATHER_PLAN_MIN_COVER = 0.05
-
-
-class GatherPlan:
-    """Device plan of the hot-column gathers: `buf` (header | hot ids | col2),
-    `nhot` cached columns holding `covered` entries, count threshold."""
-
-    def __init__(self, buf, nhot, threshold, covered):
-        self.buf, self.nhot, self.threshold, self.covered = buf, nhot, threshold, covered
-
-
-def build_gather_plan(col_idx, nnz, ncols, device, min_count=0) -> GatherPlan:
-    """wk_gather_plan_build + one D2H read of the 16-byte header."""
-    L = _lib.load()
-    buf = torch.empty((int(L.wk_gather_plan_bytes(nnz)) + 15) // 16 * 2, dtype=torch.int64, device=device)
-    scratch = torch.empty((int(L.wk_gather_plan_scratch_bytes(ncols)) + 15) // 16 * 2, dtype=torch.int64,
-                          device=device)
-    _lib.call("wk_gather_plan_build", int(ncols), int(nnz), _ptr(col_idx), int(min_count), _ptr(buf), _ptr(scratch),
-              stream_handle(device))
-    head = buf[:2].cpu()
-    del scratch
-    nhot = int(head[0].item() & 0xFFFFFFFF)
-    threshold = int(head[0].item() >> 32)
-    return GatherPlan(buf, nhot, threshold, int(head[1].item()))
-
-
-class _GatherPlanMixin:
-    """Lazy gather plan over (self.col_idx, self.nnz, self.ncols)."""
-
-    _gplan = None        # GatherPlan, or False once decided against
-    gather_policy = "auto"  # "auto" | "on" | "off"
-
-    def set_gather_plan(self, policy="auto", min_count=0):
-        """'on': build with `min_count` (<= 0: 2 x SM count) and always use it
-        (tests / A-B); 'off': never; 'auto': see GATHER_PLAN_MIN_*."""
-        if policy not in ("auto", "on", "off"):
-            raise ValueError(f"gather plan policy must be auto/on/off, got {policy!r}")
-        self.gather_policy = policy
-        self._gplan = None
-        self._gplan_min_count = int(min_count)
-        self._wk = None
-        return self
-
-    def gather_plan(self):
-        if self._gplan is None:
-            self._gplan = False
-            pol = self.gather_policy
-            if pol == "on" or (pol == "auto" and self.nnz >= GATHER_PLAN_MIN_NNZ):
-                g = build_gather_plan(self.col_idx, self.nnz, self.ncols, self.device,
-                                      getattr(self, "_gplan_min_count", 0))
-                if pol == "on" or (g.nhot > 0 and g.covered >= GATHER_PLAN_MIN_COVER * self.nnz):
-                    self._gplan = g
-        return self._gplan or None
-
-    def _gather_ptr(self):
-        g = self.gather_plan()
-        return _ptr(g.buf) if g is not None else ctypes.c_void_p(0)
-
-
 # ---- device matrices -------------------------------------------------------------
 
 
@@ -182,7 +116,7 @@ class DeviceMatrix:
         return (self.nrows, self.ncols)
 
 
-class DeviceCsr(DeviceMatrix, _GatherPlanMixin):
+class DeviceCsr(DeviceMatrix):
     fmt = "csr"
 
     def __init__(self, nrows, ncols, row_ptrs, col_idx, values):
@@ -266,7 +200,6 @@ class DeviceCsr(DeviceMatrix, _GatherPlanMixin):
             m.plan = _ptr(self.merge_plan())
         elif self.strategy == _lib.WK_CSR_LOAD_BALANCE:
             m.plan = _ptr(self.load_balance_plan())
-            m.gather_plan = self._gather_ptr()
         return m
 
     def row_lengths(self):
@@ -284,7 +217,7 @@ class DeviceCsr(DeviceMatrix, _GatherPlanMixin):
         return CsrMatrix(self.nrows, self.ncols, _np64(self.row_ptrs), _np64(self.col_idx), self.values.cpu().numpy())
 
 
-class DeviceCoo(DeviceMatrix, _GatherPlanMixin):
+class DeviceCoo(DeviceMatrix):
     fmt = "coo"
 
     def __init__(self, nrows, ncols, row_idx, col_idx, values):
@@ -299,7 +232,6 @@ class DeviceCoo(DeviceMatrix, _GatherPlanMixin):
         m.format = _lib.WK_FMT_COO
         m.nrows, m.ncols, m.nnz = self.nrows, self.ncols, self.nnz
         m.row_idx, m.col_idx, m.values = _ptr(self.row_idx), _ptr(self.col_idx), _ptr(self.values)
-        m.gather_plan = self._gather_ptr()
         return m
 
     def algorithmic_bytes(self):
@@ -412,7 +344,6 @@ class DeviceHybrid(DeviceMatrix):
         m.nnz = self.ell.stored + self.coo.nnz
         m.coo_nnz = self.coo.nnz
         m.coo_row, m.coo_col, m.coo_val = _ptr(self.coo.row_idx), _ptr(self.coo.col_idx), _ptr(self.coo.values)
-        m.gather_plan = self.coo._gather_ptr() if self.coo.nnz else ctypes.c_void_p(0)
         return m
 
     def algorithmic_bytes(self):

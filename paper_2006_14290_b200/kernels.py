@@ -23,14 +23,9 @@ def _prepare(exec: Executor, m, fmt=None):
     d = D.as_device(m, exec.device)
     if fmt is not None and d.fmt != fmt:
         raise TypeError(f"expected a {fmt} matrix, got {d.fmt}")
-    t = exec.tuning
     if d.fmt == "csr":
+        t = exec.tuning
         d.with_strategy(t["csr_strategy"], t["csr_subwarp_size"])
-    g = d.coo if d.fmt == "hybrid" else d
-    if d.fmt in ("csr", "coo", "hybrid") and (g.gather_policy != t["gather_plan"] or
-                                               getattr(g, "_gplan_min_count", 0) != t["gather_min_count"]):
-        g.set_gather_plan(t["gather_plan"], t["gather_min_count"])
-        d._wk = None
     return d
 
 

@@ -104,31 +104,27 @@ def test_csr_subwarp_golden(wk, case):
             assert sparse_ref.max_scaled_rel_err(y, case.y, nnz) <= TOL, tile
 
 
-GATHER = ("off", "on")  # hot-column gather plan (hotcols.cu); "on" caches every column with >= 1 entry
-
-
-def _gather_ex(wk, gather):
-    return wk.make_executor("b200", device=0, tuning={"gather_plan": gather, "gather_min_count": 1})
-
-
-@pytest.mark.parametrize("gather", GATHER)
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
-def test_coo_golden(wk, case, gather):
-    y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, _gather_ex(wk, gather))
+def test_coo_golden(wk, ex, case):
+    y = wk.spmv_coo(_host(wk, case.coo, "coo"), case.x, ex)
     if _is_int(case):
         assert np.array_equal(y, case.y)
     else:
         assert sparse_ref.max_scaled_rel_err(y, case.y, sparse_ref.row_nnz(case.csr)) <= TOL
 
 
-@pytest.mark.parametrize("gather", GATHER)
+@pytest.mark.parametrize("aligned", [True, False])
 @pytest.mark.parametrize("shape", ["skewed", "many_tiles", "one_row", "multi_range"])
-def test_coo_hybrid_skewed(wk, rng, shape, gather):
+def test_coo_hybrid_skewed(wk, ex, rng, shape, aligned):
     """COO and Hybrid (ELL + COO accumulate) on skewed / multi-range inputs
-    (more 2048-entry warp ranges than warps in the persistent hot-column
-    grid, nnz not a multiple of 4), with and without the gather plan; the
-    plan's results are bitwise those of the plain kernel."""
-    ex = _gather_ex(wk, gather)
+    (nnz not a multiple of 4: a tail past the last vector boundary); the
+    unaligned case (device arrays offset by one element) takes the scalar-load
+    path of the same kernel."""
+    import torch
+
+    from paper_2006_14290_b200 import device as D
+    from paper_2006_14290_b200 import kernels as K
+
     ncols = 70000
     if shape == "one_row":
         lens = np.array([0, 60000, 0, 3])
@@ -145,39 +141,20 @@ def test_coo_hybrid_skewed(wk, rng, shape, gather):
     x = rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
     coo = wk.csr_to_coo(csr, ex)
-    y = wk.spmv_coo(coo, x, ex)
-    assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
-    y_plain = wk.spmv_coo(coo, x, _gather_ex(wk, "off"))
-    hyb = wk.csr_to_hybrid(csr, width=3, exec=ex)
-    assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
-    if gather == "on":
-        # same folds, x read from shared memory for the cached columns:
-        # only the atomics at range boundaries may order differently
-        assert sparse_ref.max_scaled_rel_err(y, y_plain, lens) <= TOL
+    if aligned:
+        assert sparse_ref.max_scaled_rel_err(wk.spmv_coo(coo, x, ex), y_ref, lens) <= TOL
+        hyb = wk.csr_to_hybrid(csr, width=3, exec=ex)
+        assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), y_ref, lens) <= TOL
+    else:
+        def off1(a, dt):
+            t = torch.empty(len(a) + 1, dtype=dt, device="cuda")
+            t[1:] = torch.as_tensor(np.asarray(a), dtype=dt, device="cuda")
+            return t[1:]
 
-
-def test_gather_plan_contents(wk):
-    """The plan caches the most frequent columns (count >= threshold, at most
-    8192, column order) and rewrites exactly their entries as ~slot."""
-    import torch
-
-    from paper_2006_14290_b200 import device as D
-
-    rng = np.random.default_rng(5)
-    ncols = 50000
-    cols = np.concatenate([rng.integers(0, ncols, 300000), np.repeat(np.arange(0, 20000, 2), 40)])
-    col_t = torch.as_tensor(cols.astype(np.int32), device="cuda")
-    g = D.build_gather_plan(col_t, len(cols), ncols, col_t.device, min_count=20)
-    counts = np.bincount(cols, minlength=ncols)
-    hot_ref = np.flatnonzero(counts >= g.threshold)
-    assert len(hot_ref) <= 8192 and np.sum(counts >= g.threshold - 1) > 8192  # smallest admissible threshold
-    assert g.nhot == len(hot_ref) and g.covered == int(counts[hot_ref].sum())
-    buf = g.buf.view(torch.int32).cpu().numpy()
-    assert np.array_equal(buf[4:4 + g.nhot], hot_ref)
-    slot = np.full(ncols, -1)
-    slot[hot_ref] = np.arange(len(hot_ref))
-    col2 = buf[4 + 8192:4 + 8192 + len(cols)]
-    assert np.array_equal(col2, np.where(slot[cols] >= 0, ~slot[cols], cols))
+        d = D.DeviceCoo(coo.nrows, coo.ncols, off1(coo.row_idx, torch.int32), off1(coo.col_idx, torch.int32),
+                        off1(coo.values, torch.float64))
+        y = K.spmv_device(d, torch.as_tensor(x, device="cuda")).cpu().numpy()
+        assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
 
 
 @pytest.mark.parametrize("case", SPMV, ids=[c.name for c in SPMV])
@@ -403,18 +380,14 @@ def _banded_case(rng, lens, ncols):
     return ptrs, cols.astype(np.int64), rng.standard_normal(int(ptrs[-1]))
 
 
-@pytest.mark.parametrize("gather", GATHER)
 @pytest.mark.parametrize("strategy", ["merge", "load_balance"])
 @pytest.mark.parametrize("shape", ["tile_spanning_row", "empty_runs", "tile_aligned", "all_empty", "one_row",
                                    "skewed", "ints", "many_tiles", "multi_range"])
-def test_csr_balanced_edge_cases(wk, rng, shape, strategy, gather):
+def test_csr_balanced_edge_cases(wk, rng, shape, strategy):
     """merge-path and load-balance CSR: rows spanning many tiles / warp
     ranges, long runs of empty rows crossing them, rows ending exactly on tile /
     thread boundaries, empty matrices; tolerance 1e-12, exact on integer data;
-    both are deterministic; load_balance with and without the hot-column
-    gather plan (bitwise equal: same folds, same carries)."""
-    if strategy == "merge" and gather == "on":
-        pytest.skip("the gather plan applies to load_balance (and COO) only")
+    both are deterministic."""
     ncols = 70000
     if shape == "tile_spanning_row":
         lens = np.array([3, 50000, 2, 0, 7000, 1] + [5] * 900)
@@ -450,13 +423,8 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, gather):
     csr = wk.CsrMatrix(len(lens), ncols, ptrs, cols, vals)
     x = rng.integers(-5, 6, size=ncols).astype(np.float64) if shape == "ints" else rng.standard_normal(ncols)
     y_ref = sparse_ref.spmv(csr, x)
-    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy, "gather_plan": gather,
-                                                   "gather_min_count": 1})
+    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy})
     y = wk.spmv_csr(csr, x, e)
-    if gather == "on":
-        e_off = wk.make_executor("b200", device=0, tuning={"csr_strategy": strategy, "gather_plan": "off"})
-        assert wk.spmv_csr(csr, x, e_off).tobytes() == y.tobytes()
-        wk.spmv_csr(csr, x, e)  # back to the plan for the masked call below
     assert sparse_ref.max_scaled_rel_err(y, y_ref, lens) <= TOL
     if shape == "ints":
         assert np.array_equal(y, y_ref)
@@ -471,8 +439,6 @@ def test_csr_balanced_edge_cases(wk, rng, shape, strategy, gather):
     from paper_2006_14290_b200 import _lib
 
     d = D.as_device(csr, 0).with_strategy(strategy)
-    if gather == "on":
-        assert d.gather_plan() is not None
     xt = torch.as_tensor(x, device="cuda")
     yt = torch.full((csr.nrows,), 7.0, dtype=torch.float64, device="cuda")
     flag = torch.ones(1, dtype=torch.int32, device="cuda")

@@ -181,18 +181,24 @@ def test_cfg5_bicgstab_128_within_oracle_self_variation(wk):
     h = h.cpu().numpy()
     P = native.Prepared(_HostOp(C))
     nnz = _nnz_per_row(C)
-    threads = sorted({1, 2, 4, THREADS})
+    # BiCGSTAB on this nonsymmetric operator is chaotic in its iteration
+    # count: the C oracle alone takes 268-306 iterations to 1e-8 depending only
+    # on its thread count (the dot summation order; profiles/r02/bicgstab_counts.log).
+    # The GPU count must fall inside that distribution (widened by its spread).
+    threads = sorted(set(range(1, 17)) | {THREADS})
     runs = [P.bicgstab(np.ones(n), tol, 5000, nthreads=t) for t in threads]
     counts = [len(rh) - 1 for _, rh in runs]
     spread = max(counts) - min(counts)
-    x0 = runs[-1][0]
-    self_var = max(sparse_ref.max_scaled_rel_err(rx, x0, nnz) for rx, _ in runs[:-1])
+    i0 = threads.index(THREADS)
+    others = [r for i, r in enumerate(runs) if i != i0]
+    x0 = runs[i0][0]
+    self_var = max(sparse_ref.max_scaled_rel_err(rx, x0, nnz) for rx, _ in others)
     # early history: within 1e-10 ||b||, or within 10x the CPU runs' own
     # spread where that spread already exceeds it (the amplification starts
     # within the first iterations: 1.9e-10 ||b|| at iteration 5 on B200)
-    h0 = runs[-1][1]
+    h0 = runs[i0][1]
     k = 6
-    early_var = max(np.max(np.abs(rh[:k] - h0[:k])) for _, rh in runs[:-1]) / h0[0]
+    early_var = max(np.max(np.abs(rh[:k] - h0[:k])) for _, rh in others) / h0[0]
     for rx, rh in runs:
         dev = np.max(np.abs(h[:k] - rh[:k])) / rh[0]
         assert dev <= max(REL_TOL, 10 * early_var), (dev, early_var)
