@@ -583,6 +583,35 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
     res["hybrid_k8_rmat24"].update(ell_width=H.ell.width, ell_real_nnz=int(H.ell.nnz), coo_nnz=H.coo.nnz)
     del R, Rc, H, flush_buf
     torch.cuda.empty_cache()
+    # device ingestion of the raw R-MAT edge list (from_entries, sparse.py:63-80):
+    # stable radix sort of (row * 2^24 + col, value) over 48 key bits (6 passes
+    # of 8), duplicate offsets (scan) and the in-order duplicate fold
+    keys0, vals0 = corpus.rmat_edge_keys(RMAT_SCALE)
+    kb, vb = torch.empty_like(keys0), torch.empty_like(vals0)
+    n_r = 1 << RMAT_SCALE
+    m = keys0.numel()
+
+    def setup():
+        kb.copy_(keys0)
+        vb.copy_(vals0)
+
+    out = {}
+
+    def ingest():
+        out["coo"] = D.coo_from_keys(n_r, n_r, kb, vb, sum_duplicates=True, owned=True)
+
+    _, per = timed(ingest, 3, 1, None, flush=setup)
+    ms = statistics.mean(per)
+    nu = out["coo"].nnz
+    passes = (2 * RMAT_SCALE + 7) // 8
+    moved = m * (passes * 40 + 24) + m * 8 + nu * 16 + m * 16
+    res["from_entries_rmat24"] = {
+        "ms": round(ms, 3), "entries": int(m), "unique": int(nu), "Gentries/s": round(m / (ms * 1e-3) / 1e9, 2),
+        "GB/s": round(moved / (ms * 1e-3) / 1e9, 1), "bytes_moved": int(moved),
+        "note": "stable LSD radix sort (csrc/sort.cu: per pass 8 B upsweep read + 16 B read + 16 B write per "
+                "entry) + unique offsets + duplicate fold; includes one D2H read of the unique count"}
+    del keys0, vals0, kb, vb, out
+    torch.cuda.empty_cache()
     return res
 
 

@@ -188,6 +188,13 @@ int wk_csr_to_sellp_fill(int64_t nrows, int64_t slice_size, const int32_t* row_p
 int wk_csr_to_ell_fill(int64_t nrows, int64_t width, int64_t stride, const int32_t* row_ptrs,
                        const int32_t* col_idx, const double* values, int32_t* e_col, double* e_val,
                        int32_t* e_row_lengths, wk_stream_t stream);
+/* Stable LSD radix sort of (key, value) pairs on the low key_bits bits of the
+ * keys (8 bits per pass; from_entries' row-major lexsort, sparse.py:63-80).
+ * Sorts in place; keys_alt / values_alt are n-element scratch buffers; work:
+ * wk_sort_pairs_workspace(n) bytes. */
+int64_t wk_sort_pairs_workspace(int64_t n);
+int wk_sort_pairs_u64_f64(int64_t n, int32_t key_bits, uint64_t* keys, double* values, uint64_t* keys_alt,
+                          double* values_alt, void* work, int64_t work_bytes, wk_stream_t stream);
 /* Hybrid COO part, pass 1: offsets[0..nrows] = exclusive scan of max(len-width, 0) */
 int wk_hybrid_coo_offsets(int64_t nrows, int64_t width, const int32_t* row_ptrs, int64_t* offsets, void* scan_ws,
                           wk_stream_t stream);

@@ -142,6 +142,8 @@ _SIGS = {
     "wk_ell_zero_padding": (ctypes.c_int, [I64, I64, I64, P, P, P, P]),
     "wk_hybrid_coo_fill": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P, P, I64, P]),
     "wk_hybrid_coo_fill_workspace": (ctypes.c_int64, [I64]),
+    "wk_sort_pairs_workspace": (ctypes.c_int64, [I64]),
+    "wk_sort_pairs_u64_f64": (ctypes.c_int, [I64, I32, P, P, P, P, P, I64, P]),
     "wk_coo_to_csr_ptrs": (ctypes.c_int, [I64, I64, P, P, P]),
     "wk_csr_to_coo_rows": (ctypes.c_int, [I64, P, P, P]),
     "wk_scan_workspace_bytes": (I64, [I64]),

@@ -75,8 +75,9 @@ def convection_diffusion3d(n, beta=CONV_DIFF_BETA, device=None) -> D.DeviceCsr:
     return stencil(n, n, n, points_7pt(6.0, beta), device)
 
 
-def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, device=None, chunk=1 << 26) -> D.DeviceCoo:
-    """R-MAT(scale, edge_factor) as a sorted, duplicate-summed device COO."""
+def rmat_edge_keys(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, device=None, chunk=1 << 26):
+    """The raw R-MAT edge list as (row * 2**scale + col int64 keys, U[0,1)
+    values), in edge order (duplicates present)."""
     dev = D._dev(device)
     nedges = (1 << scale) * edge_factor
     keys = torch.empty(nedges, dtype=torch.int64, device=dev)
@@ -86,5 +87,11 @@ def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, device=None, ch
         cnt = min(chunk, nedges - lo)
         _lib.call("wk_gen_rmat_edges", scale, edge_factor, a, b, c, seed, lo, cnt,
                   D._ptr(keys[lo:lo + cnt]), D._ptr(vals[lo:lo + cnt]), st)
+    return keys, vals
+
+
+def rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, device=None, chunk=1 << 26) -> D.DeviceCoo:
+    """R-MAT(scale, edge_factor) as a sorted, duplicate-summed device COO."""
+    keys, vals = rmat_edge_keys(scale, edge_factor, a, b, c, seed, device, chunk)
     n = 1 << scale
-    return D.coo_from_keys(n, n, keys, vals, sum_duplicates=True)
+    return D.coo_from_keys(n, n, keys, vals, sum_duplicates=True, owned=True)

@@ -83,8 +83,14 @@ __global__ void sum_dups_kernel(int64_t n, int64_t ncols, const int64_t* __restr
     double acc = 0.0;
     for (int64_t j = i; j < n && keys[j] == key; ++j) acc += vals[j];
     const int64_t o = offsets[i];
-    row[o] = int(key / ncols);
-    col[o] = int(key % ncols);
+    if ((ncols & (ncols - 1)) == 0) {  // power of two (R-MAT): no 64-bit division
+        const int sh = __ffsll(ncols) - 1;
+        row[o] = int(key >> sh);
+        col[o] = int(key & (ncols - 1));
+    } else {
+        row[o] = int(key / ncols);
+        col[o] = int(key - (key / ncols) * ncols);
+    }
     out[o] = acc;
 }
 

@@ -671,9 +671,10 @@ def csr_to_hybrid(m, width=None, strategy="minimal_storage", percent=0.8, stride
 def coo_from_entries_device(nrows, ncols, rows, cols, values, sum_duplicates=True, device=None) -> DeviceCoo:
     """Sort triplets row-major and sum duplicates (sparse.py:63-80) on the GPU.
 
-    The key sort is torch's stable device sort (plumbing); the duplicate
-    fold is `wk_coo_sum_duplicates`: 0.0 + v1 + v2 + ... per key in input
-    order, which is `np.add.at` on zeros in the reference.
+    The key sort is `wk_sort_pairs_u64_f64` (stable LSD radix sort over the
+    bits of nrows * ncols, values moved with their keys); the duplicate fold
+    is `wk_coo_sum_duplicates`: 0.0 + v1 + v2 + ... per key in input order,
+    which is `np.add.at` on zeros in the reference.
     """
     dev = _dev(device)
     r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dev) if not isinstance(rows, torch.Tensor) else rows.to(dev, torch.int64)
@@ -688,15 +689,40 @@ def coo_from_entries_device(nrows, ncols, rows, cols, values, sum_duplicates=Tru
     return coo_from_keys(nrows, ncols, keys, v, sum_duplicates=sum_duplicates)
 
 
-def coo_from_keys(nrows, ncols, keys, values, sum_duplicates=True) -> DeviceCoo:
+def sort_pairs(keys, values, key_bits=64, inplace=False):
+    """Stable sort of int64 keys (>= 0, < 2**key_bits) with their f64 values
+    (csrc/sort.cu, 8-bit LSD passes over the low key_bits bits). Returns the
+    sorted (keys, values); with inplace=True the given contiguous tensors are
+    sorted and returned, otherwise copies."""
+    n = keys.numel()
+    if inplace:
+        assert keys.is_contiguous() and values.is_contiguous() and values.dtype == torch.float64
+        assert keys.data_ptr() % 16 == 0 and values.data_ptr() % 16 == 0, "sort_pairs needs 16-byte aligned tensors"
+        k, v = keys, values
+    else:
+        k = keys.contiguous().clone()
+        v = values.to(torch.float64).contiguous().clone()
+    if n <= 1:
+        return k, v
+    ka = torch.empty_like(k)
+    va = torch.empty_like(v)
+    nwork = int(_lib.load().wk_sort_pairs_workspace(n))
+    work = torch.empty((nwork + 15) // 16 * 2, dtype=torch.int64, device=k.device)
+    _lib.call("wk_sort_pairs_u64_f64", n, int(key_bits), _ptr(k), _ptr(v), _ptr(ka), _ptr(va), _ptr(work), nwork,
+              stream_handle(k.device))
+    return k, v
+
+
+def coo_from_keys(nrows, ncols, keys, values, sum_duplicates=True, owned=False) -> DeviceCoo:
+    """COO from int64 keys row * ncols + col (any order, duplicates allowed)
+    and values; owned=True lets the sort reorder `keys` / `values` in place."""
     dev = keys.device
     n = keys.numel()
     if n == 0:
         e32 = torch.empty(0, dtype=torch.int32, device=dev)
         return DeviceCoo(nrows, ncols, e32, e32.clone(), torch.empty(0, dtype=torch.float64, device=dev))
-    sk, perm = torch.sort(keys, stable=True)
-    sv = values[perm]
-    del perm
+    sk, sv = sort_pairs(keys, values, key_bits=max(int(nrows) * max(int(ncols), 1) - 1, 0).bit_length(),
+                        inplace=owned)
     if not sum_duplicates:
         if n > 1 and bool((sk[1:] == sk[:-1]).any()):
             raise ValueError("entries must be sorted row-major with unique (row, col) pairs")
