@@ -171,14 +171,18 @@ def sellp_bytes(d):
 
 
 def load_traffic(name):
-    """dram bytes per launch from a committed ncu --set full summary."""
+    """DRAM bytes per launch of `name` from the committed ncu --set full
+    summary (a STATIC capture, not measured in this run: ncu replays a kernel
+    ~40 times and cannot run inside the timed region). Returns (bytes,
+    source description) or (None, reason)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
             s = json.load(fh)
         k = s["kernels"][name]
-        return int(k["dram_bytes_read"] + k["dram_bytes_write"])
-    except Exception:
-        return None
+        return (int(k["dram_bytes_read"] + k["dram_bytes_write"]),
+                f"static: profiles/ncu_summary.json [{name}], {s.get('source', '')}")
+    except Exception as exc:  # noqa: BLE001
+        return None, f"unavailable ({exc.__class__.__name__})"
 
 
 # ---- CPU baseline (oracle C port, all host threads) ---------------------------------------------
@@ -458,7 +462,8 @@ def run_gpu(args, rank, world, dist):
         "hbm_gbs": round(bytes_launch * args.steps * world / (total_ms * 1e-3) / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000.0, 4),
-                     "peak_source": peak_src, "traffic": load_traffic("sellp_spmv"),
+                     "peak_source": peak_src, "traffic": load_traffic("sellp_spmv")[0],
+                     "traffic_source": load_traffic("sellp_spmv")[1],
                      "kernel": "sellp64_tma_kernel<J=4,S=3,W=16> (SELL-P(64), TMA bulk-copy ring, 2 rows/lane)",
                      "kernel_ms": round(kernel_ms, 4), "algorithmic_bytes": int(bytes_launch)},
         "e2e": e2e,

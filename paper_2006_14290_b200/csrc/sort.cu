@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kRsThreads)
 rs_upsweep(int64_t n, const unsigned long long* __restrict__ keys, int shift, int64_t nchunks,
            unsigned* __restrict__ counts) {
     __shared__ unsigned h[kRsWarps][kRsDigits];  // per-warp histograms
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, w = t >> 5;
 #pragma unroll
     for (int q = 0; q < kRsWarps; ++q) h[q][t] = 0u;
     __syncthreads();

@@ -130,16 +130,32 @@ static int log2i(int64_t v) {
     return l;
 }
 
+// SELL-P(64) TMA pipeline configuration by mean slice width (`stored` =
+// stored slots; 0 = unknown): narrow slices (the 7-point operators of CG,
+// BiCGSTAB, GMRES: width 7) stream 2-column chunks through 5-stage rings of
+// 24 warps — more independent warp pipelines, each with shorter gather
+// rounds; wide slices (27-point: width 27) 4-column chunks, 3 stages, 16
+// warps. Sweeps: profiles/r01/sellp_sweep*.jsonl, profiles/r02/sellp_sweep.log
+// (7-pt 256^3: 0.267 vs 0.275 ms; 27-pt 200^3: 0.389 vs 0.405 ms).
+using SellpNarrow = SellpTmaCfg<2, 5, 24, 1>;
+using SellpWide = SellpTmaCfg<4, 3, 16, 1>;
+constexpr int64_t kSellpNarrowWidth = 12;
+
+static bool sellp_narrow(int64_t nrows, int64_t stored) {
+    return stored > 0 && stored <= kSellpNarrowWidth * 64 * ceil_div(nrows, 64);
+}
+
 int launch_sellp(int64_t nrows, int64_t ncols, int64_t ss, const int64_t* sets, const int* col,
                  const double* val, const int* row_lengths, const double* x, double* y,
-                 const int* skip, cudaStream_t st) {
+                 const int* skip, cudaStream_t st, int64_t stored = 0) {
     if (nrows == 0) return 0;
     const int l2 = log2i(ss);
-    // SELL-P(64), 16-byte aligned: the TMA pipeline (J = 4 columns per chunk,
-    // 3-stage rings, 16 warps: the best of the (J, S, W) sweep in
-    // profiles/r01/sellp_sweep.jsonl); otherwise the register kernel.
-    if (ss == 64 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16))
-        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st);
+    // SELL-P(64), 16-byte aligned: the TMA pipeline; otherwise the register kernel.
+    if (ss == 64 && aligned(val, 16) && aligned(col, 16) && aligned(y, 16)) {
+        if (sellp_narrow(nrows, stored))
+            return launch_sellp64_tma<SellpNarrow>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st);
+        return launch_sellp64_tma<SellpWide>(nrows, ncols, sets, col, val, row_lengths, x, y, skip, st);
+    }
     const bool vec = ss >= 2 && aligned(val, 16) && aligned(col, 8) && aligned(y, 16);
     if (vec) {
         const int64_t threads = ceil_div(nrows, 2);
@@ -175,13 +191,14 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
     DotEpilogue dot{reinterpret_cast<double*>(w),
                     reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
                     reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo)};
+    // the fused-dot variant always takes the wide configuration: its extra
+    // registers (~100) do not fit the narrow configuration's 24 warps
+    // (spills: 319 vs 293 us on the 7-point 256^3 operator, same-box A/B)
     if (halo != nullptr)  // peer CG: the halo of p lands during the kernel (coherent gathers)
-        return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true, false, true>(
-            A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values, A->row_lengths, p, q, &s->done, st, dot, 0, 0,
-            rev);
-    return launch_sellp64_tma<SellpTmaCfg<4, 3, 16, 1>, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
-                                                             A->values, A->row_lengths, p, q, &s->done, st, dot,
-                                                             0, 0, rev);
+        return launch_sellp64_tma<SellpWide, true, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
+                                                         A->row_lengths, p, q, &s->done, st, dot, rev);
+    return launch_sellp64_tma<SellpWide, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
+                                               A->row_lengths, p, q, &s->done, st, dot, rev);
 }
 
 int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col,
@@ -492,7 +509,7 @@ int wk_spmv_masked(const wk_matrix* A, const double* x, double* y, const int32_t
                               y, skip, st);
         case WK_FMT_SELLP:
             return launch_sellp(A->nrows, A->ncols, A->slice_size, A->slice_sets, A->col_idx, A->values,
-                                A->row_lengths, x, y, skip, st);
+                                A->row_lengths, x, y, skip, st, A->nnz);
         case WK_FMT_HYBRID: {
             int rc = launch_ell(A->nrows, A->ncols, A->width, A->stride, A->col_idx, A->values, A->row_lengths, x,
                                 y, skip, st);

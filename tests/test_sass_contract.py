@@ -46,11 +46,12 @@ def _pick(funcs, *parts):
 
 
 def test_sellp_spmv_has_no_atomics_and_uses_tma(sass):
-    # default SpMV configuration SellpTmaCfg<4,3,16,1>, kDot = kEll = kCoh = false
-    (k,) = _pick(sass, "sellp64_tma_kernel", "SellpTmaCfgILi4ELi3ELi16ELi1E", "Lb0ELb0ELb0E")
-    assert not ATOMIC.search(sass[k])
-    assert "UBLKCP" in sass[k]
-    assert "DMUL" in sass[k] and "DADD" in sass[k] and "DFMA" not in sass[k]  # separately rounded fold
+    # both SpMV configurations (wide SellpTmaCfg<4,3,16,1>, narrow <2,5,24,1>), kDot = kCoh = false
+    for cfg in ("SellpTmaCfgILi4ELi3ELi16ELi1E", "SellpTmaCfgILi2ELi5ELi24ELi1E"):
+        (k,) = _pick(sass, "sellp64_tma_kernel", cfg, "Lb0ELb0E")
+        assert not ATOMIC.search(sass[k])
+        assert "UBLKCP" in sass[k]
+        assert "DMUL" in sass[k] and "DADD" in sass[k] and "DFMA" not in sass[k]  # separately rounded fold
 
 
 def test_ell_and_csr_rowblock_spmv_have_no_atomics(sass):
