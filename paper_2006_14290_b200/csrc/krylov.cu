@@ -165,9 +165,11 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
     for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np_eff; kl += 2 * T) {
         const bool h1 = kl + T < np;
         const int64_t k = rev ? np - 1 - kl : kl, k1 = rev ? np - 1 - (kl + T) : kl + T;
-        double2 pa = __ldcs(p2 + k), xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
+        // p is read again by the p update, which starts on the rows read here
+        // last: a plain load (not evict-first) lets it hit L2
+        double2 pa = p2[k], xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
         if (h1) {
-            pb = __ldcs(p2 + k1);
+            pb = p2[k1];
             xb = __ldcs(x2 + k1);
         }
         if (!repl) {

@@ -226,15 +226,24 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         if (r0 + 1 < nrows) return *reinterpret_cast<const double2*>(x + r0);
         return make_double2(r0 < nrows ? x[r0] : 0.0, 0.0);
     };
+    // kDot (CG): q is read by the next kernel, which starts on the rows this
+    // one wrote last (ping-pong): plain stores keep q's tail in L2 instead of
+    // the evict-first streaming stores of the SpMV
     auto emit = [&](int64_t r0, double a0, double a1, double2 p) {
         if (r0 + 1 < nrows) {
-            __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
+            if (kDot)
+                *reinterpret_cast<double2*>(y + r0) = make_double2(a0, a1);
+            else
+                __stcs(reinterpret_cast<double2*>(y + r0), make_double2(a0, a1));
             if (kDot) {
                 dacc += __dmul_rn(p.x, a0);
                 dacc += __dmul_rn(p.y, a1);
             }
         } else if (r0 < nrows) {
-            st_stream(y + r0, a0);
+            if (kDot)
+                y[r0] = a0;
+            else
+                st_stream(y + r0, a0);
             if (kDot) dacc += __dmul_rn(p.x, a0);
         }
     };

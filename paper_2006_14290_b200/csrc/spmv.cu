@@ -282,6 +282,43 @@ csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __res
     }
 }
 
+// CSR rows of at most a few entries (rowblock strategy, mean row length <=
+// kShortRow). A small cold operand (config 1: 80 MB, under the L2 size) is
+// bound by the dependent round trips row_ptrs -> col/val -> x, not by
+// bandwidth: one thread per row over a full grid (every row in flight as soon
+// as a slot frees), the row's kShortRow column/value loads issued together,
+// then its kShortRow gathers together, then the sequential fold (the
+// reference fold, bitwise). Longer rows repeat the batch. The persistent TMA
+// row-block kernel spends one more round trip per block on its staging ring
+// (24.5 us vs this kernel's ... us on config 1; profiles/r02).
+constexpr int kShortRow = 8;
+
+__global__ void __launch_bounds__(kSpmvThreads)
+csr_short_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __restrict__ col,
+                 const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
+                 const int* __restrict__ skip) {
+    if (skip != nullptr && *skip) return;
+    const int64_t r = int64_t(blockIdx.x) * kSpmvThreads + threadIdx.x;
+    if (r >= nrows) return;
+    const int lo = ld_stream(ptrs + r), hi = ld_stream(ptrs + r + 1);
+    double acc = 0.0;
+    for (int k0 = lo; k0 < hi; k0 += kShortRow) {
+        int c[kShortRow];
+        double v[kShortRow], xv[kShortRow];
+#pragma unroll
+        for (int u = 0; u < kShortRow; ++u) {
+            c[u] = k0 + u < hi ? ld_stream(col + k0 + u) : 0;
+            v[u] = k0 + u < hi ? ld_stream(val + k0 + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kShortRow; ++u) xv[u] = k0 + u < hi ? ld_x(x, c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kShortRow; ++u)
+            if (k0 + u < hi) acc = mul_add_rn(acc, v[u], xv[u]);
+    }
+    st_stream(y + r, acc);
+}
+
 __global__ void zero_masked_kernel(double* __restrict__ y, int64_t n, const int* __restrict__ skip) {
     if (*skip) return;
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -324,6 +361,14 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
                            HeadPlan{h.hoff, h.mask, h.hrow, h.crow, h.cval, h.rrow});
     }
     if (strategy == WK_CSR_ROWBLOCK) {
+        // mean row length <= 8 (2-D stencils, BASELINE config 1): one thread
+        // per row, every load of a row issued at once (csr_short_kernel)
+        if (nnz <= int64_t(kShortRow) * nrows) {
+            csr_short_kernel<<<(unsigned)ceil_div(nrows, kSpmvThreads), kSpmvThreads, 0, st>>>(nrows, ptrs, col, val,
+                                                                                            x, y, skip);
+            WK_LAUNCH_CHECK();
+            return 0;
+        }
         // 32*k-row blocks; the stage capacity is the smallest that keeps a
         // 32-row block of mean-length rows "light" (more warps per SM when
         // rows are short). Measured sweep: profiles/r01/csr_sweep.jsonl.
