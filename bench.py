@@ -638,10 +638,18 @@ def bench_cg(args, wk, corpus, D):
     it = len(hist) - 1
     spmv_b = A.algorithmic_bytes()
     per_it = spmv_b + 72 * A.nrows + (spmv_b + 24 * A.nrows) / 50
+    # the CG operator's plain SpMV (narrow SELL-P configuration: 7-wide slices)
+    xs = torch.rand(A.ncols, dtype=torch.float64, device="cuda")
+    ys = torch.empty(A.nrows, dtype=torch.float64, device="cuda")
+    _, per = timed(lambda: wk.kernels.spmv_device(A, xs, ys), 20, 3, None)
+    sp_ms = statistics.mean(per)
     return {"workload": f"CG, 7-point Laplacian {CG_GRID}^3, SELL-P({SLICE}), b = ones, tol 1e-30, {CG_ITERS} iterations",
             "iterations": it, "ms": round(ms, 2), "it_per_s": round(it / (ms * 1e-3), 1),
             "GB/s_effective": round(per_it * it / (ms * 1e-3) / 1e9, 1), "bytes_per_iteration": int(per_it),
-            "n_gpus": 1}
+            "n_gpus": 1,
+            "operator_spmv": {"ms": round(sp_ms, 4), "GB/s": round(spmv_b / (sp_ms * 1e-3) / 1e9, 1),
+                              "bytes": int(spmv_b), "GFLOP/s": round(2 * A.nnz / (sp_ms * 1e-3) / 1e9, 1),
+                              "kernel": "sellp64_tma_kernel<J=2,S=5,W=24> (narrow: slices <= 12 wide)"}}
 
 
 def _safe(fn):
