@@ -134,21 +134,22 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     bool pvalid = false;
     // slice offsets are read one slice ahead (registers), so the next
     // slice's sets[] loads are in flight while this slice streams
-    int64_t q0 = 0, q1 = 0, n0 = 0, n1 = 0;
+    // (slice offsets in 64-slot units: int32 is enough below 2^37 stored slots)
+    int q0 = 0, q1 = 0, n0 = 0, n1 = 0;
     if (ps < nslices) {
-        q0 = __ldg(sets + SP(ps));
-        q1 = __ldg(sets + SP(ps) + 1);
+        q0 = int(__ldg(sets + SP(ps)));
+        q1 = int(__ldg(sets + SP(ps) + 1));
     }
     if (ps + nwarps < nslices) {
-        n0 = __ldg(sets + SP(ps + nwarps));
-        n1 = __ldg(sets + SP(ps + nwarps) + 1);
+        n0 = int(__ldg(sets + SP(ps + nwarps)));
+        n1 = int(__ldg(sets + SP(ps + nwarps) + 1));
     }
     auto seek = [&]() {
         pvalid = false;
         while (ps < nslices) {
             pw = int(q1 - q0);
             if (pj < pw) {
-                pbase = q0 * 64;
+                pbase = int64_t(q0) * 64;
                 pvalid = true;
                 return;
             }
@@ -157,8 +158,8 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             q0 = n0;
             q1 = n1;
             if (ps + nwarps < nslices) {
-                n0 = __ldg(sets + SP(ps + nwarps));
-                n1 = __ldg(sets + SP(ps + nwarps) + 1);
+                n0 = int(__ldg(sets + SP(ps + nwarps)));
+                n1 = int(__ldg(sets + SP(ps + nwarps) + 1));
             }
         }
     };
@@ -218,9 +219,8 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         }
     };
     double dacc = 0.0;
-    // kDot: x at the slice's own rows (CG: p[r]) is loaded when the slice
-    // starts and consumed after its fold (a load at the end cost one more L2
-    // round trip per slice: 305 vs 269 us on the 7-point operator)
+    // kDot: x at the slice's own rows (CG: p[r]), read after the fold (L1/L2
+    // hits: the same lines were just gathered)
     auto xown = [&](int64_t r0) -> double2 {
         if (!kDot) return make_double2(0.0, 0.0);
         if (r0 + 1 < nrows) return *reinterpret_cast<const double2*>(x + r0);
@@ -284,7 +284,6 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             }
         };
         lens();
-        double2 pown = xown(r0);
         double a0 = 0.0, a1 = 0.0;
         SellpChunkRegs<J> ca, cb;
         load(ca, s, w, 0);
@@ -305,13 +304,12 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
                 j0 += J;
                 return true;
             }
-            emit(r0, a0, a1, pown);
+            emit(r0, a0, a1, xown(r0));
             if (sn >= nslices) return false;
             s = sn;
             w = wn;
             j0 = 0;
             r0 = SP(s) * 64 + 2 * lane;
-            pown = xown(r0);
             lens();
             a0 = 0.0;
             a1 = 0.0;

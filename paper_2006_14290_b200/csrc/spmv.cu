@@ -191,9 +191,13 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
     DotEpilogue dot{reinterpret_cast<double*>(w),
                     reinterpret_cast<unsigned*>(w + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, finalize,
                     reinterpret_cast<PeerCtx*>(peer), reinterpret_cast<const PeerHalo*>(halo)};
-    // the fused-dot variant always takes the wide configuration: its extra
-    // registers (~100) do not fit the narrow configuration's 24 warps
-    // (spills: 319 vs 293 us on the 7-point 256^3 operator, same-box A/B)
+    // narrow slices (CG's 7-point operator): the narrow configuration (the
+    // register-lean cursor state keeps its fused-dot variant at 80 registers,
+    // no spills: 279 vs 287 us for the wide one); the peer variant, with its
+    // halo logic, keeps the wide configuration
+    if (halo == nullptr && sellp_narrow(A->nrows, A->nnz))
+        return launch_sellp64_tma<SellpNarrow, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
+                                                     A->row_lengths, p, q, &s->done, st, dot, rev);
     if (halo != nullptr)  // peer CG: the halo of p lands during the kernel (coherent gathers)
         return launch_sellp64_tma<SellpWide, true, true>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
                                                          A->row_lengths, p, q, &s->done, st, dot, rev);

@@ -160,3 +160,39 @@ def test_c_bicgstab_matches_python_restatement(name):
         # both converged to tol: the iterates agree to the conditioning-scaled
         # tolerance of the solve
         assert np.max(np.abs(xc - xr)) / np.max(np.abs(xr)) <= 1e-5
+
+
+def _scaled_laplacian(n, seed):
+    """S L S with S = diag(sqrt(U[1, 100])): SPD and badly scaled, so the
+    Jacobi preconditioner matters."""
+    rng = np.random.default_rng(seed)
+    P = corpus_ref.poisson2d(n)
+    L = _op(P)
+    s = np.sqrt(rng.uniform(1.0, 100.0, size=P.nrows))
+    return (scipy_sparse.diags(s) @ L @ scipy_sparse.diags(s)).tocsr()
+
+
+@pytest.mark.parametrize("n,seed", [(8, 1), (10, 2), (12, 3)])
+def test_pcg_jacobi_restatement_equals_scipy_bitwise(n, seed):
+    """krylov_ref.pcg_jacobi_solve reproduces scipy.sparse.linalg.cg with
+    M = diag(A)^-1 (scipy's `_isolve/iterative.py` cg: z = psolve(r),
+    rho = r.z, p = z + beta p, alpha = rho / p.Ap, x += alpha p,
+    r -= alpha q) bit for bit, iteration for iteration, while no residual
+    replacement happens (< 50 iterations). Pins the PCG restatement — which
+    the GPU PCG is tested against — to a third-party implementation (the
+    reference has no PCG)."""
+    S = _scaled_laplacian(n, seed)
+    d = S.diagonal().copy()
+    b = np.ones(S.shape[0])
+    tol = 1e-10
+    x, hist = krylov_ref.pcg_jacobi_solve(lambda v: S @ v, d, b, tol, 500, dot=np.dot)
+    assert len(hist) - 1 < 50
+    M = sla.LinearOperator(S.shape, matvec=lambda r: r / d)
+    xs_ = []
+    xref, info = sla.cg(S, b, rtol=tol, atol=0.0, maxiter=500, M=M, callback=lambda xk: xs_.append(xk.copy()))
+    assert info == 0
+    assert len(xs_) == len(hist) - 1
+    assert xref.tobytes() == x.tobytes()
+    # and every iterate's residual norm equals the restatement's history
+    for k, xk in enumerate(xs_):
+        assert np.linalg.norm(b - S @ xk) == pytest.approx(hist[k + 1], rel=1e-6)
