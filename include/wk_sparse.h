@@ -236,14 +236,16 @@ int wk_gen_stencil_csr(int64_t nx, int64_t ny, int64_t nz, int32_t npoints, cons
  * (oracle/corpus_ref.py rmat_edges restates the same hash) */
 int wk_gen_rmat_edges(int32_t scale, int32_t edge_factor, double a, double b, double c, uint64_t seed,
                       int64_t edge_lo, int64_t count, int64_t* keys, double* values, wk_stream_t stream);
-/* duplicate summation over keys sorted stably (sparse.py:73-79):
- * pass 1 flags[i] = (i == 0 || key[i] != key[i-1]) scanned into offsets (n+1) */
-int wk_coo_unique_offsets(int64_t n, const int64_t* keys, int64_t* offsets, void* scan_ws, wk_stream_t stream);
-/* pass 2: out entry per unique key (row = key / ncols, col = key % ncols),
- * value = 0.0 + v1 + v2 + ... in order */
-int wk_coo_sum_duplicates(int64_t n, int64_t ncols, const int64_t* keys, const double* values,
-                          const int64_t* offsets, int32_t* row, int32_t* col, double* out_values,
-                          wk_stream_t stream);
+/* from_entries duplicate fold (sparse.py:73-79) over keys sorted by
+ * wk_sort_pairs_u64_f64: pass 1 counts the unique keys per 2048-key tile and
+ * scans them (work: wk_coo_dedup_workspace(n) bytes; the unique count lands
+ * at ((int64_t*)work)[wk_coo_dedup_tiles(n)]); pass 2 writes row = key / ncols,
+ * col = key % ncols and value = 0.0 + v1 + v2 + ... in input order. */
+int64_t wk_coo_dedup_tiles(int64_t n);
+int64_t wk_coo_dedup_workspace(int64_t n);
+int wk_coo_dedup_count(int64_t n, const int64_t* keys, void* work, wk_stream_t stream);
+int wk_coo_dedup_scatter(int64_t n, int64_t ncols, const int64_t* keys, const double* values, const void* work,
+                         int32_t* row, int32_t* col, double* out_values, wk_stream_t stream);
 
 /* ---- Krylov solvers (replace cg_solve, kernels.py:283-331; BiCGSTAB and
  *      GMRES(m) have no reference). x, hist are device arrays; hist holds

@@ -150,8 +150,10 @@ _SIGS = {
     "wk_exclusive_scan_i64": (ctypes.c_int, [I64, P, P, P, P]),
     "wk_gen_stencil_csr": (ctypes.c_int, [I64, I64, I64, I32, P, P, P, P, P, P, P, P, P]),
     "wk_gen_rmat_edges": (ctypes.c_int, [I32, I32, F64, F64, F64, U64, I64, I64, P, P, P]),
-    "wk_coo_unique_offsets": (ctypes.c_int, [I64, P, P, P, P]),
-    "wk_coo_sum_duplicates": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P]),
+    "wk_coo_dedup_tiles": (ctypes.c_int64, [I64]),
+    "wk_coo_dedup_workspace": (ctypes.c_int64, [I64]),
+    "wk_coo_dedup_count": (ctypes.c_int, [I64, P, P, P]),
+    "wk_coo_dedup_scatter": (ctypes.c_int, [I64, I64, P, P, P, P, P, P, P]),
     "wk_cg_workspace_bytes": (I64, [I64]),
     "wk_cg_solve": (ctypes.c_int, [P, P, F64, I64, P, P, P, P, P]),
     "wk_bicgstab_workspace_bytes": (I64, [I64]),

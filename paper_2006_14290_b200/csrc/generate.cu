@@ -73,25 +73,87 @@ __global__ void rmat_kernel(int scale, double a, double b, double c, uint64_t se
     vals[t] = uniform01(seed, e * L + uint64_t(scale));
 }
 
-__global__ void sum_dups_kernel(int64_t n, int64_t ncols, const int64_t* __restrict__ keys,
-                                const double* __restrict__ vals, const int64_t* __restrict__ offsets,
-                                int* __restrict__ row, int* __restrict__ col, double* __restrict__ out) {
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int64_t key = keys[i];
-    if (i > 0 && keys[i - 1] == key) return;
-    double acc = 0.0;
-    for (int64_t j = i; j < n && keys[j] == key; ++j) acc += vals[j];
-    const int64_t o = offsets[i];
-    if ((ncols & (ncols - 1)) == 0) {  // power of two (R-MAT): no 64-bit division
-        const int sh = __ffsll(ncols) - 1;
-        row[o] = int(key >> sh);
-        col[o] = int(key & (ncols - 1));
+// Duplicate fold of a sorted key array (from_entries, sparse.py:73-79: the
+// values of equal (row, col) keys summed as 0.0 + v1 + v2 + ... in input
+// order, np.add.at on zeros). Tiles of 2048 keys, 8 consecutive per thread:
+//   dedup_count_kernel    heads (key != previous key) per tile
+//   (exclusive scan of the tile counts, total in the last slot)
+//   dedup_scatter_kernel  heads again, block scan -> output slot, each head
+//                         folds its run and writes (row, col, value)
+// Keys are read twice and values once; the round-1 version materialised an
+// int64 offset per input key (three passes over 268M keys on R-MAT 24).
+constexpr int kDdThreads = 256, kDdItems = 8;
+constexpr int64_t kDdTile = int64_t(kDdThreads) * kDdItems;
+
+__device__ __forceinline__ int tile_heads(int64_t n, const int64_t* __restrict__ keys, int64_t base, int64_t (&k)[kDdItems],
+                                          unsigned& hmask) {
+    int64_t prev = base > 0 && base < n ? keys[base - 1] : 0;
+    int c = 0;
+    hmask = 0u;
+    if (base + kDdItems <= n) {
+#pragma unroll
+        for (int u = 0; u < kDdItems; u += 2) {
+            const longlong2 t = __ldcs(reinterpret_cast<const longlong2*>(keys + base + u));
+            k[u] = t.x;
+            k[u + 1] = t.y;
+        }
     } else {
-        row[o] = int(key / ncols);
-        col[o] = int(key - (key / ncols) * ncols);
+#pragma unroll
+        for (int u = 0; u < kDdItems; ++u) k[u] = base + u < n ? keys[base + u] : 0;
     }
-    out[o] = acc;
+#pragma unroll
+    for (int u = 0; u < kDdItems; ++u) {
+        const int64_t i = base + u;
+        if (i < n && (i == 0 || k[u] != prev)) {
+            hmask |= 1u << u;
+            ++c;
+        }
+        prev = k[u];
+    }
+    return c;
+}
+
+__global__ void __launch_bounds__(kDdThreads)
+dedup_count_kernel(int64_t n, const int64_t* __restrict__ keys, int64_t* __restrict__ tile_counts) {
+    __shared__ int64_t smem[kDdThreads / 32 + 1];
+    int64_t k[kDdItems];
+    unsigned hm;
+    const int c = tile_heads(n, keys, int64_t(blockIdx.x) * kDdTile + int64_t(threadIdx.x) * kDdItems, k, hm);
+    int64_t tot;
+    block_exclusive_scan<int64_t>(int64_t(c), smem, tot);
+    if (threadIdx.x == 0) tile_counts[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kDdThreads)
+dedup_scatter_kernel(int64_t n, int64_t ncols, const int64_t* __restrict__ keys, const double* __restrict__ vals,
+                     const int64_t* __restrict__ tile_offs, int* __restrict__ row, int* __restrict__ col,
+                     double* __restrict__ out) {
+    __shared__ int64_t smem[kDdThreads / 32 + 1];
+    const int64_t base = int64_t(blockIdx.x) * kDdTile + int64_t(threadIdx.x) * kDdItems;
+    int64_t k[kDdItems];
+    unsigned hm;
+    const int c = tile_heads(n, keys, base, k, hm);
+    int64_t tot;
+    int64_t o = block_exclusive_scan<int64_t>(int64_t(c), smem, tot) + tile_offs[blockIdx.x];
+    const bool pow2 = (ncols & (ncols - 1)) == 0;  // R-MAT: no 64-bit division
+    const int sh = pow2 ? __ffsll(ncols) - 1 : 0;
+#pragma unroll
+    for (int u = 0; u < kDdItems; ++u) {
+        if (!((hm >> u) & 1u)) continue;
+        const int64_t key = k[u];
+        double acc = 0.0;
+        for (int64_t j = base + u; j < n && keys[j] == key; ++j) acc += vals[j];
+        if (pow2) {
+            row[o] = int(key >> sh);
+            col[o] = int(key & (ncols - 1));
+        } else {
+            const int64_t q = key / ncols;
+            row[o] = int(q);
+            col[o] = int(key - q * ncols);
+        }
+        out[o] = acc;
+        ++o;
+    }
 }
 
 }  // namespace wk
@@ -151,19 +213,30 @@ int wk_gen_rmat_edges(int32_t scale, int32_t edge_factor, double a, double b, do
     return 0;
 }
 
-int wk_coo_unique_offsets(int64_t n, const int64_t* keys, int64_t* offsets, void* scan_ws, wk_stream_t stream) {
+int64_t wk_coo_dedup_tiles(int64_t n) { return ceil_div(n, kDdTile); }
+
+int64_t wk_coo_dedup_workspace(int64_t n) { return (wk_coo_dedup_tiles(n) + 1) * 8; }
+
+int wk_coo_dedup_count(int64_t n, const int64_t* keys, void* work, wk_stream_t stream) {
     clear_error();
-    auto head = [=] __device__(int64_t i) { return int64_t(i == 0 || keys[i] != keys[i - 1]); };
-    return exclusive_scan(n, head, offsets, scan_ws, as_stream(stream));
+    cudaStream_t st = as_stream(stream);
+    const int64_t nt = wk_coo_dedup_tiles(n);
+    int64_t* tc = reinterpret_cast<int64_t*>(work);
+    WK_CUDA(cudaMemsetAsync(tc + nt, 0, 8, st));
+    if (nt) {
+        dedup_count_kernel<<<(unsigned)nt, kDdThreads, 0, st>>>(n, keys, tc);
+        WK_LAUNCH_CHECK();
+    }
+    return scan_tile_sums_exclusive_launch(nt + 1, tc, st);  // tc[nt] = number of unique keys
 }
 
-int wk_coo_sum_duplicates(int64_t n, int64_t ncols, const int64_t* keys, const double* values,
-                          const int64_t* offsets, int32_t* row, int32_t* col, double* out_values,
-                          wk_stream_t stream) {
+int wk_coo_dedup_scatter(int64_t n, int64_t ncols, const int64_t* keys, const double* values, const void* work,
+                         int32_t* row, int32_t* col, double* out_values, wk_stream_t stream) {
     clear_error();
-    if (n == 0) return 0;
-    sum_dups_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(n, ncols > 0 ? ncols : 1, keys, values, offsets,
-                                                                             row, col, out_values);
+    const int64_t nt = wk_coo_dedup_tiles(n);
+    if (nt == 0) return 0;
+    dedup_scatter_kernel<<<(unsigned)nt, kDdThreads, 0, as_stream(stream)>>>(
+        n, ncols > 0 ? ncols : 1, keys, values, reinterpret_cast<const int64_t*>(work), row, col, out_values);
     WK_LAUNCH_CHECK();
     return 0;
 }

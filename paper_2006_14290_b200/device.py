@@ -673,8 +673,8 @@ def coo_from_entries_device(nrows, ncols, rows, cols, values, sum_duplicates=Tru
 
     The key sort is `wk_sort_pairs_u64_f64` (stable LSD radix sort over the
     bits of nrows * ncols, values moved with their keys); the duplicate fold
-    is `wk_coo_sum_duplicates`: 0.0 + v1 + v2 + ... per key in input order,
-    which is `np.add.at` on zeros in the reference.
+    is `wk_coo_dedup_count` + `wk_coo_dedup_scatter`: 0.0 + v1 + v2 + ... per
+    key in input order, which is `np.add.at` on zeros in the reference.
     """
     dev = _dev(device)
     r = torch.as_tensor(np.asarray(rows, dtype=np.int64), device=dev) if not isinstance(rows, torch.Tensor) else rows.to(dev, torch.int64)
@@ -728,14 +728,15 @@ def coo_from_keys(nrows, ncols, keys, values, sum_duplicates=True, owned=False) 
             raise ValueError("entries must be sorted row-major with unique (row, col) pairs")
         nc = max(int(ncols), 1)
         return DeviceCoo(nrows, ncols, (sk // nc).to(torch.int32), (sk % nc).to(torch.int32), sv.contiguous())
-    ws = workspace(dev)
     st = stream_handle(dev)
-    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
-    _lib.call("wk_coo_unique_offsets", n, _ptr(sk), _ptr(offsets), _ptr(ws.scan_ws(n)), st)
-    nu = int(offsets[-1].item())
+    L = _lib.load()
+    nt = int(L.wk_coo_dedup_tiles(n))
+    work = torch.empty(nt + 1, dtype=torch.int64, device=dev)
+    _lib.call("wk_coo_dedup_count", n, _ptr(sk), _ptr(work), st)
+    nu = int(work[nt].item())
     row = torch.empty(nu, dtype=torch.int32, device=dev)
     col = torch.empty(nu, dtype=torch.int32, device=dev)
     val = torch.empty(nu, dtype=torch.float64, device=dev)
-    _lib.call("wk_coo_sum_duplicates", n, int(ncols), _ptr(sk), _ptr(sv), _ptr(offsets), _ptr(row), _ptr(col),
-              _ptr(val), st)
+    _lib.call("wk_coo_dedup_scatter", n, int(ncols), _ptr(sk), _ptr(sv), _ptr(work), _ptr(row), _ptr(col), _ptr(val),
+              st)
     return DeviceCoo(nrows, ncols, row, col, val)
