@@ -767,3 +767,54 @@ def test_from_entries_rmat_matches_oracle(wk):
     r = corpus_ref.rmat(16)
     assert np.array_equal(d.row_idx, r.row_idx) and np.array_equal(d.col_idx, r.col_idx)
     assert d.values.tobytes() == r.values.tobytes()
+
+
+@pytest.mark.parametrize("shape", ["short_with_long_rows", "empty_rows", "exactly_8", "mean_above_8"])
+def test_csr_rowblock_short_kernel_edges(wk, ex, rng, shape):
+    """The rowblock strategy's thread-per-row kernel (mean row length <= 8)
+    on rows longer than its 8-entry batch (one of 3000 entries), runs of
+    empty rows, rows of exactly 8, and the TMA row-block path just above the
+    mean threshold: bitwise against the reference fold, also with x[0] = inf
+    (padding never enters a CSR fold)."""
+    n, ncols = 50000, 60000
+    lens = rng.integers(0, 9, size=n)
+    if shape == "short_with_long_rows":
+        lens[[3, 777, n - 1]] = [3000, 17, 9]
+    elif shape == "empty_rows":
+        lens[1000:9000] = 0
+    elif shape == "exactly_8":
+        lens[:] = 8
+    else:
+        lens = rng.integers(6, 13, size=n)  # mean ~9: the TMA row-block kernel
+    ptrs, cols, vals = _banded_case(rng, lens, ncols)
+    csr = wk.CsrMatrix(n, ncols, ptrs, cols, vals)
+    e = wk.make_executor("b200", device=0, tuning={"csr_strategy": "rowblock"})
+    for x0 in (0.25, np.inf):
+        x = rng.standard_normal(ncols)
+        x[0] = x0
+        y = wk.spmv_csr(csr, x, e)
+        assert y.tobytes() == sparse_ref.spmv(csr, x).tobytes()
+
+
+@pytest.mark.parametrize("width", [0, 1, 4])
+def test_hybrid_fill_long_row_boundaries(wk, ex, rng, width):
+    """CSR -> Hybrid COO remainder around the fill's thresholds: rows whose
+    overflow is 255 / 256 / 257 entries (flattened run vs long-row queue),
+    4095 / 4096 / 4097 and 12289 (segment boundaries of the queue), 32-row
+    groups full of long rows, and empty groups; bitwise against the oracle."""
+    n, ncols = 4000, 20000
+    lens = rng.integers(0, 6, size=n)
+    specials = [255, 256, 257, 4095, 4096, 4097, 12289]
+    for i, L in enumerate(specials):
+        lens[100 + i] = L + width
+    lens[640:672] = 300 + width       # a 32-row group of long rows
+    lens[2000:2100] = 0               # empty groups
+    ptrs, cols, vals = _banded_case(rng, lens, ncols)
+    csr = wk.CsrMatrix(n, ncols, ptrs, cols, vals)
+    hyb = wk.csr_to_hybrid(csr, width=width, exec=ex)
+    ref = sparse_ref.csr_to_hybrid(csr, width)
+    assert np.array_equal(hyb.coo.row_idx, ref.coo.row_idx)
+    assert np.array_equal(hyb.coo.col_idx, ref.coo.col_idx)
+    assert hyb.coo.values.tobytes() == ref.coo.values.tobytes()
+    x = rng.standard_normal(ncols)
+    assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), sparse_ref.spmv(csr, x), lens) <= TOL
