@@ -337,6 +337,14 @@ static int cgs_grid(int64_t n, int K) {
     return int(g < 1 ? 1 : g);
 }
 
+static int orth_grid(int64_t n) {
+    int64_t g = ceil_div(ceil_div(n, 2), 256);
+    const int64_t cap = int64_t(sm_count()) * 4;
+    if (g > cap) g = cap;
+    if (g > kRedMaxBlocks) g = kRedMaxBlocks;
+    return int(g < 1 ? 1 : g);
+}
+
 static bool cgs_vec_ok(const double* V, int64_t ld, const double* w) {
     return ((reinterpret_cast<uintptr_t>(V) | reinterpret_cast<uintptr_t>(w)) & 15) == 0 && (ld & 1) == 0;
 }
@@ -379,8 +387,11 @@ gmres_multidot_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, c
     }
 }
 
+// (256, 4): at most 64 registers, so 4 blocks per SM of the orthogonalisation
+// (which keeps no accumulators) instead of the 2 its K = 32 variant got with
+// every basis load hoisted: 5.5-6.0 -> 6.2-6.4 TB/s (tools/orth_probe.py)
 template <int K>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)
 gmres_orth_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, double* __restrict__ w,
                const double* __restrict__ Hj, GS* s, RedWorkspace ws) {
     if (s->cycle_done) return;
@@ -465,11 +476,18 @@ static int gmres_orth(int64_t n, int j, const double* V, int64_t ld, double* w, 
     const int k = j + 1;
     if (cgs_vec_ok(V, ld, w) && k <= kRedMaxVec) {
         const RedWorkspace rw = red_ws(ws);
-        if (k <= 2) WK_CGS_LAUNCH(gmres_orth_vec, 2, n, k, V, ld, w, Hj, s, rw);
-        if (k <= 4) WK_CGS_LAUNCH(gmres_orth_vec, 4, n, k, V, ld, w, Hj, s, rw);
-        if (k <= 8) WK_CGS_LAUNCH(gmres_orth_vec, 8, n, k, V, ld, w, Hj, s, rw);
-        if (k <= 16) WK_CGS_LAUNCH(gmres_orth_vec, 16, n, k, V, ld, w, Hj, s, rw);
-        WK_CGS_LAUNCH(gmres_orth_vec, kRedMaxVec, n, k, V, ld, w, Hj, s, rw);
+#define WK_ORTH(KK)                                                                        \
+    do {                                                                                   \
+        gmres_orth_vec<KK><<<orth_grid(n), 256, 0, st>>>(n, k, V, ld, w, Hj, s, rw);        \
+        WK_LAUNCH_CHECK();                                                                 \
+        return 0;                                                                          \
+    } while (0)
+        if (k <= 2) WK_ORTH(2);
+        if (k <= 4) WK_ORTH(4);
+        if (k <= 8) WK_ORTH(8);
+        if (k <= 16) WK_ORTH(16);
+        WK_ORTH(kRedMaxVec);
+#undef WK_ORTH
     }
     return launch_map_reduce(
         n,
