@@ -246,28 +246,30 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
-    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += 2 * T) {
-        const bool h1 = kl + T < np;
-        const int64_t k = rev ? np - 1 - kl : kl, k1 = rev ? np - 1 - (kl + T) : kl + T;
-        double2 ra = __ldcs(r2 + k), pa = p2[k], rb{0, 0}, pb{0, 0};
-        if (h1) {
-            rb = __ldcs(r2 + k1);
-            pb = p2[k1];
+    // four pairs of r and p in flight per thread (a copy-shaped step: two
+    // pairs left it at 5.7 TB/s)
+    constexpr int U = 4;
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += U * T) {
+        double2 ra[U], pa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            ra[u] = ku < np ? __ldcs(r2 + k) : make_double2(0.0, 0.0);
+            pa[u] = ku < np ? p2[k] : make_double2(0.0, 0.0);
         }
-        pa.x = __dadd_rn(ra.x, __dmul_rn(beta, pa.x));
-        pa.y = __dadd_rn(ra.y, __dmul_rn(beta, pa.y));
-        p2[k] = pa;
-        if (halo != nullptr) {  // the boundary rows go straight into the neighbours' halo copies
-            halo_store(peer, halo, 2 * k, pa.x);
-            halo_store(peer, halo, 2 * k + 1, pa.y);
-        }
-        if (h1) {
-            pb.x = __dadd_rn(rb.x, __dmul_rn(beta, pb.x));
-            pb.y = __dadd_rn(rb.y, __dmul_rn(beta, pb.y));
-            p2[k1] = pb;
-            if (halo != nullptr) {
-                halo_store(peer, halo, 2 * k1, pb.x);
-                halo_store(peer, halo, 2 * k1 + 1, pb.y);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            if (ku >= np) break;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            double2 q;
+            q.x = __dadd_rn(ra[u].x, __dmul_rn(beta, pa[u].x));
+            q.y = __dadd_rn(ra[u].y, __dmul_rn(beta, pa[u].y));
+            p2[k] = q;
+            if (halo != nullptr) {  // the boundary rows go straight into the neighbours' halo copies
+                halo_store(peer, halo, 2 * k, q.x);
+                halo_store(peer, halo, 2 * k + 1, q.y);
             }
         }
     }

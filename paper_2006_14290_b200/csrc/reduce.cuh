@@ -142,8 +142,8 @@ int launch_map_reduce(int64_t n, F f, Epi epi, void* ws, const int* skip, cudaSt
 // Vectorised element-wise step with optional fused reductions (the Krylov
 // BLAS-1 updates): NIN input vectors, NOUT output vectors (may alias inputs:
 // every load of an iteration precedes its stores), NRED sums. Each thread
-// handles two double2 pairs per iteration (k and k + T), so four elements of
-// every vector are in flight per thread; the solver scalars are read ONCE per
+// handles U double2 pairs per iteration (k, k + T, ...; U = 4 for one input,
+// 2 otherwise), so 2U elements of every vector are in flight per thread; the solver scalars are read ONCE per
 // thread by `pro()` instead of once per element (a scalar read through the
 // state pointer cannot be hoisted past the vector stores). Per-thread sums run
 // in a fixed element order and are folded by grid_reduce_last_n: deterministic.
@@ -166,8 +166,11 @@ inline int vmap_grid(int64_t n) {
 }
 
 // kRunIf: run only while *skip != 0 (instead of skipping then)
+// (kRedThreads, 4): at most 64 registers, so the grid's 8 blocks per SM are
+// not cut to 3 by the one-in / one-out instances (GMRES basis scaling: 80
+// registers, 4.8 TB/s)
 template <int NIN, int NOUT, int NRED, bool kRunIf, typename Pro, typename F, typename Epi>
-__global__ void __launch_bounds__(kRedThreads)
+__global__ void __launch_bounds__(kRedThreads, 4)
 vmap_kernel(int64_t n, VecArgs<NIN, NOUT> a, Pro pro, F f, Epi epi, RedWorkspace ws, const int* __restrict__ skip) {
     constexpr int NR = NRED > 0 ? NRED : 1, NO = NOUT > 0 ? NOUT : 1;
     if (skip != nullptr && (kRunIf ? *skip == 0 : *skip != 0)) return;
@@ -181,36 +184,34 @@ vmap_kernel(int64_t n, VecArgs<NIN, NOUT> a, Pro pro, F f, Epi epi, RedWorkspace
 #pragma unroll
         for (int q = 0; q < NRED; ++q) acc[q] += red[q];
     };
+    // U pairs of every vector in flight per thread: 4 for one input (a copy-
+    // shaped step needs the bytes in flight: 2 pairs ran the GMRES basis
+    // scaling at 4.9 TB/s), 2 otherwise
+    constexpr int U = NIN <= 1 ? 4 : 2;
+    constexpr int NI = NIN > 0 ? NIN : 1;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * kRedThreads;
-    for (int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; k < np; k += 2 * T) {
-        const int64_t k1 = k + T;
-        const bool h1 = k1 < np;
-        double2 va[NIN > 0 ? NIN : 1], vb[NIN > 0 ? NIN : 1];
+    for (int64_t k = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; k < np; k += U * T) {
+        double2 v[U][NI];
 #pragma unroll
-        for (int q = 0; q < NIN; ++q) {
-            va[q] = reinterpret_cast<const double2*>(a.in[q])[k];
-            vb[q] = h1 ? reinterpret_cast<const double2*>(a.in[q])[k1] : make_double2(0.0, 0.0);
-        }
-        double i0[NIN > 0 ? NIN : 1], i1[NIN > 0 ? NIN : 1], o0[NO], o1[NO];
+        for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int q = 0; q < NIN; ++q) {
-            i0[q] = va[q].x;
-            i1[q] = va[q].y;
-        }
-        elem(i0, o0);
-        elem(i1, o1);
+            for (int q = 0; q < NIN; ++q)
+                v[u][q] = k + u * T < np ? reinterpret_cast<const double2*>(a.in[q])[k + u * T]
+                                         : make_double2(0.0, 0.0);
 #pragma unroll
-        for (int q = 0; q < NOUT; ++q) reinterpret_cast<double2*>(a.out[q])[k] = make_double2(o0[q], o1[q]);
-        if (h1) {
+        for (int u = 0; u < U; ++u) {
+            if (u > 0 && k + u * T >= np) break;
+            double i0[NI], i1[NI], o0[NO], o1[NO];
 #pragma unroll
             for (int q = 0; q < NIN; ++q) {
-                i0[q] = vb[q].x;
-                i1[q] = vb[q].y;
+                i0[q] = v[u][q].x;
+                i1[q] = v[u][q].y;
             }
             elem(i0, o0);
             elem(i1, o1);
 #pragma unroll
-            for (int q = 0; q < NOUT; ++q) reinterpret_cast<double2*>(a.out[q])[k1] = make_double2(o0[q], o1[q]);
+            for (int q = 0; q < NOUT; ++q)
+                reinterpret_cast<double2*>(a.out[q])[k + u * T] = make_double2(o0[q], o1[q]);
         }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {

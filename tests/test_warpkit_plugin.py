@@ -123,3 +123,29 @@ def test_plugin_breakdown_is_warpkit_breakdown(installed):
     m = CooMatrix.from_entries(2, 2, [0, 1], [0, 1], [-1.0, -2.0])
     with pytest.raises(warpkit.errors.BreakdownError):
         warpkit.dispatch("cg", warpkit.make_executor("b200"), coo_to_sellp(m, 2), np.ones(2), 1e-8, 10)
+
+
+@pytest.mark.gpu
+def test_reference_cli_strict_on_b200(installed, tmp_path):
+    """The reference's own command line (bench.py:434-500) with the b200
+    executor: --strict exits 0 only if every record validates against the
+    reference oracle, and results.csv carries the b200 rows."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import csv
+
+    from warpkit.bench import main
+    from warpkit.corpus import generate_corpus
+
+    corpus, out = tmp_path / "corpus", tmp_path / "out"
+    corpus.mkdir()
+    generate_corpus(corpus)
+    rc = main(["--corpus", str(corpus), "--out", str(out), "--execs", "ref,b200", "--kernels", "coo,csr,sellp,cg",
+               "--warmup", "1", "--iters", "2", "--strict"])
+    assert rc == 0
+    with open(out / "results.csv") as fh:
+        rows = list(csv.DictReader(fh))
+    b200 = [r for r in rows if r.get("exec") == "b200"]
+    assert b200 and {r["kernel"] for r in b200} == {"coo", "csr", "sellp", "cg"}
+    assert all(r["correct"] in ("True", "true", "1") for r in b200), [r for r in b200 if r["correct"] not in ("True", "true", "1")]
