@@ -240,7 +240,8 @@ int wk_gen_rmat_edges(int32_t scale, int32_t edge_factor, double a, double b, do
  * wk_sort_pairs_u64_f64: pass 1 counts the unique keys per 2048-key tile and
  * scans them (work: wk_coo_dedup_workspace(n) bytes; the unique count lands
  * at ((int64_t*)work)[wk_coo_dedup_tiles(n)]); pass 2 writes row = key / ncols,
- * col = key % ncols and value = 0.0 + v1 + v2 + ... in input order. */
+ * col = key % ncols and value = 0.0 + v1 + v2 + ... in input order. keys
+ * must be 16-byte aligned. */
 int64_t wk_coo_dedup_tiles(int64_t n);
 int64_t wk_coo_dedup_workspace(int64_t n);
 int wk_coo_dedup_count(int64_t n, const int64_t* keys, void* work, wk_stream_t stream);

@@ -219,6 +219,8 @@ int64_t wk_coo_dedup_workspace(int64_t n) { return (wk_coo_dedup_tiles(n) + 1) *
 
 int wk_coo_dedup_count(int64_t n, const int64_t* keys, void* work, wk_stream_t stream) {
     clear_error();
+    WK_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0 && (reinterpret_cast<uintptr_t>(work) & 7) == 0,
+               WK_ERR_INVALID, "dedup keys must be 16-byte aligned");
     cudaStream_t st = as_stream(stream);
     const int64_t nt = wk_coo_dedup_tiles(n);
     int64_t* tc = reinterpret_cast<int64_t*>(work);
@@ -233,6 +235,7 @@ int wk_coo_dedup_count(int64_t n, const int64_t* keys, void* work, wk_stream_t s
 int wk_coo_dedup_scatter(int64_t n, int64_t ncols, const int64_t* keys, const double* values, const void* work,
                          int32_t* row, int32_t* col, double* out_values, wk_stream_t stream) {
     clear_error();
+    WK_REQUIRE((reinterpret_cast<uintptr_t>(keys) & 15) == 0, WK_ERR_INVALID, "dedup keys must be 16-byte aligned");
     const int64_t nt = wk_coo_dedup_tiles(n);
     if (nt == 0) return 0;
     dedup_scatter_kernel<<<(unsigned)nt, kDdThreads, 0, as_stream(stream)>>>(
