@@ -323,7 +323,7 @@ hybrid_coo_fill_kernel(int64_t nrows, int64_t width, const int* __restrict__ ptr
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    constexpr int kU = 4;
+    constexpr int kU = 8;
     for (int64_t r0 = ((int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 32; r0 < nrows; r0 += warps * 32) {
         const int64_t r = r0 + lane;
         int lo = 0, cnt = 0;
@@ -396,7 +396,7 @@ hybrid_coo_long_kernel(int64_t width, const int* __restrict__ ptrs, const int* _
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const int64_t n = int64_t(*nseg);
-    constexpr int kU = 4;
+    constexpr int kU = 8;
     for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
         const int2 sg = segs[i];
         const int p0 = ptrs[sg.x], p1 = ptrs[sg.x + 1];
