@@ -64,3 +64,18 @@ def test_ell_and_csr_rowblock_spmv_have_no_atomics(sass):
 def test_coo_kernel_uses_atomics(sass):
     ks = _pick(sass, "seg8_kernelILb0E")
     assert any(ATOMIC.search(sass[k]) for k in ks)
+
+
+def test_radix_sort_downsweep_streams_with_tma(sass):
+    """The ingestion sort's downsweep stages its sub-tiles with cp.async.bulk
+    (UBLKCP) and ranks with ballots (VOTE), not match.any (MATCH)."""
+    (k,) = _pick(sass, "rs_downsweep")
+    assert "UBLKCP" in sass[k]
+    assert "VOTE" in sass[k] and "MATCH" not in sass[k]
+
+
+def test_csr_short_kernel_is_a_plain_fold(sass):
+    """config-1 CSR kernel: separately rounded fold, no atomics."""
+    (k,) = _pick(sass, "csr_short_kernel")
+    assert not ATOMIC.search(sass[k])
+    assert "DMUL" in sass[k] and "DADD" in sass[k] and "DFMA" not in sass[k]
