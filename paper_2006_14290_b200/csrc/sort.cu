@@ -92,20 +92,29 @@ rs_upsweep(int64_t n, const unsigned long long* __restrict__ keys, int shift, in
 constexpr int kRsStageBytes = kRsTile * 16;
 constexpr int kRsSmem = 2 * kRsStageBytes + 64;
 
-__global__ void __launch_bounds__(kRsThreads, 3)
+// The downsweep runs 512 threads (16 warps, 4 pairs each) on a 2048-pair
+// sub-tile: every serial phase of a sub-tile (the per-warp ranking chain, the
+// writes) is half as long as with 256 threads x 8 pairs, and two CTAs fit an
+// SM (32 warps instead of 24); the 256 digit-indexed steps use threads 0..255.
+constexpr int kDsThreads = 512;
+constexpr int kDsWarps = kDsThreads / 32;
+constexpr int kDsItems = kRsTile / kDsThreads;
+
+__global__ void __launch_bounds__(kDsThreads, 2)
 rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double* __restrict__ vin,
              unsigned long long* __restrict__ kout, double* __restrict__ vout, int shift, int64_t nchunks,
              const int64_t* __restrict__ offs) {
     extern __shared__ __align__(128) unsigned char rs_smem[];
     __shared__ int64_t base[kRsDigits];
-    __shared__ unsigned short wcnt[kRsWarps][kRsDigits];  // <= 256 per warp and digit
+    __shared__ unsigned short wcnt[kDsWarps][kRsDigits];  // <= 128 per warp and digit
     __shared__ unsigned dstart[kRsDigits];
     __shared__ unsigned dcount[kRsDigits];
-    __shared__ unsigned wsum[kRsWarps];
+    __shared__ unsigned wsum[kRsDigits / 32];
     uint64_t* full = reinterpret_cast<uint64_t*>(rs_smem + 2 * kRsStageBytes);
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const bool dig = t < kRsDigits;  // thread t owns digit t in the digit-indexed steps
     const unsigned lt = (1u << lane) - 1u;
-    base[t] = offs[int64_t(t) * nchunks + blockIdx.x];
+    if (dig) base[t] = offs[int64_t(t) * nchunks + blockIdx.x];
     const int64_t clo = int64_t(blockIdx.x) * kRsChunk;
     const int64_t chi = clo + kRsChunk < n ? clo + kRsChunk : n;
     const int ntile = int((chi - clo + kRsTile - 1) / kRsTile);
@@ -129,6 +138,7 @@ rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double
         }
     };
     if (t == 0) issue(0);
+    unsigned short* wflat = &wcnt[0][0];
     for (int it = 0; it < ntile; ++it) {
         const int64_t s0 = clo + int64_t(it) * kRsTile;
         const int cnt = int(chi - s0 < kRsTile ? chi - s0 : kRsTile);
@@ -136,26 +146,26 @@ rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double
         double* sv = reinterpret_cast<double*>(rs_smem + (it & 1) * kRsStageBytes + kRsTile * 8);
         if (t == 0 && it + 1 < ntile) issue(it + 1);  // the other stage was released at the end of it - 1
 #pragma unroll
-        for (int q = 0; q < kRsWarps; ++q) wcnt[q][t] = 0;
+        for (int q = 0; q < kDsWarps * kRsDigits / kDsThreads; ++q) wflat[q * kDsThreads + t] = 0;
         mbar_wait(full + (it & 1), uint32_t((it >> 1) & 1));
         if ((cnt & 1) && t == 0) {  // odd tail pair: not part of the bulk copy
             sk[cnt - 1] = kin[s0 + cnt - 1];
             sv[cnt - 1] = vin[s0 + cnt - 1];
         }
         __syncthreads();
-        unsigned long long k[kRsItems];
-        double v[kRsItems];
-        unsigned d[kRsItems];  // digit (256: no pair), then | rank << 9
+        unsigned long long k[kDsItems];
+        double v[kDsItems];
+        unsigned d[kDsItems];  // digit (256: no pair), then | rank << 9
 #pragma unroll
-        for (int j = 0; j < kRsItems; ++j) {
-            const int li = w * 256 + j * 32 + lane;
+        for (int j = 0; j < kDsItems; ++j) {
+            const int li = w * (32 * kDsItems) + j * 32 + lane;
             const bool ok = li < cnt;
             k[j] = ok ? sk[li] : 0ull;
             v[j] = ok ? sv[li] : 0.0;
             d[j] = ok ? unsigned(k[j] >> shift) & 255u : 256u;
         }
 #pragma unroll
-        for (int j = 0; j < kRsItems; ++j) {
+        for (int j = 0; j < kDsItems; ++j) {
             const unsigned dj = d[j];
             const unsigned peers = digit_peers(dj & 255u, dj < 256u);
             const unsigned before = dj < 256u ? wcnt[w][dj] : 0u;
@@ -165,30 +175,33 @@ rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double
             __syncwarp();
         }
         __syncthreads();  // every pair of the stage is in registers: the stage becomes the reorder buffer
-        // thread t = digit t: exclusive prefix over the warps, total count
-        unsigned run = 0;
+        // digit t: exclusive prefix over the warps, total count, block scan of the totals
+        unsigned run = 0, incl = 0;
+        if (dig) {
 #pragma unroll
-        for (int q = 0; q < kRsWarps; ++q) {
-            const unsigned c = wcnt[q][t];
-            wcnt[q][t] = (unsigned short)run;  // < 2048: the sub-tile offset of warp q's first pair
-            run += c;
+            for (int q = 0; q < kDsWarps; ++q) {
+                const unsigned c = wcnt[q][t];
+                wcnt[q][t] = (unsigned short)run;  // < 2048: the sub-tile offset of warp q's first pair
+                run += c;
+            }
+            dcount[t] = run;
+            incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsum[w] = incl;
         }
-        dcount[t] = run;
-        // block exclusive scan of the 256 digit totals
-        unsigned incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+        __syncthreads();
+        if (dig) {
+            unsigned wpre = 0;
+            for (int q = 0; q < w; ++q) wpre += wsum[q];
+            dstart[t] = wpre + incl - run;
         }
-        if (lane == 31) wsum[w] = incl;
-        __syncthreads();
-        unsigned wpre = 0;
-        for (int q = 0; q < w; ++q) wpre += wsum[q];
-        dstart[t] = wpre + incl - run;
         __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kRsItems; ++j) {
+        for (int j = 0; j < kDsItems; ++j) {
             const unsigned dj = d[j] & 511u;
             if (dj < 256u) {
                 const unsigned pos = dstart[dj] + wcnt[w][dj] + (d[j] >> 9);
@@ -197,7 +210,7 @@ rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double
             }
         }
         __syncthreads();
-        for (int i = t; i < cnt; i += kRsThreads) {
+        for (int i = t; i < cnt; i += kDsThreads) {
             const unsigned long long key = sk[i];
             const unsigned dd = unsigned(key >> shift) & 255u;
             const int64_t dst = base[dd] + (i - int(dstart[dd]));
@@ -206,7 +219,7 @@ rs_downsweep(int64_t n, const unsigned long long* __restrict__ kin, const double
         }
         __syncthreads();  // stage free: the next iteration's bulk copy may overwrite it
         if (t == 0) fence_proxy_async_smem();
-        base[t] += dcount[t];
+        if (dig) base[t] += dcount[t];
     }
 }
 
@@ -259,7 +272,7 @@ int wk_sort_pairs_u64_f64(int64_t n, int32_t key_bits, uint64_t* keys, double* v
         WK_LAUNCH_CHECK();
         const unsigned* c = counts;
         WK_TRY(exclusive_scan(m, [=] __device__(int64_t i) { return int64_t(c[i]); }, offs, scan_ws, st));
-        rs_downsweep<<<unsigned(nchunks), kRsThreads, kRsSmem, st>>>(n, ka, va, kb, vb, shift, nchunks, offs);
+        rs_downsweep<<<unsigned(nchunks), kDsThreads, kRsSmem, st>>>(n, ka, va, kb, vb, shift, nchunks, offs);
         WK_LAUNCH_CHECK();
         unsigned long long* tk = ka;
         ka = kb;
