@@ -526,7 +526,7 @@ def bench_formats(args, wk, corpus, D, A_csr, A_sellp, x, peak):
         ms = statistics.mean(per)
         b = d.algorithmic_bytes()
         nz = d.nnz if nnz is None else nnz
-        res[name] = {"ms": round(ms, 4), "GFLOP/s": round(2 * nz / (ms * 1e-3) / 1e9, 2),
+        res[name] = {"ms": round(ms, 4), "min_ms": round(min(per), 4), "GFLOP/s": round(2 * nz / (ms * 1e-3) / 1e9, 2),
                      "GB/s": round(b / (ms * 1e-3) / 1e9, 1), "frac_hbm": round(b / (ms * 1e-3) / 1e9 / peak, 4),
                      "bytes": int(b), "nnz": int(nz)}
         if flush_l2:
