@@ -267,22 +267,55 @@ int64_t csr_stream_chunks(int64_t nnz) {
 // lanes strides the row, butterfly reduction, rank 0 writes. T == 1 is the
 // sequential thread-per-row fold (bitwise).
 // ---------------------------------------------------------------------------
+// kRows rows per tile in flight: the row bounds, then the first entries'
+// values / columns, then the gathers of all kRows rows are issued before any
+// fold (one row at a time left the kernel at three dependent round trips per
+// row: 1.24 ms, 0.33 of the copy peak, on the 27-point operator; 4 rows: 1.06
+// ms; 8 rows: 1.54 ms, fewer resident warps). Per row the
+// arithmetic is unchanged: lane l folds entries lo + l, lo + l + T, ... in
+// order, then the butterfly.
 template <unsigned T>
 __global__ void __launch_bounds__(kSpmvThreads)
 csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __restrict__ col,
                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
                    const int* __restrict__ skip) {
+    constexpr int kRows = 4;
     if (skip != nullptr && *skip) return;
     auto tile = cg::tiled_partition<T>(cg::this_thread_block());
     const int64_t tiles_per_grid = int64_t(gridDim.x) * (kSpmvThreads / T);
-    for (int64_t row = int64_t(blockIdx.x) * (kSpmvThreads / T) + tile.meta_group_rank(); row < nrows;
-         row += tiles_per_grid) {
-        const int64_t lo = ptrs[row], hi = ptrs[row + 1];
-        double acc = 0.0;
-        for (int64_t k = lo + tile.thread_rank(); k < hi; k += T)
-            acc = mul_add_rn(acc, ld_stream(val + k), ld_x(x, ld_stream(col + k)));
-        acc = reduce_subwarp(tile, acc);
-        if (tile.thread_rank() == 0) y[row] = acc;
+    const int tr = int(tile.thread_rank());
+    for (int64_t row0 = int64_t(blockIdx.x) * (kSpmvThreads / T) + tile.meta_group_rank(); row0 < nrows;
+         row0 += kRows * tiles_per_grid) {
+        int64_t lo[kRows], hi[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const int64_t row = row0 + u * tiles_per_grid;
+            lo[u] = row < nrows ? ptrs[row] : 0;
+            hi[u] = row < nrows ? ptrs[row + 1] : 0;
+        }
+        double acc[kRows], v0[kRows], x0[kRows];
+        int c0[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const int64_t k = lo[u] + tr;
+            c0[u] = k < hi[u] ? ld_stream(col + k) : 0;
+            v0[u] = k < hi[u] ? ld_stream(val + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) x0[u] = lo[u] + tr < hi[u] ? ld_x(x, c0[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            acc[u] = 0.0;
+            if (lo[u] + tr < hi[u]) acc[u] = mul_add_rn(0.0, v0[u], x0[u]);
+            for (int64_t k = lo[u] + tr + T; k < hi[u]; k += T)
+                acc[u] = mul_add_rn(acc[u], ld_stream(val + k), ld_x(x, ld_stream(col + k)));
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+            const double r = reduce_subwarp(tile, acc[u]);
+            const int64_t row = row0 + u * tiles_per_grid;
+            if (tr == 0 && row < nrows) y[row] = r;
+        }
     }
 }
 
