@@ -291,6 +291,8 @@ typedef struct wk_cg_state {
     int64_t max_iters;
     int32_t done;      /* converged / max_iters reached / breakdown          */
     int32_t breakdown;
+    int32_t xpend;     /* wk_cg_solve: x += alpha p of the last r update pending */
+    int32_t pad;
 } wk_cg_state;
 
 /* rho := b.b (local), x = 0, r = p = b */

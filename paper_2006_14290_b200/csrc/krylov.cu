@@ -37,6 +37,7 @@ static int cg_init_local(int64_t n, const double* b, double* x, double* r, doubl
             s->iteration = 0;
             s->done = 0;
             s->breakdown = 0;
+            s->xpend = 0;
         }, st);
     }
     return launch_map_reduce(
@@ -53,6 +54,7 @@ static int cg_init_local(int64_t n, const double* b, double* x, double* r, doubl
             s->iteration = 0;
             s->done = 0;
             s->breakdown = 0;
+            s->xpend = 0;
         },
         ws, nullptr, st);
 }
@@ -291,6 +293,110 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
     }
 }
 
+// Single-GPU CG iteration in two vector passes instead of three (the
+// non-replacement iterations of wk_cg_solve's graph). The reference updates x
+// then r (kernels.py:320-325) and then p (329); the three updates are
+// element-wise and independent of each other's order, so x can wait for the
+// p pass, which reads p_old anyway:
+//   cg_update_r_vec   r -= alpha q, r.r (beta step in the last block); marks
+//                     the x update of this iteration pending (xpend)
+//   cg_update_xp_vec  x += alpha p_old and, unless the beta step ended the
+//                     solve, p = r + beta p_old; the last block clears xpend
+// 8 vector passes per iteration instead of 9 (p is read once less), every
+// element bitwise as before. Residual-replacement iterations need the new x
+// before the next r, so they keep cg_update_xr_vec + cg_update_p_vec.
+__global__ void __launch_bounds__(256)
+cg_update_r_vec(int64_t n, const double* __restrict__ q, double* __restrict__ r, wk_cg_state* s, double* hist,
+                RedWorkspace ws, int rev) {
+    if (s->done) return;
+    const double alpha = s->alpha;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    double acc = 0.0;
+    constexpr int U = 4;
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += U * T) {
+        double2 qa[U], ra[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            qa[u] = ku < np ? __ldcs(q2 + k) : make_double2(0.0, 0.0);
+            ra[u] = ku < np ? __ldcs(r2 + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            if (ku >= np) break;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            ra[u].x = __dadd_rn(ra[u].x, -__dmul_rn(alpha, qa[u].x));
+            ra[u].y = __dadd_rn(ra[u].y, -__dmul_rn(alpha, qa[u].y));
+            r2[k] = ra[u];  // read next by the x/p pass, which starts on these rows
+            acc += __dmul_rn(ra[u].x, ra[u].x);
+            acc += __dmul_rn(ra[u].y, ra[u].y);
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = n - 1;
+        r[i] = __dadd_rn(r[i], -__dmul_rn(alpha, q[i]));
+        acc += __dmul_rn(r[i], r[i]);
+    }
+    double total;
+    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0) {
+        s->rr = total;
+        cg_beta_step(s, hist);
+        s->xpend = 1;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+cg_update_xp_vec(int64_t n, const double* __restrict__ r, double* __restrict__ x, double* __restrict__ p,
+                 wk_cg_state* s, RedWorkspace ws, int rev) {
+    if (!s->xpend) return;
+    const double alpha = s->alpha, beta = s->beta;
+    const bool upd_p = !s->done;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    constexpr int U = 2;
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += U * T) {
+        double2 pa[U], xa[U], ra[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            const bool ok = ku < np;
+            pa[u] = ok ? p2[k] : make_double2(0.0, 0.0);
+            xa[u] = ok ? __ldcs(x2 + k) : make_double2(0.0, 0.0);
+            ra[u] = ok && upd_p ? __ldcs(r2 + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            if (ku >= np) break;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            xa[u].x = __dadd_rn(xa[u].x, __dmul_rn(alpha, pa[u].x));
+            xa[u].y = __dadd_rn(xa[u].y, __dmul_rn(alpha, pa[u].y));
+            __stcs(x2 + k, xa[u]);
+            if (upd_p) {
+                double2 q;
+                q.x = __dadd_rn(ra[u].x, __dmul_rn(beta, pa[u].x));
+                q.y = __dadd_rn(ra[u].y, __dmul_rn(beta, pa[u].y));
+                p2[k] = q;
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = n - 1;
+        const double pi = p[i];
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+        if (upd_p) p[i] = __dadd_rn(r[i], __dmul_rn(beta, pi));
+    }
+    double total;
+    if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) s->xpend = 0;  // every block has read it
+}
+
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
                         double* hist, void* ws, bool finalize, cudaStream_t st, int rev = 0) {
     if (n > 0 && vec_ok(p, q, x, r)) {
@@ -517,10 +623,20 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     // recently written q / r / p are still in the 126 MB L2). Iteration i:
     // SpMV d, x/r update !d, p update d, with d flipping every iteration (the
     // 50-iteration period is even).
+    // the two-pass iteration (cg_update_r_vec / cg_update_xp_vec) for every
+    // iteration but the residual replacement, when the vectors are aligned
+    const bool two_pass = n > 0 && vec_ok(p, q, x, r) && vec_grid(n) <= kRedMaxBlocks;
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kReplaceEvery; ++i) {
             const int d = i & 1;
             WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs, nullptr, nullptr, d));
+            if (two_pass && i < kReplaceEvery - 1) {
+                cg_update_r_vec<<<vec_grid(n), 256, 0, cs>>>(n, q, r, s, hist, red_ws(red), 1 - d);
+                WK_LAUNCH_CHECK();
+                cg_update_xp_vec<<<vec_grid(n), 256, 0, cs>>>(n, r, x, p, s, red_ws(red), d);
+                WK_LAUNCH_CHECK();
+                continue;
+            }
             WK_TRY(cg_update_xr(n, p, q, x, r, s, hist, red, true, cs, 1 - d));
             if (i == kReplaceEvery - 1) {
                 WK_TRY(wk_spmv_masked(A, x, q, &s->done, cs));
