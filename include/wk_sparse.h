@@ -336,6 +336,7 @@ int wk_cg_update_p(int64_t n, const double* r, double* p, const wk_cg_state* sta
 typedef struct wk_bicg_state {
     double rho, rho_new, alpha, omega, beta, threshold;
     double rv, ss, tt, ts, rr; /* local partials: all-reduce rho_new, rv, ss, {tt,ts}, rr */
+    double rho_next;           /* wk_bicgstab_solve: rh.r of the new r, fused into the x/r step */
     int64_t iteration, max_iters;
     int32_t done, breakdown, apply_half, pad;
 } wk_bicg_state;

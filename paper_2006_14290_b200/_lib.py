@@ -78,7 +78,7 @@ class WkCgState(ctypes.Structure):
 
 class WkBicgState(ctypes.Structure):
     _fields_ = [(n, F64) for n in ("rho", "rho_new", "alpha", "omega", "beta", "threshold", "rv", "ss", "tt", "ts",
-                                   "rr")] + [("iteration", I64), ("max_iters", I64), ("done", I32),
+                                   "rr", "rho_next")] + [("iteration", I64), ("max_iters", I64), ("done", I32),
                                              ("breakdown", I32), ("apply_half", I32), ("pad", I32)]
 
 

@@ -48,4 +48,15 @@ struct DotEpilogue {
     const PeerHalo* halo;  // non-null: wait for the pushed halo of x before the first gather
 };
 
+// Epilogue of an SpMV with BiCGSTAB's dots fused (wk_bicgstab_solve):
+// mode 1 (v = A p): rv = sum w[r] * y[r] with w = r-hat;
+// mode 2 (t = A s): tt = sum y[r]^2, ts = sum y[r] * x[r] (x = s).
+struct BicgEpilogue {
+    double* partials;
+    unsigned* ticket;
+    wk_bicg_state* state;
+    const double* w;
+    int mode;
+};
+
 }  // namespace wk

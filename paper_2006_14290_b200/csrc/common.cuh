@@ -66,6 +66,11 @@ int sm_count();
 int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* s, void* red_ws, int finalize,
                    cudaStream_t st, void* peer = nullptr, const void* halo = nullptr, int rev = 0);
 
+// BiCGSTAB SpMV with its dot(s) fused: mode 1 rv = w.y, mode 2 tt = y.y, ts =
+// y.x (spmv.cu); returns 1 if A cannot take the fused path.
+int spmv_bicg_fused(const wk_matrix* A, const double* x, double* y, wk_bicg_state* s, const double* w, int mode,
+                    void* red_ws, cudaStream_t st);
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---- device helpers ------------------------------------------------------------

@@ -248,6 +248,44 @@ static int bicg_update_xr(int64_t n, const double* p, const double* sv, const do
         [=] __device__(double tot) { s->rr = tot; }, ws, &s->done, st);
 }
 
+// wk_bicgstab_solve's fused variant of bicg_update_xr + the next iteration's
+// bicg_rho: the new r is in registers, so rh.r (rho_new of the next
+// iteration) is summed in the same pass (one read of rh instead of a pass
+// over rh and r). Same vmap traversal and grid as bicg_rho: the sum is
+// bitwise the one bicg_rho would return.
+static int bicg_update_xr_rho(int64_t n, const double* p, const double* sv, const double* t, const double* rh,
+                              double* x, double* r, BS* s, void* ws, cudaStream_t st) {
+    return launch_vmap<5, 2, 2>(
+        n, VecArgs<5, 2>{{x, p, sv, t, rh}, {x, r}}, [=] __device__() { return make_double2(s->alpha, s->omega); },
+        [] __device__(double2 c, const double(&in)[5], double(&out)[2], double(&red)[2]) {
+            out[0] = __dadd_rn(__dadd_rn(in[0], __dmul_rn(c.x, in[1])), __dmul_rn(c.y, in[2]));
+            const double ri = __dadd_rn(in[2], -__dmul_rn(c.y, in[3]));
+            out[1] = ri;
+            red[0] = __dmul_rn(ri, ri);
+            red[1] = __dmul_rn(in[4], ri);
+        },
+        [=] __device__(double(&tot)[2]) {
+            s->rr = tot[0];
+            s->rho_next = tot[1];
+        },
+        ws, &s->done, st);
+}
+
+// rho_new of the coming iteration from the previous fused x/r step (or from
+// bicg_rho_first before the first iteration)
+static int bicg_take_rho(BS* s, cudaStream_t st) {
+    return launch_scalar([=] __device__() {
+        if (!s->done) s->rho_new = s->rho_next;
+    }, st);
+}
+
+static int bicg_rho_first(int64_t n, const double* rh, const double* r, BS* s, void* ws, cudaStream_t st) {
+    return launch_vmap<2, 0, 1>(
+        n, VecArgs<2, 0>{{rh, r}, {nullptr}}, NoScalars{},
+        [] __device__(int, const double(&in)[2], double(&)[1], double(&red)[1]) { red[0] = __dmul_rn(in[0], in[1]); },
+        [=] __device__(double(&t)[1]) { s->rho_next = t[0]; }, ws, &s->done, st);
+}
+
 static int bicg_step_r(BS* s, double* hist, cudaStream_t st) {
     return launch_scalar([=] __device__() {
         if (s->done) return;
@@ -751,21 +789,37 @@ int wk_bicgstab_solve(const wk_matrix* A, const double* b, double tol, int64_t m
     WK_TRY(bicg_init_finish(s, tol, max_iters, hist, st));
     const int* done = &s->done;
     constexpr int kChunk = 10;
+    // fused rho (rh.r summed in the x/r step of the previous iteration) when
+    // every vector is 16-byte aligned
+    const bool fused = n > 0 && vmap_ok({b, x, r, rh, p, v, sv, t});
+    if (fused) WK_TRY(bicg_rho_first(n, rh, r, s, red, st));
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kChunk; ++i) {
-            WK_TRY(bicg_rho(n, rh, r, s, red, cs));
+            if (fused)
+                WK_TRY(bicg_take_rho(s, cs));
+            else
+                WK_TRY(bicg_rho(n, rh, r, s, red, cs));
             WK_TRY(bicg_step_beta(s, cs));
             WK_TRY(bicg_update_p(n, r, v, p, s, cs));
-            WK_TRY(wk_spmv_masked(A, p, v, done, cs));
-            WK_TRY(bicg_rv(n, rh, v, s, red, cs));
+            // v = A p with rv = r-hat.v fused into the SpMV when it can take it
+            if (!fused || spmv_bicg_fused(A, p, v, s, rh, 1, red, cs) != 0) {
+                WK_TRY(wk_spmv_masked(A, p, v, done, cs));
+                WK_TRY(bicg_rv(n, rh, v, s, red, cs));
+            }
             WK_TRY(bicg_step_alpha(s, cs));
             WK_TRY(bicg_update_s(n, r, v, sv, s, red, cs));
             WK_TRY(bicg_step_s(s, hist, cs));
             WK_TRY(bicg_half_x(n, p, x, s, red, cs));
-            WK_TRY(wk_spmv_masked(A, sv, t, done, cs));
-            WK_TRY(bicg_tt_ts(n, t, sv, s, red, cs));
+            // t = A s with t.t and t.s fused into the SpMV when it can take them
+            if (!fused || spmv_bicg_fused(A, sv, t, s, nullptr, 2, red, cs) != 0) {
+                WK_TRY(wk_spmv_masked(A, sv, t, done, cs));
+                WK_TRY(bicg_tt_ts(n, t, sv, s, red, cs));
+            }
             WK_TRY(bicg_step_omega(s, cs));
-            WK_TRY(bicg_update_xr(n, p, sv, t, x, r, s, red, cs));
+            if (fused)
+                WK_TRY(bicg_update_xr_rho(n, p, sv, t, rh, x, r, s, red, cs));
+            else
+                WK_TRY(bicg_update_xr(n, p, sv, t, x, r, s, red, cs));
             WK_TRY(bicg_step_r(s, hist, cs));
         }
         return 0;

@@ -67,6 +67,38 @@ __device__ __forceinline__ bool grid_reduce_last(double v, RedWorkspace ws, doub
     return true;
 }
 
+// Two values, any block size: partial slot v of block b at partials[v *
+// kRedMaxBlocks + b]; returns true in the last-arriving block (thread 0 holds
+// both grid totals).
+template <int kThreads>
+__device__ __forceinline__ bool grid_reduce_last2(double v0, double v1, RedWorkspace ws, double& t0, double& t1) {
+    __shared__ double red[kThreads / 32];
+    __shared__ bool is_last;
+    const double b0 = block_sum<kThreads>(v0, red);
+    __syncthreads();  // `red` reuse
+    const double b1 = block_sum<kThreads>(v1, red);
+    if (threadIdx.x == 0) {
+        ws.partials[blockIdx.x] = b0;
+        ws.partials[kRedMaxBlocks + blockIdx.x] = b1;
+        __threadfence();
+        is_last = atomicAdd(ws.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return false;
+    __threadfence();
+    double a0 = 0.0, a1 = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += kThreads) {
+        a0 += __ldcg(ws.partials + b);
+        a1 += __ldcg(ws.partials + kRedMaxBlocks + b);
+    }
+    __syncthreads();
+    t0 = block_sum<kThreads>(a0, red);
+    __syncthreads();
+    t1 = block_sum<kThreads>(a1, red);
+    if (threadIdx.x == 0) *ws.ticket = 0;
+    return true;
+}
+
 // N-value variant: f(i, acc) adds into acc[0..N-1]; partial slot v of block b
 // lives at partials[v * kRedMaxBlocks + b]. Returns true in the last block,
 // where total[] (thread 0) holds the grid totals.

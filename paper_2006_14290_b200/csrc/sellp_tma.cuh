@@ -101,12 +101,13 @@ __device__ __forceinline__ void sellp_chunk_fold(const SellpChunkRegs<J>& c, int
 // kDot: also accumulate sum_r x[r] * y[r] over the owned rows (CG's p.Ap with
 // x = p, y = q) and publish it through DotEpilogue (last-arriving CTA).
 // kCoh: coherent x gathers (peer CG: the halo of x lands during the kernel).
-template <class Cfg, bool kDot = false, bool kCoh = false>
+// kBicg (BiCGSTAB, BicgEpilogue): 1 = r-hat.y, 2 = (y.y, y.x) over the rows.
+template <class Cfg, bool kDot = false, bool kCoh = false, int kBicg = 0>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, Cfg::kCtas)
 sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t* __restrict__ sets,
                    const int* __restrict__ col, const double* __restrict__ val, const int* __restrict__ row_lengths,
                    const double* __restrict__ x, double* __restrict__ y, const int* __restrict__ skip,
-                   DotEpilogue dot, int rev = 0) {
+                   DotEpilogue dot, int rev = 0, BicgEpilogue bep = BicgEpilogue{nullptr, nullptr, nullptr, nullptr, 0}) {
     constexpr int J = Cfg::kJ, S = Cfg::kS, WARPS = Cfg::kWarps, CH = Cfg::kChunk;
     if (skip != nullptr && *skip) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -218,7 +219,7 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
             cphase ^= 1u;
         }
     };
-    double dacc = 0.0;
+    double dacc = 0.0, bacc0 = 0.0, bacc1 = 0.0;
     // kDot: x at the slice's own rows (CG: p[r]), read after the fold (L1/L2
     // hits: the same lines were just gathered)
     auto xown = [&](int64_t r0) -> double2 {
@@ -230,6 +231,26 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
     // one wrote last (ping-pong): plain stores keep q's tail in L2 instead of
     // the evict-first streaming stores of the SpMV
     auto emit = [&](int64_t r0, double a0, double a1, double2 p) {
+        if (kBicg == 1) {  // r-hat at the own rows
+            if (r0 + 1 < nrows) {
+                const double2 w = *reinterpret_cast<const double2*>(bep.w + r0);
+                bacc0 += __dmul_rn(w.x, a0);
+                bacc0 += __dmul_rn(w.y, a1);
+            } else if (r0 < nrows) {
+                bacc0 += __dmul_rn(bep.w[r0], a0);
+            }
+        } else if (kBicg == 2) {  // t.t and t.s (s = x at the own rows)
+            if (r0 + 1 < nrows) {
+                const double2 s2 = *reinterpret_cast<const double2*>(x + r0);
+                bacc0 += __dmul_rn(a0, a0);
+                bacc0 += __dmul_rn(a1, a1);
+                bacc1 += __dmul_rn(a0, s2.x);
+                bacc1 += __dmul_rn(a1, s2.y);
+            } else if (r0 < nrows) {
+                bacc0 += __dmul_rn(a0, a0);
+                bacc1 += __dmul_rn(a0, x[r0]);
+            }
+        }
         if (r0 + 1 < nrows) {
             if (kDot)
                 *reinterpret_cast<double2*>(y + r0) = make_double2(a0, a1);
@@ -320,6 +341,18 @@ sellp64_tma_kernel(int64_t nrows, int64_t ncols, int64_t nslices, const int64_t*
         }
     }
 done:
+    if (kBicg != 0) {
+        RedWorkspace ws{bep.partials, bep.ticket};
+        double t0, t1;
+        if (grid_reduce_last2<WARPS * 32>(bacc0, bacc1, ws, t0, t1) && threadIdx.x == 0) {
+            if (kBicg == 1) {
+                bep.state->rv = t0;
+            } else {
+                bep.state->tt = t0;
+                bep.state->ts = t1;
+            }
+        }
+    }
     if (kDot) {
         RedWorkspace ws{dot.partials, dot.ticket};
         double total;
@@ -335,24 +368,25 @@ done:
 }
 
 // Launch one configuration (persistent grid: one CTA per SM).
-template <class Cfg, bool kDot = false, bool kCoh = false>
+template <class Cfg, bool kDot = false, bool kCoh = false, int kBicg = 0>
 int launch_sellp64_tma(int64_t nrows, int64_t ncols, const int64_t* sets, const int* col, const double* val,
                        const int* row_lengths, const double* x, double* y, const int* skip, cudaStream_t st,
-                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int rev = 0) {
+                       DotEpilogue dot = DotEpilogue{nullptr, nullptr, nullptr, 0, nullptr, nullptr}, int rev = 0,
+                       BicgEpilogue bep = BicgEpilogue{nullptr, nullptr, nullptr, nullptr, 0}) {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot, kCoh>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(Cfg::kSmem)));
+        WK_CUDA(cudaFuncSetAttribute(sellp64_tma_kernel<Cfg, kDot, kCoh, kBicg>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
     const int64_t nslices = ceil_div(nrows, 64);
     int64_t grid = int64_t(sm_count()) * Cfg::kCtas;
     const int64_t need = ceil_div(nslices, Cfg::kWarps);
     if (grid > need) grid = need;
-    sellp64_tma_kernel<Cfg, kDot, kCoh><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
-        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, rev);
+    sellp64_tma_kernel<Cfg, kDot, kCoh, kBicg><<<(unsigned)grid, Cfg::kWarps * 32, Cfg::kSmem, st>>>(
+        nrows, ncols, nslices, sets, col, val, row_lengths, x, y, skip, dot, rev, bep);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -205,6 +205,36 @@ int spmv_dot_fused(const wk_matrix* A, const double* p, double* q, wk_cg_state* 
                                                A->row_lengths, p, q, &s->done, st, dot, rev);
 }
 
+// BiCGSTAB's SpMVs with their dots fused (wk_bicgstab_solve): mode 1
+// (v = A p): state->rv = r-hat.v; mode 2 (t = A s): state->tt = t.t,
+// state->ts = t.s. SELL-P(64), 16-byte aligned only; returns 1 otherwise (the
+// caller runs the SpMV and the dot pass separately).
+int spmv_bicg_fused(const wk_matrix* A, const double* xin, double* y, wk_bicg_state* s, const double* w, int mode,
+                    void* red_ws, cudaStream_t st) {
+    if (A->format != WK_FMT_SELLP || A->slice_size != 64 || A->nrows == 0 || !aligned(A->values, 16) ||
+        !aligned(A->col_idx, 16) || !aligned(y, 16) || !aligned(xin, 16) || (mode == 1 && !aligned(w, 16)))
+        return 1;
+    char* wb = reinterpret_cast<char*>(red_ws);
+    BicgEpilogue bep{reinterpret_cast<double*>(wb),
+                     reinterpret_cast<unsigned*>(wb + sizeof(double) * kRedMaxVec * kRedMaxBlocks), s, w, mode};
+    const DotEpilogue none{nullptr, nullptr, nullptr, 0, nullptr, nullptr};
+    const bool narrow = sellp_narrow(A->nrows, A->nnz);
+    if (mode == 1) {
+        if (narrow)
+            return launch_sellp64_tma<SellpNarrow, false, false, 1>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
+                                                                   A->values, A->row_lengths, xin, y, &s->done, st,
+                                                                   none, 0, bep);
+        return launch_sellp64_tma<SellpWide, false, false, 1>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
+                                                             A->row_lengths, xin, y, &s->done, st, none, 0, bep);
+    }
+    if (narrow)
+        return launch_sellp64_tma<SellpNarrow, false, false, 2>(A->nrows, A->ncols, A->slice_sets, A->col_idx,
+                                                               A->values, A->row_lengths, xin, y, &s->done, st, none,
+                                                               0, bep);
+    return launch_sellp64_tma<SellpWide, false, false, 2>(A->nrows, A->ncols, A->slice_sets, A->col_idx, A->values,
+                                                         A->row_lengths, xin, y, &s->done, st, none, 0, bep);
+}
+
 int launch_ell(int64_t nrows, int64_t ncols, int64_t width, int64_t stride, const int* col,
                const double* val, const int* row_lengths, const double* x, double* y, const int* skip,
                cudaStream_t st) {
