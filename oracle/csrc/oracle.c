@@ -442,3 +442,111 @@ void or_sellp_fill(int64_t nrows, int64_t ss, const int64_t* ptrs, const int32_t
             }
     }
 }
+
+/* ---- R-MAT ingestion (BASELINE config 3) ------------------------------------
+ * corpus_ref.splitmix64 / uniform / rmat_edges / coo_from_entries restated so
+ * the whole scale-24 pipeline (268M raw edges -> sorted, duplicate-summed COO)
+ * can be checked entry for entry against the device generator, the device
+ * radix sort and the device dedup at full size. */
+
+static inline uint64_t or_splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static inline double or_uniform(uint64_t seed, uint64_t ctr) {
+    return (double)(or_splitmix64(seed * 0xD1B54A32D192ED03ull + ctr) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+/* corpus_ref.rmat_edges for edges [edge_lo, edge_hi): key = row * 2^scale + col */
+void or_rmat_keys(int scale, double a, double b, double c, uint64_t seed, int64_t edge_lo, int64_t edge_hi,
+                  int64_t* keys, double* vals, int nthreads) {
+    set_threads(nthreads);
+    const double ab = a + b, abc = a + b + c;
+    const uint64_t L = (uint64_t)scale + 1;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = edge_lo; e < edge_hi; ++e) {
+        int64_t row = 0, col = 0;
+        for (int l = 0; l < scale; ++l) {
+            double u = or_uniform(seed, (uint64_t)e * L + (uint64_t)l);
+            int64_t bit = (int64_t)1 << (scale - 1 - l);
+            if (u >= ab) row |= bit;
+            if ((u >= a && u < ab) || u >= abc) col |= bit;
+        }
+        keys[e - edge_lo] = (row << scale) | col;
+        vals[e - edge_lo] = or_uniform(seed, (uint64_t)e * L + (uint64_t)scale);
+    }
+}
+
+/* Stable LSD radix sort of (key, value) pairs on the low `key_bits` bits,
+ * 8-bit digits. Thread t owns the contiguous block [n t / T, n (t+1) / T);
+ * bucket offsets are laid out digit-major, thread-minor, so equal keys keep
+ * their input order (np.lexsort is stable). The result ends in keys/vals. */
+void or_sort_pairs(int64_t n, int key_bits, int64_t* keys, double* vals, int64_t* keys_alt,
+                   double* vals_alt, int nthreads) {
+    set_threads(nthreads);
+    int64_t* cnt = (int64_t*)malloc(sizeof(int64_t) * 256 * OR_MAX_THREADS);
+    int64_t *ks = keys, *kd = keys_alt;
+    double *vs = vals, *vd = vals_alt;
+    for (int shift = 0; shift < key_bits; shift += 8) {
+#pragma omp parallel
+        {
+            int nt = 1, t = 0;
+#ifdef _OPENMP
+            nt = omp_get_num_threads();
+            t = omp_get_thread_num();
+#endif
+            if (nt > OR_MAX_THREADS) nt = OR_MAX_THREADS;
+            const int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+            int64_t* mine = cnt + 256 * (int64_t)t;
+            if (t < nt) {
+                memset(mine, 0, sizeof(int64_t) * 256);
+                for (int64_t i = lo; i < hi; ++i) ++mine[((uint64_t)ks[i] >> shift) & 255];
+            }
+#pragma omp barrier
+#pragma omp single
+            {
+                int64_t run = 0;
+                for (int d = 0; d < 256; ++d)
+                    for (int u = 0; u < nt; ++u) {
+                        int64_t v = cnt[256 * (int64_t)u + d];
+                        cnt[256 * (int64_t)u + d] = run;
+                        run += v;
+                    }
+            }
+            if (t < nt)
+                for (int64_t i = lo; i < hi; ++i) {
+                    int64_t p = mine[((uint64_t)ks[i] >> shift) & 255]++;
+                    kd[p] = ks[i];
+                    vd[p] = vs[i];
+                }
+        }
+        int64_t* tk = ks; ks = kd; kd = tk;
+        double* tv = vs; vs = vd; vd = tv;
+    }
+    if (ks != keys) {
+        memcpy(keys, ks, sizeof(int64_t) * (size_t)n);
+        memcpy(vals, vs, sizeof(double) * (size_t)n);
+    }
+    free(cnt);
+}
+
+/* sparse_ref.coo_from_entries' duplicate sum over sorted keys: each run of
+ * equal keys folds 0.0 + v0 + v1 + ... in input order (np.add.at into zeros).
+ * Writes int32 row/col and the sums; returns the unique count. */
+int64_t or_coo_dedup(int64_t n, int64_t ncols, const int64_t* keys, const double* vals, int32_t* row,
+                     int32_t* col, double* out) {
+    int64_t u = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        if (i == 0 || keys[i] != keys[i - 1]) {
+            ++u;
+            row[u] = (int32_t)(keys[i] / ncols);
+            col[u] = (int32_t)(keys[i] % ncols);
+            out[u] = 0.0;
+        }
+        out[u] += vals[i];
+    }
+    return u + 1;
+}

@@ -46,6 +46,11 @@ def lib():
         L.or_sellp_sets.argtypes = [_I64, _I64, _P, _P, _P, ctypes.c_int]
         L.or_sellp_sets.restype = _I64
         L.or_sellp_fill.argtypes = [_I64, _I64, _P, _P, _P, _P, _P, _P, ctypes.c_int]
+        L.or_rmat_keys.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                   ctypes.c_uint64, _I64, _I64, _P, _P, ctypes.c_int]
+        L.or_sort_pairs.argtypes = [_I64, ctypes.c_int, _P, _P, _P, _P, ctypes.c_int]
+        L.or_coo_dedup.argtypes = [_I64, _I64, _P, _P, _P, _P, _P]
+        L.or_coo_dedup.restype = _I64
         _lib = L
     return _lib
 
@@ -181,3 +186,43 @@ def csr_to_sellp(m, slice_size=64, nthreads=0):
     L.or_sellp_fill(n, ss, _p(ptrs), _p(ccol), _p(cval), _p(sets), _p(col), _p(val), nthreads)
     return SimpleNamespace(nrows=n, ncols=m.ncols, slice_size=ss, slice_sets=sets, col_idx=col, values=val,
                            row_lengths=lengths)
+
+
+def rmat_keys(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, nthreads=0):
+    """corpus_ref.rmat_edges in C as (row * 2**scale + col int64 keys, values)."""
+    n = (1 << scale) * edge_factor
+    keys = np.empty(n, dtype=np.int64)
+    vals = np.empty(n, dtype=np.float64)
+    lib().or_rmat_keys(scale, a, b, c, seed, 0, n, _p(keys), _p(vals), nthreads)
+    return keys, vals
+
+
+def sort_pairs(keys, vals, key_bits=64, nthreads=0):
+    """Stable LSD radix sort of (int64 key, f64 value) pairs, in place."""
+    assert keys.dtype == np.int64 and vals.dtype == np.float64 and len(keys) == len(vals)
+    assert keys.flags.c_contiguous and vals.flags.c_contiguous
+    ka, va = np.empty_like(keys), np.empty_like(vals)
+    lib().or_sort_pairs(len(keys), key_bits, _p(keys), _p(vals), _p(ka), _p(va), nthreads)
+    return keys, vals
+
+
+def coo_from_keys(nrows, ncols, keys, vals, key_bits=64, nthreads=0):
+    """sparse_ref.coo_from_entries (sum_duplicates) on packed keys, in C:
+    stable sort, then each duplicate run folded 0.0 + v0 + v1 + ... in input
+    order. int32 row/column indices. Sorts keys/vals in place."""
+    from types import SimpleNamespace
+
+    sort_pairs(keys, vals, key_bits, nthreads)
+    n = len(keys)
+    row = np.empty(n, dtype=np.int32)
+    col = np.empty(n, dtype=np.int32)
+    out = np.empty(n, dtype=np.float64)
+    u = lib().or_coo_dedup(n, ncols, _p(keys), _p(vals), _p(row), _p(col), _p(out))
+    return SimpleNamespace(nrows=nrows, ncols=ncols, row_idx=row[:u], col_idx=col[:u], values=out[:u])
+
+
+def rmat_coo(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=42, nthreads=0):
+    """corpus_ref.rmat (sorted, duplicate-summed R-MAT COO) in C."""
+    n = 1 << scale
+    keys, vals = rmat_keys(scale, edge_factor, a, b, c, seed, nthreads)
+    return coo_from_keys(n, n, keys, vals, 2 * scale, nthreads)

@@ -146,3 +146,32 @@ def test_c_generators_equal_numpy_restatements():
             for k in ("slice_sets", "col_idx", "row_lengths"):
                 assert np.array_equal(getattr(sa, k), getattr(sb, k)), k
             assert sa.values.tobytes() == sb.values.tobytes()
+
+
+def test_c_rmat_pipeline_equals_numpy_restatement():
+    """oracle.native.rmat_coo (the C R-MAT generator + stable radix sort +
+    duplicate fold used by the full-size config-3 parity test) equals
+    corpus_ref.rmat (np.lexsort + np.add.at, sparse.py:63-80) entry for entry."""
+    from oracle import native
+
+    for scale, ef, seed in ((6, 16, 42), (11, 8, 7), (13, 16, 42)):
+        a = native.rmat_coo(scale, ef, seed=seed)
+        b = corpus_ref.rmat(scale, ef, seed=seed)
+        assert np.array_equal(a.row_idx, b.row_idx) and np.array_equal(a.col_idx, b.col_idx)
+        assert a.values.tobytes() == b.values.tobytes()
+
+
+@pytest.mark.parametrize("nthreads", [1, 3, 8])
+def test_c_sort_pairs_is_stable(nthreads):
+    from oracle import native
+
+    rng = np.random.default_rng(nthreads)
+    for n, bits in ((0, 8), (1, 16), (1000, 10), (100_003, 40), (50_000, 64)):
+        k = rng.integers(0, 1 << min(bits, 62), n, dtype=np.int64)
+        if bits == 64:
+            k = k ^ (rng.integers(0, 2, n, dtype=np.int64) << 63)  # negative keys sort as u64
+        k[: n // 3] = k[n // 3: 2 * (n // 3)]  # duplicates
+        v = rng.random(n)
+        order = np.argsort(k.view(np.uint64), kind="stable")
+        ks, vs = native.sort_pairs(k.copy(), v.copy(), bits, nthreads)
+        assert np.array_equal(ks, k[order]) and vs.tobytes() == v[order].tobytes()

@@ -46,9 +46,9 @@ def _pick(funcs, *parts):
 
 
 def test_sellp_spmv_has_no_atomics_and_uses_tma(sass):
-    # both SpMV configurations (wide SellpTmaCfg<4,3,16,1>, narrow <2,5,24,1>), kDot = kCoh = false
+    # both SpMV configurations (wide SellpTmaCfg<4,3,16,1>, narrow <2,5,24,1>), kDot = kCoh = false, kBicg = 0
     for cfg in ("SellpTmaCfgILi4ELi3ELi16ELi1E", "SellpTmaCfgILi2ELi5ELi24ELi1E"):
-        (k,) = _pick(sass, "sellp64_tma_kernel", cfg, "Lb0ELb0E")
+        (k,) = _pick(sass, "sellp64_tma_kernel", cfg, "Lb0ELb0ELi0E")
         assert not ATOMIC.search(sass[k])
         assert "UBLKCP" in sass[k]
         assert "DMUL" in sass[k] and "DADD" in sass[k] and "DFMA" not in sass[k]  # separately rounded fold
