@@ -91,7 +91,7 @@ int wk_spmv_ell_f64(int64_t nrows, int64_t ncols, int64_t width, int64_t stride,
  * (wk_csr_merge_plan_bytes / wk_csr_merge_plan_build; also holds the
  * per-tile carries, so one SpMV at a time per plan) and for
  * WK_CSR_LOAD_BALANCE (wk_csr_load_balance_plan_*); subwarp_size <= 0 picks
- * next_pow2(nnz/nrows) <= 32. */
+ * the largest power of two <= nnz/nrows, clamped to [1, 32]. */
 int wk_spmv_csr_f64(int64_t nrows, int64_t ncols, int64_t nnz, const int32_t* row_ptrs, const int32_t* col_idx,
                     const double* values, const double* x, double* y, int32_t strategy, int32_t subwarp_size,
                     void* plan, wk_stream_t stream);

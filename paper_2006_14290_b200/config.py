@@ -26,7 +26,7 @@ DEFAULT_TUNING = {
     # reference keys (config.py:56): kept for drop-in tuning tables
     "block_size": 256,
     "subwarps_per_block": 32,
-    # 0 = auto: next power of two of the mean row length, <= 32
+    # 0 = auto: the largest power of two <= the mean row length, clamped to [1, 32]
     "csr_subwarp_size": 0,
     # B200 additions
     # auto: rowblock for regular row lengths, stream (load-balanced) otherwise

@@ -297,47 +297,55 @@ int64_t csr_stream_chunks(int64_t nnz) {
 // lanes strides the row, butterfly reduction, rank 0 writes. T == 1 is the
 // sequential thread-per-row fold (bitwise).
 // ---------------------------------------------------------------------------
-// kRows rows per tile in flight: the row bounds, then the first entries'
-// values / columns, then the gathers of all kRows rows are issued before any
-// fold (one row at a time left the kernel at three dependent round trips per
-// row: 1.24 ms, 0.33 of the copy peak, on the 27-point operator; 4 rows: 1.06
-// ms; 8 rows: 1.54 ms, fewer resident warps). Per row the
-// arithmetic is unchanged: lane l folds entries lo + l, lo + l + T, ... in
-// order, then the butterfly.
+// Two rows per tile in flight, software-pipelined: the next group's row
+// bounds load while this group's first entries and x gathers are in flight,
+// so a group costs two dependent round trips instead of three. Measured on
+// the 27-point 200^3 operator (tools/subwarp_probe.py, same box): 4 rows
+// unpipelined 1.06 ms (T = 32) / 0.84 ms (T = 4); this kernel 0.69 ms at
+// T = 16; 4 or 8 rows with deeper prefetch 0.94-1.33 ms (registers: fewer
+// resident warps). Per row the arithmetic is unchanged: lane l folds entries
+// lo + l, lo + l + T, ... in order, then the butterfly.
 template <unsigned T>
 __global__ void __launch_bounds__(kSpmvThreads)
 csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __restrict__ col,
                    const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y,
                    const int* __restrict__ skip) {
-    constexpr int kRows = 4;
+    constexpr int kRows = 2;
     if (skip != nullptr && *skip) return;
     auto tile = cg::tiled_partition<T>(cg::this_thread_block());
     const int64_t tiles_per_grid = int64_t(gridDim.x) * (kSpmvThreads / T);
+    const int64_t step = kRows * tiles_per_grid;
     const int tr = int(tile.thread_rank());
-    for (int64_t row0 = int64_t(blockIdx.x) * (kSpmvThreads / T) + tile.meta_group_rank(); row0 < nrows;
-         row0 += kRows * tiles_per_grid) {
-        int64_t lo[kRows], hi[kRows];
+    int lo[kRows], hi[kRows];
+    auto bounds = [&](int64_t r0, int* l, int* h) {
 #pragma unroll
         for (int u = 0; u < kRows; ++u) {
-            const int64_t row = row0 + u * tiles_per_grid;
-            lo[u] = row < nrows ? ptrs[row] : 0;
-            hi[u] = row < nrows ? ptrs[row + 1] : 0;
+            const int64_t row = r0 + u * tiles_per_grid;
+            l[u] = row < nrows ? __ldg(ptrs + row) : 0;
+            h[u] = row < nrows ? __ldg(ptrs + row + 1) : 0;
         }
-        double acc[kRows], v0[kRows], x0[kRows];
+    };
+    int64_t row0 = int64_t(blockIdx.x) * (kSpmvThreads / T) + tile.meta_group_rank();
+    bounds(row0, lo, hi);
+    for (; row0 < nrows; row0 += step) {
         int c0[kRows];
+        double v0[kRows], x0[kRows];
 #pragma unroll
         for (int u = 0; u < kRows; ++u) {
-            const int64_t k = lo[u] + tr;
+            const int k = lo[u] + tr;
             c0[u] = k < hi[u] ? ld_stream(col + k) : 0;
             v0[u] = k < hi[u] ? ld_stream(val + k) : 0.0;
         }
+        int nlo[kRows], nhi[kRows];
+        bounds(row0 + step, nlo, nhi);
 #pragma unroll
         for (int u = 0; u < kRows; ++u) x0[u] = lo[u] + tr < hi[u] ? ld_x(x, c0[u]) : 0.0;
+        double acc[kRows];
 #pragma unroll
         for (int u = 0; u < kRows; ++u) {
             acc[u] = 0.0;
             if (lo[u] + tr < hi[u]) acc[u] = mul_add_rn(0.0, v0[u], x0[u]);
-            for (int64_t k = lo[u] + tr + T; k < hi[u]; k += T)
+            for (int k = lo[u] + tr + int(T); k < hi[u]; k += T)
                 acc[u] = mul_add_rn(acc[u], ld_stream(val + k), ld_x(x, ld_stream(col + k)));
         }
 #pragma unroll
@@ -345,6 +353,8 @@ csr_subwarp_kernel(int64_t nrows, const int* __restrict__ ptrs, const int* __res
             const double r = reduce_subwarp(tile, acc[u]);
             const int64_t row = row0 + u * tiles_per_grid;
             if (tr == 0 && row < nrows) y[row] = r;
+            lo[u] = nlo[u];
+            hi[u] = nhi[u];
         }
     }
 }
@@ -453,10 +463,14 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
     }
     WK_REQUIRE(strategy == WK_CSR_SUBWARP, WK_ERR_INVALID, "unknown CSR strategy %d", strategy);
     int T = subwarp;
-    if (T <= 0) {  // auto: next power of two of the mean row length, clamped to [1, 32]
-        const int64_t avg = ceil_div(nnz, nrows);
+    if (T <= 0) {
+        // auto: the largest power of two <= the mean row length, clamped to
+        // [1, 32] (rounding up left most lanes of a short row idle: 27-point
+        // rows at T = 32 take 0.86 ms vs 0.69 at T = 16; 5-point rows 32 vs
+        // 25 us at T = 8 vs 4)
+        const int64_t avg = nnz / (nrows > 0 ? nrows : 1);
         T = 1;
-        while (T < avg && T < 32) T <<= 1;
+        while (2 * T <= avg && T < 32) T <<= 1;
     }
     const int64_t tiles_per_block = kSpmvThreads / T;
     int64_t blocks = ceil_div(nrows, tiles_per_block);

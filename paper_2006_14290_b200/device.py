@@ -126,7 +126,7 @@ class DeviceCsr(DeviceMatrix):
         self.nnz = int(values.numel())
         self._plan = None
         self._wk = None
-        self.strategy = _lib.WK_CSR_STREAM
+        self.strategy = None  # "auto", resolved at the first launch (auto_strategy)
         self.subwarp = 0
         self._auto = None
 
@@ -188,6 +188,8 @@ class DeviceCsr(DeviceMatrix):
         return self
 
     def _make_wk(self):
+        if self.strategy is None:
+            self.with_strategy("auto")
         m = WkMatrix()
         m.format = _lib.WK_FMT_CSR
         m.csr_strategy = self.strategy
