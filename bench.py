@@ -642,10 +642,12 @@ def bench_cg(args, wk, corpus, D):
     ms = t0.elapsed_time(t1)
     it = len(hist) - 1
     spmv_b = A.algorithmic_bytes()
-    # SpMV + vector passes: 8 per iteration (r, q -> r; x, p, r -> x, p), 9 in
-    # the residual-replacement iteration (x/r then p), which also runs
-    # SpMV(x) and r = b - q; one replacement per 50 iterations
-    per_it = spmv_b + (49 * 64 + 72) * A.nrows / 50 + (spmv_b + 24 * A.nrows) / 50
+    # SpMV + vector passes per 50-iteration period: iterations 0..47 in pairs
+    # (r, q -> r twice; p, r -> p'; x, p_prev, p, r -> x, p'': 15 vectors per
+    # pair), iteration 48 with 8 (r, q -> r; x, p, r -> x, p), the
+    # residual-replacement iteration with 9 (x/r then p) plus SpMV(x) and
+    # r = b - q
+    per_it = spmv_b + (24 * 120 + 64 + 72) * A.nrows / 50 + (spmv_b + 24 * A.nrows) / 50
     # the CG operator's plain SpMV (narrow SELL-P configuration: 7-wide slices)
     xs = torch.rand(A.ncols, dtype=torch.float64, device="cuda")
     ys = torch.empty(A.nrows, dtype=torch.float64, device="cuda")

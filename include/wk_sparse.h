@@ -292,7 +292,8 @@ typedef struct wk_cg_state {
     int32_t done;      /* converged / max_iters reached / breakdown          */
     int32_t breakdown;
     int32_t xpend;     /* wk_cg_solve: x += alpha p of the last r update pending */
-    int32_t pad;
+    int32_t xdefer;    /* wk_cg_solve: x += alpha_prev p_prev deferred to the next x pass */
+    double alpha_prev; /* wk_cg_solve: alpha of the deferred x update         */
 } wk_cg_state;
 
 /* rho := b.b (local), x = 0, r = p = b */

@@ -73,7 +73,7 @@ class WkMatrix(ctypes.Structure):
 class WkCgState(ctypes.Structure):
     _fields_ = [("rho", F64), ("pq", F64), ("rr", F64), ("threshold", F64), ("alpha", F64), ("beta", F64),
                 ("iteration", I64), ("max_iters", I64), ("done", I32), ("breakdown", I32), ("xpend", I32),
-                ("pad", I32)]
+                ("xdefer", I32), ("alpha_prev", F64)]
 
 
 class WkBicgState(ctypes.Structure):

@@ -38,6 +38,7 @@ static int cg_init_local(int64_t n, const double* b, double* x, double* r, doubl
             s->done = 0;
             s->breakdown = 0;
             s->xpend = 0;
+            s->xdefer = 0;
         }, st);
     }
     return launch_map_reduce(
@@ -55,6 +56,7 @@ static int cg_init_local(int64_t n, const double* b, double* x, double* r, doubl
             s->done = 0;
             s->breakdown = 0;
             s->xpend = 0;
+            s->xdefer = 0;
         },
         ws, nullptr, st);
 }
@@ -303,8 +305,9 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
 //   cg_update_xp_vec  x += alpha p_old and, unless the beta step ended the
 //                     solve, p = r + beta p_old; the last block clears xpend
 // 8 vector passes per iteration instead of 9 (p is read once less), every
-// element bitwise as before. Residual-replacement iterations need the new x
-// before the next r, so they keep cg_update_xr_vec + cg_update_p_vec.
+// element bitwise as before (7.5 with the x updates of two iterations applied
+// together, cg_update_xp_pair). Residual-replacement iterations need the new
+// x before the next r, so they keep cg_update_xr_vec + cg_update_p_vec.
 __global__ void __launch_bounds__(256)
 cg_update_r_vec(int64_t n, const double* __restrict__ q, double* __restrict__ r, wk_cg_state* s, double* hist,
                 RedWorkspace ws, int rev) {
@@ -395,6 +398,85 @@ cg_update_xp_vec(int64_t n, const double* __restrict__ r, double* __restrict__ x
     }
     double total;
     if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) s->xpend = 0;  // every block has read it
+}
+
+// The x update of every other iteration deferred and applied together with
+// the next one (pairs of two-pass iterations, wk_cg_solve):
+//   kPair = 0  p_next = r + beta p into the other p buffer; x += alpha p is
+//              deferred (alpha kept in alpha_prev, p stays in its buffer).
+//              If the beta step ended the solve, x += alpha p is applied now.
+//   kPair = 1  x += alpha_prev p_prev, then x += alpha p (two separately
+//              rounded adds per element: the same roundings, in the same
+//              order, as two passes); p_next = r + beta p into p_prev's buffer.
+// x is read and written once per two iterations instead of every iteration:
+// 3 + 6 vectors per pair instead of 5 + 5, every element bitwise as before.
+template <int kPair>
+__global__ void __launch_bounds__(256)
+cg_update_xp_pair(int64_t n, const double* __restrict__ r, double* __restrict__ x, const double* __restrict__ p,
+                  const double* __restrict__ pprev, double* __restrict__ pn, wk_cg_state* s, RedWorkspace ws,
+                  int rev) {
+    if (!s->xpend) return;
+    const double alpha = s->alpha, beta = s->beta, alpha0 = kPair ? s->alpha_prev : 0.0;
+    const bool upd_p = !s->done;
+    const bool upd_x = kPair == 1 || !upd_p;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* q2 = reinterpret_cast<const double2*>(pprev);
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* n2 = reinterpret_cast<double2*>(pn);
+    constexpr int U = 2;
+    const double2 z = make_double2(0.0, 0.0);
+    for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += U * T) {
+        double2 pa[U], xa[U], ra[U], qa[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            const bool ok = ku < np;
+            pa[u] = ok ? p2[k] : z;
+            xa[u] = ok && upd_x ? __ldcs(x2 + k) : z;
+            ra[u] = ok && upd_p ? __ldcs(r2 + k) : z;
+            qa[u] = ok && kPair == 1 ? __ldcs(q2 + k) : z;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t ku = kl + u * T;
+            if (ku >= np) break;
+            const int64_t k = rev ? np - 1 - ku : ku;
+            if (upd_x) {
+                if (kPair == 1) {
+                    xa[u].x = __dadd_rn(xa[u].x, __dmul_rn(alpha0, qa[u].x));
+                    xa[u].y = __dadd_rn(xa[u].y, __dmul_rn(alpha0, qa[u].y));
+                }
+                xa[u].x = __dadd_rn(xa[u].x, __dmul_rn(alpha, pa[u].x));
+                xa[u].y = __dadd_rn(xa[u].y, __dmul_rn(alpha, pa[u].y));
+                __stcs(x2 + k, xa[u]);
+            }
+            if (upd_p) {
+                double2 v;
+                v.x = __dadd_rn(ra[u].x, __dmul_rn(beta, pa[u].x));
+                v.y = __dadd_rn(ra[u].y, __dmul_rn(beta, pa[u].y));
+                n2[k] = v;
+            }
+        }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = n - 1;
+        const double pi = p[i];
+        if (upd_x) {
+            double xi = x[i];
+            if (kPair == 1) xi = __dadd_rn(xi, __dmul_rn(alpha0, pprev[i]));
+            x[i] = __dadd_rn(xi, __dmul_rn(alpha, pi));
+        }
+        if (upd_p) pn[i] = __dadd_rn(r[i], __dmul_rn(beta, pi));
+    }
+    double total;
+    if (grid_reduce_last(0.0, ws, total) && threadIdx.x == 0) {  // every block has read the state
+        s->xpend = 0;
+        s->xdefer = upd_x ? 0 : 1;
+        if (!upd_x) s->alpha_prev = alpha;
+    }
 }
 
 static int cg_update_xr(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* s,
@@ -591,7 +673,7 @@ int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state*
 // ---------------- single-GPU CG ---------------------------------------------------
 
 int64_t wk_cg_workspace_bytes(int64_t n) {
-    return 256 + red_ws_bytes() + 256 + 3 * (ceil_div(n * 8, 256) * 256) + 256;
+    return 256 + red_ws_bytes() + 256 + 4 * (ceil_div(n * 8, 256) * 256) + 256;
 }
 
 
@@ -607,6 +689,7 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     double* r = cv.take<double>(n);
     double* p = cv.take<double>(n);
     double* q = cv.take<double>(n);
+    double* p1 = cv.take<double>(n);  // the second p buffer of paired iterations
     cudaStream_t user = as_stream(stream);
     GraphRunner g;
     WK_CUDA(cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking));
@@ -625,15 +708,26 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
     // 50-iteration period is even).
     // the two-pass iteration (cg_update_r_vec / cg_update_xp_vec) for every
     // iteration but the residual replacement, when the vectors are aligned
-    const bool two_pass = n > 0 && vec_ok(p, q, x, r) && vec_grid(n) <= kRedMaxBlocks;
+    // Iterations 0..47 run in pairs (cg_update_xp_pair): the even one leaves
+    // its x update pending and writes the next p into p1, the odd one applies
+    // both x updates and writes the next p back into p; iteration 48 is a
+    // plain two-pass iteration and 49 the residual replacement (both in p).
+    const bool two_pass = n > 0 && vec_ok(p, q, x, r) && vec_ok(p1, p1, p1, p1) && vec_grid(n) <= kRedMaxBlocks;
     int rc = capture(g, [&](cudaStream_t cs) -> int {
         for (int i = 0; i < kReplaceEvery; ++i) {
             const int d = i & 1;
-            WK_TRY(cg_spmv_dot(A, n, p, q, s, red, true, cs, nullptr, nullptr, d));
+            const bool paired = two_pass && i < kReplaceEvery - 2;
+            const double* pcur = paired && (i & 1) ? p1 : p;
+            WK_TRY(cg_spmv_dot(A, n, pcur, q, s, red, true, cs, nullptr, nullptr, d));
             if (two_pass && i < kReplaceEvery - 1) {
                 cg_update_r_vec<<<vec_grid(n), 256, 0, cs>>>(n, q, r, s, hist, red_ws(red), 1 - d);
                 WK_LAUNCH_CHECK();
-                cg_update_xp_vec<<<vec_grid(n), 256, 0, cs>>>(n, r, x, p, s, red_ws(red), d);
+                if (paired && !(i & 1))
+                    cg_update_xp_pair<0><<<vec_grid(n), 256, 0, cs>>>(n, r, x, p, nullptr, p1, s, red_ws(red), d);
+                else if (paired)
+                    cg_update_xp_pair<1><<<vec_grid(n), 256, 0, cs>>>(n, r, x, p1, p, p, s, red_ws(red), d);
+                else
+                    cg_update_xp_vec<<<vec_grid(n), 256, 0, cs>>>(n, r, x, p, s, red_ws(red), d);
                 WK_LAUNCH_CHECK();
                 continue;
             }
@@ -656,6 +750,11 @@ int wk_cg_solve(const wk_matrix* A, const double* b, double tol, int64_t max_ite
         WK_CUDA(cudaStreamSynchronize(st));
         if (h.done) break;
         WK_CUDA(cudaGraphLaunch(g.exec, st));
+    }
+    if (h.xdefer) {  // stopped by a breakdown right after an even iteration of a pair: x += alpha_prev p
+        WK_TRY(launch_masked_map(
+            n, [=] __device__(int64_t i) { x[i] = __dadd_rn(x[i], __dmul_rn(s->alpha_prev, p[i])); }, nullptr, st));
+        WK_CUDA(cudaStreamSynchronize(st));
     }
     WK_CUDA(cudaEventRecord(ev, st));
     WK_CUDA(cudaStreamWaitEvent(user, ev, 0));
