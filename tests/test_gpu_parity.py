@@ -818,3 +818,53 @@ def test_hybrid_fill_long_row_boundaries(wk, ex, rng, width):
     assert hyb.coo.values.tobytes() == ref.coo.values.tobytes()
     x = rng.standard_normal(ncols)
     assert sparse_ref.max_scaled_rel_err(wk.spmv_hybrid(hyb, x, ex), sparse_ref.spmv(csr, x), lens) <= TOL
+
+
+def test_cg_pending_x_update_flushed_on_breakdown(wk, ex):
+    """diag(1, 1, -1.5), b = ones: iteration 1 (alpha 6) is the even half of a
+    paired x update (cg_update_xp_pair<0> defers x += alpha p), iteration 2
+    breaks down (p.Ap = 4050 - 5400 < 0) before its x pass. wk_cg_solve must
+    still leave x = x_1 = 6 * ones (the deferred update applied) and report
+    the breaking iteration, 2 (the reference's "at iteration 2")."""
+    import ctypes
+
+    import torch
+
+    from paper_2006_14290_b200 import _lib
+    from paper_2006_14290_b200 import device as D
+
+    A = wk.coo_to_sellp(wk.CooMatrix(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, -1.5]), 64, ex)
+    d = D.as_device(A, ex.device)
+    b = torch.ones(3, dtype=torch.float64, device=d.device)
+    x = torch.full((3,), -7.0, dtype=torch.float64, device=d.device)
+    hist = torch.zeros(11, dtype=torch.float64, device=d.device)
+    iters = ctypes.c_int64(-1)
+    L = _lib.load()
+    ws = torch.zeros(int(L.wk_cg_workspace_bytes(3)), dtype=torch.uint8, device=d.device)
+    rc = L.wk_cg_solve(d.wk_ptr(), D._ptr(b), 1e-12, 10, D._ptr(x), D._ptr(hist), ctypes.byref(iters),
+                       D._ptr(ws), D.stream_handle(d.device))
+    torch.cuda.synchronize()
+    assert rc == _lib.WK_ERR_BREAKDOWN
+    assert iters.value == 2
+    assert x.cpu().tolist() == [6.0, 6.0, 6.0]
+    with pytest.raises(wk.BreakdownError):
+        wk.cg_solve(A, np.ones(3), 1e-12, 10, ex)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5])
+def test_cg_converging_on_either_half_of_a_pair(wk, ex, n):
+    """Diagonal systems with k distinct eigenvalues converge in exactly k
+    iterations, so k = 2..5 ends the solve on the even (x update otherwise
+    deferred) and the odd (both updates applied) iteration of a pair; x and
+    the history must match the reference CG (dot products may reassociate:
+    1e-12 relative)."""
+    from oracle import krylov_ref
+
+    vals = [1.0, 2.0, 4.0, 8.0, 16.0][:n]
+    m = wk.coo_to_sellp(wk.CooMatrix(n, n, list(range(n)), list(range(n)), vals), 64, ex)
+    b = np.arange(1.0, n + 1.0)
+    x, hist = wk.cg_solve(m, b, 1e-14, 50, ex)
+    rx, rh = krylov_ref.cg_solve(lambda v: np.asarray(vals) * v, b, 1e-14, 50)
+    assert len(hist) == len(rh) == n + 1
+    assert np.max(np.abs(np.asarray(x) - rx)) <= 1e-12 * np.max(np.abs(rx))
+    assert np.max(np.abs(np.asarray(hist) - rh)) <= 1e-12 * rh[0]
