@@ -31,7 +31,9 @@ cap ell_fill fill_tma_kernel 2 1 python tools/profile_spmv.py convert 27 200
 cap sellp_fill fill_tma_kernel 3 1 python tools/profile_spmv.py convert 27 200
 cap cg_spmv_dot sellp64_tma 5 1 python tools/profile_cg.py 256 60
 cap cg_update_r cg_update_r_vec 5 1 python tools/profile_cg.py 256 60
-cap cg_update_xp cg_update_xp_vec 5 1 python tools/profile_cg.py 256 60
+cap cg_update_xp cg_update_xp_vec 0 1 python tools/profile_cg.py 256 60
+cap cg_update_xp_pair0 cg_update_xp_pair 4 1 python tools/profile_cg.py 256 60
+cap cg_update_xp_pair1 cg_update_xp_pair 5 1 python tools/profile_cg.py 256 60
 cap sort_downsweep rs_downsweep 2 1 python tools/quick_sort.py 22
 cap sort_upsweep rs_upsweep 2 1 python tools/quick_sort.py 22
 cap hybrid_coo_fill hybrid_coo 0 2 python tools/quick_hybrid.py 22
