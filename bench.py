@@ -678,14 +678,14 @@ def _nonsym_bytes(n, spmv_b, kind, iters, restart=30):
     """Algorithmic bytes per iteration: BiCGSTAB = 2 SpMV + 15 vector passes
     (p update 4, s update 3, x/r update + rh.r 7, rh read by the fused r-hat.v
     of the first SpMV 1; t.t / t.s fused into the second SpMV);
-    GMRES(m) inner step j = SpMV + (2j + 6) vector passes (CGS dots, update,
-    norm, scale), averaged over the iterations run, + one SpMV and 4 passes per
-    restart."""
+    GMRES(m) inner step j = SpMV + (2j + 4) vector passes (CGS dots, update
+    with the norm; the new direction is not rescaled: deferred normalisation),
+    averaged over the iterations run, + one SpMV and 4 passes per restart."""
     if kind == "bicgstab":
         return 2 * spmv_b + 15 * 8 * n
     steps = [(i % restart) for i in range(iters)]
     cyc = max(1, -(-iters // restart))
-    tot = sum(spmv_b + (2 * j + 6) * 8 * n for j in steps) + cyc * (spmv_b + 4 * 8 * n)
+    tot = sum(spmv_b + (2 * j + 4) * 8 * n for j in steps) + cyc * (spmv_b + 4 * 8 * n)
     return tot / max(iters, 1)
 
 

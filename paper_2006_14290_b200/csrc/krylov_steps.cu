@@ -471,6 +471,85 @@ gmres_orth_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, doubl
     if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0) s->sq = total;
 }
 
+// Deferred normalisation (single-GPU wk_gmres_solve): basis slot i holds
+// u_i with v_i = sig[i] u_i, so the new direction is never rescaled in a
+// separate pass. The SpMV writes z = A u_j straight into slot j+1 and the
+// multidot leaves d_i = u_i . z in Hj; this kernel forms h_i = sig_i sig_j d_i
+// (= v_i . A v_j), w = sig_j z - sum_i (h_i sig_i) u_i in place in slot j+1
+// and ||w||^2; the Givens step then sets sig[j+1] = 1 / ||w||. Two vector
+// passes (read w, write v_{j+1}) fewer per iteration; the same algorithm up
+// to rounding (w is formed from sig_j z instead of A fl(w / h)).
+template <int K>
+__global__ void __launch_bounds__(256, 4)
+gmres_orth_scaled_vec(int64_t n, int k, const double* __restrict__ V, int64_t ld, double* __restrict__ w,
+                      double* __restrict__ Hj, const double* __restrict__ sig, GS* s, RedWorkspace ws) {
+    if (s->cycle_done) return;
+    __shared__ double c[K];
+    __shared__ double hs[K];
+    const double sj = sig[k - 1];
+    if (threadIdx.x < K) {
+        const int q = threadIdx.x;
+        const double h = q < k ? __dmul_rn(__dmul_rn(sig[q], sj), Hj[q]) : 0.0;
+        hs[q] = h;
+        c[q] = q < k ? __dmul_rn(h, sig[q]) : 0.0;
+    }
+    __syncthreads();
+    double acc = 0.0;
+    const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
+    for (int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x; i < np; i += T) {
+        double2 wv = reinterpret_cast<const double2*>(w)[i];
+        wv.x = __dmul_rn(sj, wv.x);
+        wv.y = __dmul_rn(sj, wv.y);
+#pragma unroll
+        for (int g = 0; g < K; g += kCgsGroup) {
+            double2 v[kCgsGroup];
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) v[u] = __ldcs(reinterpret_cast<const double2*>(V + int64_t(g + u) * ld) + i);
+#pragma unroll
+            for (int u = 0; u < kCgsGroup; ++u)
+                if (g + u < k) {
+                    wv.x = __dadd_rn(wv.x, -__dmul_rn(c[g + u], v[u].x));
+                    wv.y = __dadd_rn(wv.y, -__dmul_rn(c[g + u], v[u].y));
+                }
+        }
+        reinterpret_cast<double2*>(w)[i] = wv;
+        acc += __dmul_rn(wv.x, wv.x);
+        acc += __dmul_rn(wv.y, wv.y);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        double wi = __dmul_rn(sj, w[n - 1]);
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (q < k) wi = __dadd_rn(wi, -__dmul_rn(c[q], V[int64_t(q) * ld + n - 1]));
+        w[n - 1] = wi;
+        acc += __dmul_rn(wi, wi);
+    }
+    double total;
+    if (grid_reduce_last(acc, ws, total) && threadIdx.x == 0) {  // every block has read the raw d_i
+        for (int q = 0; q < k; ++q) Hj[q] = hs[q];
+        s->sq = total;
+    }
+}
+
+static int gmres_orth_scaled(int64_t n, int j, const double* V, int64_t ld, double* w, double* Hj, const double* sig,
+                             GS* s, void* ws, cudaStream_t st) {
+    const int k = j + 1;
+    const RedWorkspace rw = red_ws(ws);
+#define WK_ORTH_S(KK)                                                                             \
+    do {                                                                                          \
+        gmres_orth_scaled_vec<KK><<<orth_grid(n), 256, 0, st>>>(n, k, V, ld, w, Hj, sig, s, rw);  \
+        WK_LAUNCH_CHECK();                                                                        \
+        return 0;                                                                                 \
+    } while (0)
+    if (k <= 2) WK_ORTH_S(2);
+    if (k <= 4) WK_ORTH_S(4);
+    if (k <= 8) WK_ORTH_S(8);
+    if (k <= 16) WK_ORTH_S(16);
+    WK_ORTH_S(kRedMaxVec);
+#undef WK_ORTH_S
+}
+
 #define WK_CGS_LAUNCH(KERN, KK, ...)                                                         \
     do {                                                                                   \
         KERN<KK><<<cgs_grid(n, KK), 256, 0, st>>>(__VA_ARGS__);                            \
@@ -538,13 +617,15 @@ static int gmres_orth(int64_t n, int j, const double* V, int64_t ld, double* w, 
         [=] __device__(double t) { s->sq = t; }, ws, &s->cycle_done, st);
 }
 
-static int gmres_givens(int j, double* H, double* cs_, double* sn_, double* g, GS* s, double* hist, cudaStream_t st) {
+static int gmres_givens(int j, double* H, double* cs_, double* sn_, double* g, GS* s, double* hist, cudaStream_t st,
+                        double* sig = nullptr) {
     return launch_scalar([=] __device__() {
         if (s->cycle_done) return;
         const int m = s->restart;
         double* Hj = H + int64_t(j) * (m + 1);
         const double hn = sqrt(s->sq);
         s->hn = hn;
+        if (sig != nullptr) sig[j + 1] = hn != 0.0 ? 1.0 / hn : 0.0;  // the scale of basis slot j + 1
         Hj[j + 1] = hn;
         for (int i = 0; i < j; ++i) {
             const double a = Hj[i], c = Hj[i + 1];
@@ -582,7 +663,7 @@ static int gmres_next_basis(int64_t n, const double* w, double* Vn, GS* s, cudaS
 }
 
 static int gmres_update_x(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y, double* x,
-                          GS* s, cudaStream_t st) {
+                          GS* s, cudaStream_t st, const double* sig = nullptr) {
     WK_TRY(launch_scalar([=] __device__() {
         if (s->done) return;
         const int m = s->restart, jd = s->j_done;
@@ -591,6 +672,9 @@ static int gmres_update_x(int64_t n, const double* V, int64_t ld, const double* 
             for (int k = i + 1; k < jd; ++k) acc = __dadd_rn(acc, -__dmul_rn(H[i + int64_t(k) * (m + 1)], y[k]));
             y[i] = acc / H[i + int64_t(i) * (m + 1)];
         }
+        // deferred normalisation: x += sum y_i v_i = sum (y_i sig_i) u_i
+        if (sig != nullptr)
+            for (int i = 0; i < jd; ++i) y[i] = __dmul_rn(y[i], sig[i]);
     }, st));
     return launch_masked_map(
         n,
@@ -849,7 +933,7 @@ int wk_bicgstab_solve(const wk_matrix* A, const double* b, double tol, int64_t m
 int64_t wk_gmres_workspace_bytes(int64_t n, int32_t restart) {
     const int64_t m = restart;
     const int64_t vec = ceil_div(n * 8, 256) * 256;
-    return 256 + red_ws_bytes() + 256 + (m + 1) * vec + 2 * vec + ceil_div((m + 1) * m * 8 + 4 * (m + 1) * 8, 256) * 256 +
+    return 256 + red_ws_bytes() + 256 + (m + 1) * vec + 2 * vec + ceil_div((m + 1) * m * 8 + 5 * (m + 1) * 8, 256) * 256 +
            256;
 }
 
@@ -869,12 +953,13 @@ int wk_gmres_solve(const wk_matrix* A, const double* b, double tol, int64_t max_
     double* V = cv.take<double>(ld * (m + 1));
     double* w = cv.take<double>(n);
     double* r = cv.take<double>(n);
-    double* small = cv.take<double>((m + 1) * m + 4 * (m + 1));
+    double* small = cv.take<double>((m + 1) * m + 5 * (m + 1));
     double* H = small;
     double* cs_ = H + (m + 1) * m;
     double* sn_ = cs_ + (m + 1);
     double* g = sn_ + (m + 1);
     double* y = g + (m + 1);
+    double* sig = y + (m + 1);
     cudaStream_t user = as_stream(stream);
     GraphRunner gr;
     WK_CUDA(cudaStreamCreateWithFlags(&gr.cs, cudaStreamNonBlocking));
@@ -888,18 +973,30 @@ int wk_gmres_solve(const wk_matrix* A, const double* b, double tol, int64_t max_
     WK_TRY(gmres_init_finish(s, tol, max_iters, m, hist, st));
     const int* done = &s->done;
     const int* cdone = &s->cycle_done;
+    // deferred normalisation (gmres_orth_scaled_vec) when the basis takes
+    // 16-byte vector access; otherwise w, then v_{j+1} = w / h (next_basis)
+    const bool scaled = n > 1 && cgs_vec_ok(V, ld, V);
     int rc = capture(gr, [&](cudaStream_t cs) -> int {
         WK_TRY(gmres_cycle_start(n, r, V, g, s, cs));
+        if (scaled) WK_TRY(launch_scalar([=] __device__() { sig[0] = 1.0; }, cs));
         for (int j = 0; j < m; ++j) {
             double* Vj = V + int64_t(j) * ld;
             double* Hj = H + int64_t(j) * (m + 1);
+            if (scaled) {
+                double* z = V + int64_t(j + 1) * ld;
+                WK_TRY(wk_spmv_masked(A, Vj, z, cdone, cs));
+                WK_TRY(gmres_multidot(n, j, V, ld, z, Hj, s, red, cs));
+                WK_TRY(gmres_orth_scaled(n, j, V, ld, z, Hj, sig, s, red, cs));
+                WK_TRY(gmres_givens(j, H, cs_, sn_, g, s, hist, cs, sig));
+                continue;
+            }
             WK_TRY(wk_spmv_masked(A, Vj, w, cdone, cs));
             WK_TRY(gmres_multidot(n, j, V, ld, w, Hj, s, red, cs));
             WK_TRY(gmres_orth(n, j, V, ld, w, Hj, s, red, cs));
             WK_TRY(gmres_givens(j, H, cs_, sn_, g, s, hist, cs));
             if (j + 1 < m) WK_TRY(gmres_next_basis(n, w, V + int64_t(j + 1) * ld, s, cs));
         }
-        WK_TRY(gmres_update_x(n, V, ld, H, g, y, x, s, cs));
+        WK_TRY(gmres_update_x(n, V, ld, H, g, y, x, s, cs, scaled ? sig : nullptr));
         WK_TRY(wk_spmv_masked(A, x, w, done, cs));
         WK_TRY(gmres_residual(n, b, w, r, s, red, cs));
         WK_TRY(gmres_restart(s, hist, cs));
