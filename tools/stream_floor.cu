@@ -14,6 +14,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #define CK(x)                                                                 \
     do {                                                                      \
@@ -93,11 +94,18 @@ __global__ void __launch_bounds__(256, 1) bulk_kernel(const char* __restrict__ i
         __stcs(out + i, make_int4(acc, 0, 0, 0));
 }
 
-int main() {
+// usage: stream_floor [read_bytes write_bytes]; the default is config 1. The
+// config-2 headline (SELL-P 27-point 200^3: 2,640,093,256 B read, 64,000,000
+// B written) is `stream_floor 2640093256 64000000`.
+int main(int argc, char** argv) {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t in_bytes = 72000000;  // col 20 MB + val 40 MB + ptrs 4 MB + x 8 MB
-    const int64_t out_bytes = 8000000;  // y
+    int64_t in_bytes = 72000000;  // col 20 MB + val 40 MB + ptrs 4 MB + x 8 MB
+    int64_t out_bytes = 8000000;  // y
+    if (argc == 3) {
+        in_bytes = (atoll(argv[1]) + 15) / 16 * 16;
+        out_bytes = (atoll(argv[2]) + 15) / 16 * 16;
+    }
     const int64_t flush_bytes = int64_t(512) << 20;
     char *in, *out, *fl;
     CK(cudaMalloc(&in, in_bytes + 4096));
