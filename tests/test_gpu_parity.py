@@ -868,3 +868,38 @@ def test_cg_converging_on_either_half_of_a_pair(wk, ex, n):
     assert len(hist) == len(rh) == n + 1
     assert np.max(np.abs(np.asarray(x) - rx)) <= 1e-12 * np.max(np.abs(rx))
     assert np.max(np.abs(np.asarray(hist) - rh)) <= 1e-12 * rh[0]
+
+
+@pytest.mark.parametrize("restart", [1, 2, 5, 31])
+def test_gmres_restart_lengths_match_oracle(wk, ex, restart):
+    """GMRES with deferred normalisation (wk_gmres_solve keeps the basis
+    unscaled, v_i = sig_i u_i) against the restatement's explicit
+    normalisation, for restart lengths from 1 to the maximum, odd n."""
+    from paper_2006_14290_b200 import corpus
+
+    A = corpus.convection_diffusion3d(7)
+    Ah = A.to_host()
+    b = np.linspace(1.0, 2.0, A.nrows)
+    f = lambda v: sparse_ref.spmv(Ah, v)  # noqa: E731
+    x, hist = wk.gmres_solve(A, b, 1e-10, 400, ex, restart=restart)
+    xr, hr = krylov_ref.gmres_solve(f, b, 1e-10, 400, restart=restart)
+    x = x.cpu().numpy() if hasattr(x, "cpu") else x
+    hist = hist.cpu().numpy() if hasattr(hist, "cpu") else hist
+    assert len(hist) == len(hr)
+    assert np.max(np.abs(hist - hr)) / np.linalg.norm(b) <= 1e-10
+    assert sparse_ref.max_scaled_rel_err(x, xr, sparse_ref.row_nnz(Ah)) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_gmres_lucky_breakdown(wk, ex, k):
+    """A diagonal matrix with k distinct eigenvalues: the Krylov space is
+    exhausted after k steps (||w|| = 0: the next basis scale is never used)
+    and GMRES returns the exact solution."""
+    n = 64
+    vals = [1.0 + (i % k) for i in range(n)]
+    m = wk.coo_to_sellp(wk.CooMatrix(n, n, list(range(n)), list(range(n)), vals), 64, ex)
+    b = np.ones(n)
+    x, hist = wk.gmres_solve(m, b, 1e-14, 50, ex, restart=10)
+    x = x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+    assert len(hist) - 1 == k
+    assert np.max(np.abs(x - 1.0 / np.asarray(vals))) <= 1e-14
