@@ -321,10 +321,13 @@ int wk_cg_replace_r(int64_t n, const double* b, const double* q, double* r, wk_c
 /* fused variants (one launch each instead of two): the alpha step evaluated
  * from the all-reduced p.Ap inside the x/r update, and the beta step from the
  * all-reduced r.r inside the p update */
+/* two vector passes per iteration: x += alpha p is applied by
+ * wk_cg_update_p_beta (which reads p anyway), except on residual-replacement
+ * iterations, where the x/r update applies it (the replacement needs x) */
 int wk_cg_update_xr_alpha(int64_t n, const double* p, const double* q, double* x, double* r, wk_cg_state* state,
                           void* workspace, wk_stream_t stream);
-int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist, void* workspace,
-                        wk_stream_t stream);
+int wk_cg_update_p_beta(int64_t n, const double* r, double* p, double* x, wk_cg_state* state, double* hist,
+                        void* workspace, wk_stream_t stream);
 /* after all-reduce of rr: hist, beta, rho := rr, done */
 int wk_cg_step_beta(wk_cg_state* state, double* hist, wk_stream_t stream);
 /* p = r + beta p ; skipped when done */
@@ -460,7 +463,7 @@ int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, doub
                                wk_cg_state* state, void* workspace, void* peer, wk_stream_t stream);
 int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r, wk_cg_state* state,
                          void* workspace, void* peer, wk_stream_t stream);
-int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
+int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, double* x, wk_cg_state* state, double* hist,
                              void* workspace, void* peer, const void* halo, wk_stream_t stream);
 
 /* ---- peer-memory communication for the row-block distributed solvers

@@ -117,7 +117,7 @@ _SIGS = {
     "wk_cg_spmv_dot_peer": (ctypes.c_int, [P, P, P, P, P, P, P, P]),
     "wk_cg_update_xr_alpha_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
     "wk_cg_replace_r_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
-    "wk_cg_update_p_beta_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
+    "wk_cg_update_p_beta_peer": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
     "wk_peer_allreduce": (ctypes.c_int, [P, P, P, I32, P]),
     "wk_peer_exchange": (ctypes.c_int, [P, P, I32, P, P, P, P, I32, P, P, P]),
     "wk_spmv_coo_f64": (ctypes.c_int, [I64, I64, I64, P, P, P, P, P, I32, P]),
@@ -170,7 +170,7 @@ _SIGS = {
     "wk_cg_replace_r": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_cg_step_beta": (ctypes.c_int, [P, P, P]),
     "wk_cg_update_xr_alpha": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
-    "wk_cg_update_p_beta": (ctypes.c_int, [I64, P, P, P, P, P, P]),
+    "wk_cg_update_p_beta": (ctypes.c_int, [I64, P, P, P, P, P, P, P]),
     "wk_cg_update_p": (ctypes.c_int, [I64, P, P, P, P]),
     "wk_bicg_init": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
     "wk_bicg_init_finish": (ctypes.c_int, [P, F64, I64, P, P]),

@@ -141,7 +141,7 @@ template <bool kAlphaIn>
 __global__ void __launch_bounds__(256)
 cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restrict__ q, double* __restrict__ x,
                  double* __restrict__ r, wk_cg_state* s, double* hist, RedWorkspace ws, int finalize,
-                 PeerCtx* peer, int rev = 0) {
+                 PeerCtx* peer, int rev = 0, int defer_x = 0) {
     if (s->done) return;
     double alpha;
     bool repl, brk = false;
@@ -158,6 +158,9 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
         repl = cg_replacing(s);
     }
     const int64_t n_eff = brk ? 0 : n;
+    // defer_x (distributed two-pass iteration): x += alpha p moves into the p
+    // update, which reads p anyway; replacement iterations need x here
+    const bool upd_x = !(defer_x && !repl);
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* p2 = reinterpret_cast<const double2*>(p);
     const double2* q2 = reinterpret_cast<const double2*>(q);
@@ -171,10 +174,14 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
         const int64_t k = rev ? np - 1 - kl : kl, k1 = rev ? np - 1 - (kl + T) : kl + T;
         // p is read again by the p update, which starts on the rows read here
         // last: a plain load (not evict-first) lets it hit L2
-        double2 pa = p2[k], xa = __ldcs(x2 + k), pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
-        if (h1) {
-            pb = p2[k1];
-            xb = __ldcs(x2 + k1);
+        double2 pa{0, 0}, xa{0, 0}, pb{0, 0}, xb{0, 0}, qa{0, 0}, ra{0, 0}, qb{0, 0}, rb{0, 0};
+        if (upd_x) {
+            pa = p2[k];
+            xa = __ldcs(x2 + k);
+            if (h1) {
+                pb = p2[k1];
+                xb = __ldcs(x2 + k1);
+            }
         }
         if (!repl) {
             qa = __ldcs(q2 + k);
@@ -184,13 +191,15 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
                 rb = __ldcs(r2 + k1);
             }
         }
-        xa.x = __dadd_rn(xa.x, __dmul_rn(alpha, pa.x));
-        xa.y = __dadd_rn(xa.y, __dmul_rn(alpha, pa.y));
-        __stcs(x2 + k, xa);
-        if (h1) {
-            xb.x = __dadd_rn(xb.x, __dmul_rn(alpha, pb.x));
-            xb.y = __dadd_rn(xb.y, __dmul_rn(alpha, pb.y));
-            __stcs(x2 + k1, xb);
+        if (upd_x) {
+            xa.x = __dadd_rn(xa.x, __dmul_rn(alpha, pa.x));
+            xa.y = __dadd_rn(xa.y, __dmul_rn(alpha, pa.y));
+            __stcs(x2 + k, xa);
+            if (h1) {
+                xb.x = __dadd_rn(xb.x, __dmul_rn(alpha, pb.x));
+                xb.y = __dadd_rn(xb.y, __dmul_rn(alpha, pb.y));
+                __stcs(x2 + k1, xb);
+            }
         }
         if (!repl) {
             ra.x = __dadd_rn(ra.x, -__dmul_rn(alpha, qa.x));
@@ -209,7 +218,7 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
     }
     if ((n_eff & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
         const int64_t i = n - 1;
-        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+        if (upd_x) x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
         if (!repl) {
             r[i] = __dadd_rn(r[i], -__dmul_rn(alpha, q[i]));
             acc += __dmul_rn(r[i], r[i]);
@@ -242,31 +251,42 @@ cg_update_xr_vec(int64_t n, const double* __restrict__ p, const double* __restri
 template <bool kBetaIn>
 __global__ void __launch_bounds__(256)
 cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p, wk_cg_state* s, double* hist,
-                RedWorkspace ws, PeerCtx* peer, const PeerHalo* halo, int rev = 0) {
+                RedWorkspace ws, PeerCtx* peer, const PeerHalo* halo, int rev = 0, double* __restrict__ x = nullptr) {
     if (s->done) return;
     double rr = 0.0;
     if (kBetaIn) rr = (peer != nullptr) ? peer_wait_sum_block(peer) : s->rr;
     const double beta = kBetaIn ? rr / s->rho : s->beta;
+    // x != nullptr (distributed two-pass iteration): the x += alpha p_old the
+    // x/r update deferred, on every iteration but the residual replacement
+    const bool upd_x = x != nullptr && !cg_replacing(s);
+    const double alpha = s->alpha;
     const int64_t np = n >> 1, T = int64_t(gridDim.x) * 256;
     const double2* r2 = reinterpret_cast<const double2*>(r);
     double2* p2 = reinterpret_cast<double2*>(p);
+    double2* x2 = reinterpret_cast<double2*>(x);
     // four pairs of r and p in flight per thread (a copy-shaped step: two
     // pairs left it at 5.7 TB/s)
     constexpr int U = 4;
     for (int64_t kl = int64_t(blockIdx.x) * 256 + threadIdx.x; kl < np; kl += U * T) {
-        double2 ra[U], pa[U];
+        double2 ra[U], pa[U], xa[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t ku = kl + u * T;
             const int64_t k = rev ? np - 1 - ku : ku;
             ra[u] = ku < np ? __ldcs(r2 + k) : make_double2(0.0, 0.0);
             pa[u] = ku < np ? p2[k] : make_double2(0.0, 0.0);
+            xa[u] = ku < np && upd_x ? __ldcs(x2 + k) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t ku = kl + u * T;
             if (ku >= np) break;
             const int64_t k = rev ? np - 1 - ku : ku;
+            if (upd_x) {
+                xa[u].x = __dadd_rn(xa[u].x, __dmul_rn(alpha, pa[u].x));
+                xa[u].y = __dadd_rn(xa[u].y, __dmul_rn(alpha, pa[u].y));
+                __stcs(x2 + k, xa[u]);
+            }
             double2 q;
             q.x = __dadd_rn(ra[u].x, __dmul_rn(beta, pa[u].x));
             q.y = __dadd_rn(ra[u].y, __dmul_rn(beta, pa[u].y));
@@ -278,6 +298,7 @@ cg_update_p_vec(int64_t n, const double* __restrict__ r, double* __restrict__ p,
         }
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (upd_x) x[n - 1] = __dadd_rn(x[n - 1], __dmul_rn(alpha, p[n - 1]));
         p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
         if (halo != nullptr) halo_store(peer, halo, n - 1, p[n - 1]);
     }
@@ -598,18 +619,18 @@ int wk_cg_update_xr_alpha(int64_t n, const double* p, const double* q, double* x
                           void* workspace, wk_stream_t stream) {
     clear_error();
     WK_REQUIRE(vec_ok(p, q, x, r), WK_ERR_INVALID, "wk_cg_update_xr_alpha needs 16-byte aligned vectors");
-    cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, p, q, x, r, state, nullptr,
-                                                                                  red_ws(workspace), 0, nullptr);
+    cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
+        n, p, q, x, r, state, nullptr, red_ws(workspace), 0, nullptr, 0, 1);
     WK_LAUNCH_CHECK();
     return 0;
 }
 
-int wk_cg_update_p_beta(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist, void* workspace,
-                        wk_stream_t stream) {
+int wk_cg_update_p_beta(int64_t n, const double* r, double* p, double* x, wk_cg_state* state, double* hist,
+                        void* workspace, wk_stream_t stream) {
     clear_error();
-    WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta needs 16-byte aligned vectors");
-    cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(n, r, p, state, hist,
-                                                                                 red_ws(workspace), nullptr, nullptr);
+    WK_REQUIRE(vec_ok(r, p, x, p), WK_ERR_INVALID, "wk_cg_update_p_beta needs 16-byte aligned vectors");
+    cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
+        n, r, p, state, hist, red_ws(workspace), nullptr, nullptr, 0, x);
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -643,7 +664,7 @@ int wk_cg_update_xr_alpha_peer(int64_t n, const double* p, const double* q, doub
     clear_error();
     WK_REQUIRE(vec_ok(p, q, x, r), WK_ERR_INVALID, "wk_cg_update_xr_alpha_peer needs 16-byte aligned vectors");
     cg_update_xr_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
-        n, p, q, x, r, state, nullptr, red_ws(workspace), 0, reinterpret_cast<PeerCtx*>(peer));
+        n, p, q, x, r, state, nullptr, red_ws(workspace), 0, reinterpret_cast<PeerCtx*>(peer), 0, 1);
     WK_LAUNCH_CHECK();
     return 0;
 }
@@ -659,13 +680,13 @@ int wk_cg_replace_r_peer(int64_t n, const double* b, const double* q, double* r,
     return cg_replace_r(n, b, q, r, state, nullptr, workspace, false, as_stream(stream), pc);
 }
 
-int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, wk_cg_state* state, double* hist,
+int wk_cg_update_p_beta_peer(int64_t n, const double* r, double* p, double* x, wk_cg_state* state, double* hist,
                              void* workspace, void* peer, const void* halo, wk_stream_t stream) {
     clear_error();
-    WK_REQUIRE(vec_ok(r, p, r, p), WK_ERR_INVALID, "wk_cg_update_p_beta_peer needs 16-byte aligned vectors");
+    WK_REQUIRE(vec_ok(r, p, x, p), WK_ERR_INVALID, "wk_cg_update_p_beta_peer needs 16-byte aligned vectors");
     cg_update_p_vec<true><<<vec_grid(n > 0 ? n : 1), 256, 0, as_stream(stream)>>>(
         n, r, p, state, hist, red_ws(workspace), reinterpret_cast<PeerCtx*>(peer),
-        reinterpret_cast<const PeerHalo*>(halo));
+        reinterpret_cast<const PeerHalo*>(halo), 0, x);
     WK_LAUNCH_CHECK();
     return 0;
 }

@@ -605,7 +605,7 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None, fused=True):
                 ops.spmv_masked(op.local, x, q, st)
                 ops.cg("wk_cg_replace_r", n, b, q, r, st)
             comm.allreduce_(f64[_RR:_RR + 1])
-            ops.cg("wk_cg_update_p_beta", n, r, p, st, hist)
+            ops.cg("wk_cg_update_p_beta", n, r, p, x, st, hist)
 
     halo = op.peer_halo(p) if (op.peer is not None and fused) else None
 
@@ -625,7 +625,7 @@ def cg_solve(op: DistOperator, b_local, tol, max_iters, graph=None, fused=True):
                 op.exchange(x)
                 ops.spmv_masked(op.local, x, q, st)
                 ops.step("wk_cg_replace_r_peer", n, b, q, r, st, ops.ws.red, pc)
-            ops.step("wk_cg_update_p_beta_peer", n, r, p, st, hist, ops.ws.red, pc, halo)
+            ops.step("wk_cg_update_p_beta_peer", n, r, p, x, st, hist, ops.ws.red, pc, halo)
 
     if op.peer is not None and fused:
         period = period_fused  # noqa: F811

@@ -143,12 +143,23 @@ class NumpyOps:
             s(st, "rho", rr)
             s(st, "done", int(not (it < g(st, "max_iters") and math.sqrt(rr) > g(st, "threshold"))))
         elif name == "wk_cg_update_xr_alpha":
+            # x += alpha p only on replacement iterations (else in the p update)
             self.cg("wk_cg_step_alpha", a[5])
-            self.cg("wk_cg_update_xr", *a)
-        elif name == "wk_cg_update_p_beta":
-            n, r, p, st, hist = a
+            n, p, q, x, r, st = a
             if g(st, "done"):
                 return
+            al = g(st, "alpha")
+            if g(st, "iteration") % 50 == 0:
+                x[:n] = x[:n] + al * p[:n]
+            else:
+                r[:] = r - al * q[:n]
+                s(st, "rr", float(r.numpy() @ r.numpy()))
+        elif name == "wk_cg_update_p_beta":
+            n, r, p, x, st, hist = a
+            if g(st, "done"):
+                return
+            if g(st, "iteration") % 50 != 0:
+                x[:n] = x[:n] + g(st, "alpha") * p[:n]
             beta = g(st, "rr") / g(st, "rho")
             p[:n] = r + beta * p[:n]
             self.cg("wk_cg_step_beta", st, hist)
