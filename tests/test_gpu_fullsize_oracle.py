@@ -8,11 +8,12 @@ each device y over ALL rows, not a sample:
 
   cfg 1: 5-point Poisson 1000^2   CSR arrays bitwise; y bitwise (every
                                   sequential-fold CSR kernel)
-  cfg 2: 27-point 200^3           CSR + SELL-P(64) arrays bitwise; y bitwise
+  cfg 2: 27-point 200^3           CSR + SELL-P(64) + ELL arrays bitwise; y bitwise
                                   for SELL-P / ELL / CSR rowblock + stream,
                                   1e-12 scaled for the reassociating CSR kernels
   cfg 3: R-MAT scale 24           raw edges, device radix sort and dedup ->
-                                  COO arrays bitwise (268M edges); y: CSR
+                                  COO arrays bitwise (268M edges), Hybrid(4)
+                                  ELL part + COO remainder bitwise; y: CSR
                                   rowblock bitwise on rows <= 64 entries, COO /
                                   load_balance / merge / Hybrid (and rowblock's
                                   long rows) within 1e-12 scaled
@@ -25,6 +26,7 @@ max(1, |y_ref|) per row, sparse_ref.max_scaled_rel_err.
 
 import numpy as np
 import pytest
+from types import SimpleNamespace
 
 torch = pytest.importorskip("torch")
 
@@ -65,6 +67,35 @@ def _same_csr(dev, host):
     assert np.array_equal(_h(dev.row_ptrs).astype(np.int64), host.row_ptrs)
     assert np.array_equal(_h(dev.col_idx), host.col_idx)
     assert _h(dev.values).tobytes() == host.values.tobytes()
+
+
+def _entry_pos(ptrs):
+    """Position of every CSR entry inside its row."""
+    ptrs = np.asarray(ptrs, dtype=np.int64)
+    lens = np.diff(ptrs)
+    return np.arange(ptrs[-1], dtype=np.int64) - np.repeat(ptrs[:-1], lens)
+
+
+def _same_ell(ell, csr, width=None):
+    """ELL(width, stride) image of a host CSR (sparse.py:233-241 layout with
+    one slice of stride n: entry j of row r at j * stride + r, padding (0,
+    0.0); entries past `width` excluded)."""
+    ptrs = np.asarray(csr.row_ptrs, dtype=np.int64)
+    n = len(ptrs) - 1
+    lens = np.diff(ptrs)
+    w = int(lens.max()) if width is None else int(width)
+    assert ell.width == w
+    pos = _entry_pos(ptrs)
+    rows = np.repeat(np.arange(n, dtype=np.int64), lens)
+    m = pos < w
+    slot = pos[m] * ell.stride + rows[m]
+    col = np.zeros(w * ell.stride, dtype=np.int32)
+    val = np.zeros(w * ell.stride, dtype=np.float64)
+    col[slot] = np.asarray(csr.col_idx)[m]
+    val[slot] = np.asarray(csr.values)[m]
+    assert np.array_equal(_h(ell.col_idx)[: w * ell.stride], col)
+    assert _h(ell.values)[: w * ell.stride].tobytes() == val.tobytes()
+    assert np.array_equal(_h(ell.row_lengths_t).astype(np.int64), np.minimum(lens, w))
 
 
 def _bitwise(y, ref, what):
@@ -115,6 +146,7 @@ def test_cfg2_27pt_200_whole_vector(wk):
     _bitwise(_spmv(sp, xd), ref, "sellp64")
     del sp
     ell = D.csr_to_ell(A)
+    _same_ell(ell, H)
     _bitwise(_spmv(ell, xd), ref, "ell")
     del ell
     for strat in ("rowblock", "stream"):
@@ -140,6 +172,8 @@ def test_cfg3_rmat24_whole_pipeline(wk):
     hp = native.Prepared(H)
     ref = hp.spmv(x)
     lens = np.bincount(H.row_idx, minlength=H.nrows)
+    ptrs = np.concatenate([[0], np.cumsum(lens)])
+    hrow, hcol, hval = H.row_idx, H.col_idx, H.values
     del hp, H
     _close(_spmv(R, xd), ref, lens, "coo")
     C = D.coo_to_csr(R)
@@ -154,6 +188,13 @@ def test_cfg3_rmat24_whole_pipeline(wk):
         C.with_strategy(strat)
         _close(_spmv(C, xd), ref, lens, strat)
     Hy = D.csr_to_hybrid(C, width=4)
+    # conversion arrays: the ELL part holds each row's first 4 entries, the COO
+    # remainder the rest in row-major order (sparse_ref.csr_to_hybrid)
+    _same_ell(Hy.ell, SimpleNamespace(row_ptrs=ptrs, col_idx=hcol, values=hval), width=4)
+    keep = _entry_pos(ptrs) >= 4
+    assert np.array_equal(_h(Hy.coo.row_idx), hrow[keep])
+    assert np.array_equal(_h(Hy.coo.col_idx), hcol[keep])
+    assert _h(Hy.coo.values).tobytes() == hval[keep].tobytes()
     _close(_spmv(Hy, xd), ref, lens, "hybrid")
 
 
