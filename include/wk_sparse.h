@@ -410,6 +410,19 @@ int wk_gmres_next_basis(int64_t n, const double* w, double* Vn, wk_gmres_state* 
 int wk_gmres_update_x(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y,
                       double* x, wk_gmres_state* st, wk_stream_t stream);
 /* r = b - w (w = A x) ; sq = r.r (local) */
+/* Deferred normalisation (what wk_gmres_solve runs): basis slot i holds u_i
+ * with v_i = sig[i] u_i (sig[0] = 1, so cycle_start is unchanged). The SpMV
+ * writes z = A u_j into slot j+1 and wk_gmres_multidot leaves u_i . z in Hj
+ * (all-reduce it when distributed); wk_gmres_orth_scaled turns Hj into
+ * h_i = sig_i sig_j (u_i . z) and slot j+1 into w = sig_j z - sum h_i sig_i u_i,
+ * local ||w||^2 in sq; wk_gmres_givens_scaled also sets sig[j+1] = 1 / ||w||;
+ * wk_gmres_update_x_scaled adds sum (y_i sig_i) u_i. No next_basis pass. */
+int wk_gmres_orth_scaled(int64_t n, int32_t j, const double* V, int64_t ld, double* w, double* Hj, const double* sig,
+                         wk_gmres_state* st, void* workspace, wk_stream_t stream);
+int wk_gmres_givens_scaled(int32_t j, double* H, double* cs, double* sn, double* g, double* sig, wk_gmres_state* st,
+                           double* hist, wk_stream_t stream);
+int wk_gmres_update_x_scaled(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y,
+                             double* x, const double* sig, wk_gmres_state* st, wk_stream_t stream);
 int wk_gmres_residual(int64_t n, const double* b, const double* w, double* r, wk_gmres_state* st, void* workspace,
                       wk_stream_t stream);
 /* after all-reduce of sq: beta, true residual replaces the last history entry, convergence */

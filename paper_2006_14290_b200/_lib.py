@@ -194,6 +194,9 @@ _SIGS = {
     "wk_gmres_givens": (ctypes.c_int, [I32, P, P, P, P, P, P, P]),
     "wk_gmres_next_basis": (ctypes.c_int, [I64, P, P, P, P]),
     "wk_gmres_update_x": (ctypes.c_int, [I64, P, I64, P, P, P, P, P, P]),
+    "wk_gmres_orth_scaled": (ctypes.c_int, [I64, I32, P, I64, P, P, P, P, P, P]),
+    "wk_gmres_givens_scaled": (ctypes.c_int, [I32, P, P, P, P, P, P, P, P]),
+    "wk_gmres_update_x_scaled": (ctypes.c_int, [I64, P, I64, P, P, P, P, P, P, P]),
     "wk_gmres_residual": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_gmres_restart": (ctypes.c_int, [P, P, P]),
 }

@@ -820,6 +820,24 @@ int wk_gmres_givens(int32_t j, double* H, double* cs, double* sn, double* g, wk_
     clear_error();
     return gmres_givens(j, H, cs, sn, g, s, hist, as_stream(stream));
 }
+// deferred normalisation (basis slot i holds u_i, v_i = sig[i] u_i; sig[0] = 1)
+int wk_gmres_orth_scaled(int64_t n, int32_t j, const double* V, int64_t ld, double* w, double* Hj, const double* sig,
+                         wk_gmres_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(j >= 0 && j + 1 <= kRedMaxVec, WK_ERR_INVALID, "GMRES restart must be < %d", kRedMaxVec);
+    WK_REQUIRE(cgs_vec_ok(V, ld, w), WK_ERR_INVALID, "wk_gmres_orth_scaled needs 16-byte aligned V, w and even ld");
+    return gmres_orth_scaled(n, j, V, ld, w, Hj, sig, s, ws, as_stream(stream));
+}
+int wk_gmres_givens_scaled(int32_t j, double* H, double* cs, double* sn, double* g, double* sig, wk_gmres_state* s,
+                           double* hist, wk_stream_t stream) {
+    clear_error();
+    return gmres_givens(j, H, cs, sn, g, s, hist, as_stream(stream), sig);
+}
+int wk_gmres_update_x_scaled(int64_t n, const double* V, int64_t ld, const double* H, const double* g, double* y,
+                             double* x, const double* sig, wk_gmres_state* s, wk_stream_t stream) {
+    clear_error();
+    return gmres_update_x(n, V, ld, H, g, y, x, s, as_stream(stream), sig);
+}
 int wk_gmres_next_basis(int64_t n, const double* w, double* Vn, wk_gmres_state* s, wk_stream_t stream) {
     clear_error();
     return gmres_next_basis(n, w, Vn, s, as_stream(stream));

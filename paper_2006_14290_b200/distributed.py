@@ -762,7 +762,8 @@ def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=Non
     """Row-block distributed restarted GMRES(m) with classical Gram-Schmidt:
     per Arnoldi step one halo exchange, one all-reduce of the j+1 batched dots
     and one of ||w||^2; Givens rotations on one device thread (replicated on
-    every rank). One cycle per CUDA-graph period. Returns (x_local, hist)."""
+    every rank); the basis is normalised lazily (per-vector scales, no
+    rescaling pass). One cycle per CUDA-graph period. Returns (x_local, hist)."""
     ops, comm = op.ops, op.comm
     n, n_ext = op.n_local, op.n_local + op.n_halo
     m = int(restart)
@@ -778,6 +779,7 @@ def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=Non
     w, r = ops.zeros(n), ops.zeros(n)
     H = ops.zeros((m + 1) * m)
     cs, sn, g, y = ops.zeros(m + 1), ops.zeros(m + 1), ops.zeros(m + 1), ops.zeros(m + 1)
+    sig = ops.zeros(m + 1) + 1.0  # basis scales (deferred normalisation): v_i = sig[i] u_i, sig[0] = 1
     hist = ops.zeros(int(max_iters) + 1)
     st = ops.new_struct(C)
     f = st.view(torch.float64)
@@ -789,20 +791,21 @@ def gmres_solve(op: DistOperator, b_local, tol, max_iters, restart=30, graph=Non
     ops.step("wk_gmres_init_finish", st, float(tol), int(max_iters), m, hist)
 
     def period():
+        # deferred normalisation (as wk_gmres_solve): A u_j lands in basis slot
+        # j+1 and is orthogonalised there; the scales live in `sig`
         ops.step("wk_gmres_cycle_start", n, r, V[:n_ext], g, st)
         for j in range(m):
             Vj = V[j * ld: j * ld + n_ext]
+            z = V[(j + 1) * ld: (j + 1) * ld + n]
             Hj = H[j * (m + 1): j * (m + 1) + m + 1]
             op.exchange(Vj)
-            ops.spmv_flag(op.local, Vj, w, st, cdone)
-            ops.step("wk_gmres_multidot", n, j, V, ld, w, Hj, st, ws=True)
+            ops.spmv_flag(op.local, Vj, z, st, cdone)
+            ops.step("wk_gmres_multidot", n, j, V, ld, z, Hj, st, ws=True)
             comm.allreduce_(Hj[: j + 1])
-            ops.step("wk_gmres_orth", n, j, V, ld, w, Hj, st, ws=True)
+            ops.step("wk_gmres_orth_scaled", n, j, V, ld, z, Hj, sig, st, ws=True)
             comm.allreduce_(f[sq:sq + 1])
-            ops.step("wk_gmres_givens", j, H, cs, sn, g, st, hist)
-            if j + 1 < m:
-                ops.step("wk_gmres_next_basis", n, w, V[(j + 1) * ld: (j + 1) * ld + n_ext], st)
-        ops.step("wk_gmres_update_x", n, V, ld, H, g, y, x, st)
+            ops.step("wk_gmres_givens_scaled", j, H, cs, sn, g, sig, st, hist)
+        ops.step("wk_gmres_update_x_scaled", n, V, ld, H, g, y, x, sig, st)
         op.exchange(x)
         ops.spmv_flag(op.local, x, w, st, done)
         ops.step("wk_gmres_residual", n, b_local, w, r, st, ws=True)

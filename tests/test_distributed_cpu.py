@@ -277,7 +277,8 @@ def _bicg_step(name, *a):
 def _gmres_step(name, *a):
     """krylov_steps.cu gmres_* (wk_gmres_state via ctypes.from_buffer)."""
     idx = {"init": 4, "init_finish": 0, "cycle_start": 4, "multidot": 6, "orth": 6, "givens": 5,
-           "next_basis": 3, "update_x": 7, "residual": 4, "restart": 0}[name]
+           "next_basis": 3, "update_x": 7, "residual": 4, "restart": 0, "orth_scaled": 7, "givens_scaled": 6,
+           "update_x_scaled": 8}[name]
     s = _lib.WkGmresState.from_buffer(a[idx].numpy())
     if name == "init":
         n, b, x, r, _ = a
@@ -311,6 +312,34 @@ def _gmres_step(name, *a):
             for q in range(j + 1):
                 w[:n] = w[:n] - float(Hj[q]) * V[q * ld: q * ld + n]
             s.sq = _dot(w[:n], w[:n])
+    elif name == "orth_scaled":
+        n, j, V, ld, w, Hj, sig, _ = a
+        if not s.cycle_done:
+            sj = float(sig[j])
+            h = [float(sig[q]) * sj * float(Hj[q]) for q in range(j + 1)]
+            w[:n] = sj * w[:n]
+            for q in range(j + 1):
+                w[:n] = w[:n] - h[q] * float(sig[q]) * V[q * ld: q * ld + n]
+                Hj[q] = h[q]
+            s.sq = _dot(w[:n], w[:n])
+    elif name == "givens_scaled":
+        j, H, cs, sn, g, sig, st, hist = a
+        if not s.cycle_done:
+            hn = math.sqrt(s.sq)
+            sig[j + 1] = 1.0 / hn if hn != 0.0 else 0.0
+        _gmres_step("givens", j, H, cs, sn, g, st, hist)
+    elif name == "update_x_scaled":
+        n, V, ld, H, g, y, x, sig, st = a
+        if s.done:
+            return
+        m, jd = s.restart, s.j_done
+        for i in range(jd - 1, -1, -1):
+            acc = float(g[i])
+            for k in range(i + 1, jd):
+                acc = acc - float(H[i + k * (m + 1)]) * float(y[k])
+            y[i] = acc / float(H[i + i * (m + 1)])
+        for q in range(jd):
+            x[:n] = x[:n] + float(y[q]) * float(sig[q]) * V[q * ld: q * ld + n]
     elif name == "givens":
         j, H, cs, sn, g, _, hist = a
         if s.cycle_done:
