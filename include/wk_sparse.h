@@ -377,6 +377,18 @@ int wk_bicg_update_xr(int64_t n, const double* p, const double* s, const double*
                       wk_bicg_state* st, void* workspace, wk_stream_t stream);
 /* after all-reduce of rr: hist, rho = rho_new, convergence */
 int wk_bicg_step_r(wk_bicg_state* st, double* hist, wk_stream_t stream);
+/* fused steps (what wk_bicgstab_solve runs): v = A p with rv = r-hat.v
+ * (mode 1, w = r-hat) or t = A s with tt, ts (mode 2, x = s extended, its
+ * own rows read) in one SpMV when A is aligned SELL-P(64), else SpMV + dot;
+ * rho_first: rho_next = r-hat.r; take_rho: rho_new = rho_next; update_xr_rho:
+ * the x/r update with rr and rho_next = r-hat.r (new r) summed together */
+int wk_bicg_spmv_dots(const wk_matrix* A, const double* x, double* y, wk_bicg_state* st, const double* w, int32_t mode,
+                      void* workspace, wk_stream_t stream);
+int wk_bicg_rho_first(int64_t n, const double* rh, const double* r, wk_bicg_state* st, void* workspace,
+                      wk_stream_t stream);
+int wk_bicg_take_rho(wk_bicg_state* st, wk_stream_t stream);
+int wk_bicg_update_xr_rho(int64_t n, const double* p, const double* sv, const double* t, const double* rh, double* x,
+                          double* r, wk_bicg_state* st, void* workspace, wk_stream_t stream);
 
 /* ---- GMRES(m) building blocks (classical Gram-Schmidt; oracle order).
  *      H is (m+1) x m column-major; cs, sn: m; g: m+1; y: m. --------------- */

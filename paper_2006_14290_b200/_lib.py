@@ -186,6 +186,10 @@ _SIGS = {
     "wk_bicg_step_omega": (ctypes.c_int, [P, P]),
     "wk_bicg_update_xr": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P]),
     "wk_bicg_step_r": (ctypes.c_int, [P, P, P]),
+    "wk_bicg_spmv_dots": (ctypes.c_int, [P, P, P, P, P, I32, P, P]),
+    "wk_bicg_rho_first": (ctypes.c_int, [I64, P, P, P, P, P]),
+    "wk_bicg_take_rho": (ctypes.c_int, [P, P]),
+    "wk_bicg_update_xr_rho": (ctypes.c_int, [I64, P, P, P, P, P, P, P, P, P]),
     "wk_gmres_init": (ctypes.c_int, [I64, P, P, P, P, P, P]),
     "wk_gmres_init_finish": (ctypes.c_int, [P, F64, I64, I32, P, P]),
     "wk_gmres_cycle_start": (ctypes.c_int, [I64, P, P, P, P, P]),

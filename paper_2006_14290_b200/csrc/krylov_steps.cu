@@ -785,6 +785,37 @@ int wk_bicg_update_xr(int64_t n, const double* p, const double* sv, const double
     clear_error();
     return bicg_update_xr(n, p, sv, t, x, r, s, ws, as_stream(stream));
 }
+// Fused steps of wk_bicgstab_solve for the distributed solver: v = A p with
+// r-hat.v (mode 1) / t = A s with t.t and t.s (mode 2) summed in the SpMV when
+// the operand takes it (SELL-P(64), aligned), else SpMV + dot kernel; the x/r
+// update with the next r-hat.r summed in the same pass (all-reduce rr and
+// rho_next together afterwards), and the rho hand-over.
+int wk_bicg_spmv_dots(const wk_matrix* A, const double* x, double* y, wk_bicg_state* s, const double* w, int32_t mode,
+                      void* ws, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(mode == 1 || mode == 2, WK_ERR_INVALID, "mode must be 1 (r-hat.v) or 2 (t.t, t.s)");
+    cudaStream_t st = as_stream(stream);
+    const int rc = spmv_bicg_fused(A, x, y, s, w, mode, ws, st);
+    if (rc != 1) return rc;
+    WK_TRY(wk_spmv_masked(A, x, y, &s->done, stream));
+    return mode == 1 ? bicg_rv(A->nrows, w, y, s, ws, st) : bicg_tt_ts(A->nrows, y, x, s, ws, st);
+}
+int wk_bicg_rho_first(int64_t n, const double* rh, const double* r, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(n > 0 && vmap_ok({rh, r}), WK_ERR_INVALID, "wk_bicg_rho_first needs 16-byte aligned vectors");
+    return bicg_rho_first(n, rh, r, s, ws, as_stream(stream));
+}
+int wk_bicg_take_rho(wk_bicg_state* s, wk_stream_t stream) {
+    clear_error();
+    return bicg_take_rho(s, as_stream(stream));
+}
+int wk_bicg_update_xr_rho(int64_t n, const double* p, const double* sv, const double* t, const double* rh, double* x,
+                          double* r, wk_bicg_state* s, void* ws, wk_stream_t stream) {
+    clear_error();
+    WK_REQUIRE(n > 0 && vmap_ok({p, sv, t, rh, x, r}), WK_ERR_INVALID,
+               "wk_bicg_update_xr_rho needs 16-byte aligned vectors");
+    return bicg_update_xr_rho(n, p, sv, t, rh, x, r, s, ws, as_stream(stream));
+}
 int wk_bicg_step_r(wk_bicg_state* s, double* hist, wk_stream_t stream) {
     clear_error();
     return bicg_step_r(s, hist, as_stream(stream));

@@ -177,6 +177,12 @@ class DeviceOps:
         flag = ctypes.c_void_p(state.data_ptr() + offset)
         _lib.call("wk_spmv_masked", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), flag, self.stream())
 
+    def bicg_spmv_dots(self, local, x_ext, y, state, w, mode):
+        """BiCGSTAB SpMV with its local dot(s) fused (mode 1: r-hat.v into rv,
+        mode 2: t.t / t.s into tt / ts; wk_bicg_spmv_dots)."""
+        _lib.call("wk_bicg_spmv_dots", local.wk_ptr(), D._ptr(x_ext), D._ptr(y), D._ptr(state),
+                  D._ptr(w) if w is not None else None, mode, D._ptr(self.ws.red), self.stream())
+
 
 # ---- partition plans ----------------------------------------------------------------------------
 
@@ -700,9 +706,10 @@ def _run_periods(ops, comm, st, cls, period, graph):
 
 
 def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=10):
-    """Row-block distributed BiCGSTAB (oracle/krylov_ref.py order): five
-    all-reduces per iteration (rh.r, rh.v, s.s, {t.t, t.s}, r.r) and two halo
-    exchanges (p before v = A p, s before t = A s). Returns (x_local, hist)."""
+    """Row-block distributed BiCGSTAB (oracle/krylov_ref.py order): four
+    all-reduces per iteration (rh.v, s.s, {t.t, t.s}, {r.r, next rh.r}) and two
+    halo exchanges (p before v = A p, s before t = A s); the dots are summed
+    inside the SpMVs and the x/r update. Returns (x_local, hist)."""
     ops, comm = op.ops, op.comm
     n = op.n_local
     if tol <= 0:
@@ -724,16 +731,19 @@ def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=
     ops.step("wk_bicg_init", n, b_local, x, r, rh, p, v, st, ws=True)
     red("rr")
     ops.step("wk_bicg_init_finish", st, float(tol), int(max_iters), hist)
+    # the fused order of wk_bicgstab_solve: r-hat.v / t.t, t.s summed inside the
+    # SpMVs, r-hat.r of the next iteration inside the x/r update (all-reduced
+    # together with r.r): four all-reduces per iteration instead of five
+    ops.step("wk_bicg_rho_first", n, rh, r, st, ws=True)
+    red("rho_next")
 
     def period():
         for _ in range(chunk):
-            ops.step("wk_bicg_rho", n, rh, r, st, ws=True)
-            red("rho_new")
+            ops.step("wk_bicg_take_rho", st)
             ops.step("wk_bicg_step_beta", st)
             ops.step("wk_bicg_update_p", n, r, v, p, st)
             op.exchange(p)
-            ops.spmv_flag(op.local, p, v, st, done)
-            ops.step("wk_bicg_rv", n, rh, v, st, ws=True)
+            ops.bicg_spmv_dots(op.local, p, v, st, rh, 1)
             red("rv")
             ops.step("wk_bicg_step_alpha", st)
             ops.step("wk_bicg_update_s", n, r, v, sv, st, ws=True)
@@ -741,12 +751,11 @@ def bicgstab_solve(op: DistOperator, b_local, tol, max_iters, graph=None, chunk=
             ops.step("wk_bicg_step_s", st, hist)
             ops.step("wk_bicg_half_x", n, p, x, st, ws=True)
             op.exchange(sv)
-            ops.spmv_flag(op.local, sv, t, st, done)
-            ops.step("wk_bicg_tt_ts", n, t, sv, st, ws=True)
+            ops.bicg_spmv_dots(op.local, sv, t, st, None, 2)
             red("tt", "ts")
             ops.step("wk_bicg_step_omega", st)
-            ops.step("wk_bicg_update_xr", n, p, sv, t, x, r, st, ws=True)
-            red("rr")
+            ops.step("wk_bicg_update_xr_rho", n, p, sv, t, rh, x, r, st, ws=True)
+            red("rr", "rho_next")
             ops.step("wk_bicg_step_r", st, hist)
 
     h = _run_periods(ops, comm, st, C, period, graph)

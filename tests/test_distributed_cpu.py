@@ -75,6 +75,14 @@ class NumpyOps:
         if int(np.frombuffer(state.numpy().tobytes()[offset:offset + 4], dtype=np.int32)[0]) == 0:
             self.spmv(local, x_ext, y)
 
+    def bicg_spmv_dots(self, local, x_ext, y, state, w, mode):
+        self.spmv_flag(local, x_ext, y, state, _lib.WkBicgState.done.offset)
+        n = local.nrows
+        if mode == 1:
+            _bicg_step("rv", n, w, y, state)
+        else:
+            _bicg_step("tt_ts", n, y, x_ext, state)
+
     def step(self, name, *a, ws=False):
         """BiCGSTAB / GMRES step kernels of csrc/krylov_steps.cu restated
         (same statement order; the state struct is edited in place)."""
@@ -177,8 +185,9 @@ def _dot(a, b):
 
 def _bicg_step(name, *a):
     """krylov_steps.cu bicg_* (wk_bicg_state via ctypes.from_buffer)."""
-    st = a[-1] if name in ("init", "rho", "update_p", "rv", "update_s", "half_x", "tt_ts", "update_xr") else None
-    if name in ("init_finish", "step_beta", "step_alpha", "step_s", "step_omega", "step_r"):
+    st = a[-1] if name in ("init", "rho", "update_p", "rv", "update_s", "half_x", "tt_ts", "update_xr",
+                           "rho_first", "update_xr_rho") else None
+    if name in ("init_finish", "step_beta", "step_alpha", "step_s", "step_omega", "step_r", "take_rho"):
         st = a[0]
     s = _lib.WkBicgState.from_buffer(st.numpy())
     if name == "init":
@@ -262,6 +271,20 @@ def _bicg_step(name, *a):
             x[:n] = (x[:n] + s.alpha * p[:n]) + s.omega * sv[:n]
             r[:n] = sv[:n] - s.omega * t[:n]
             s.rr = _dot(r[:n], r[:n])
+    elif name == "rho_first":
+        n, rh, r, _ = a
+        if not s.done:
+            s.rho_next = _dot(rh[:n], r[:n])
+    elif name == "take_rho":
+        if not s.done:
+            s.rho_new = s.rho_next
+    elif name == "update_xr_rho":
+        n, p, sv, t, rh, x, r, _ = a
+        if not s.done:
+            x[:n] = (x[:n] + s.alpha * p[:n]) + s.omega * sv[:n]
+            r[:n] = sv[:n] - s.omega * t[:n]
+            s.rr = _dot(r[:n], r[:n])
+            s.rho_next = _dot(rh[:n], r[:n])
     elif name == "step_r":
         _, hist = a
         if s.done:

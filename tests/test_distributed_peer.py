@@ -54,7 +54,7 @@ def _worker(rank, world, port, out):
             errs = [None, None]
             dist.all_gather_object(errs, res["err0"])
             if any(errs):  # the device cannot interleave the two contexts: stop early, the test reports it
-                res.update(err1=-1, err2=-1)
+                res.update(err1=-1, err2=-1, err3=-1)
                 out[rank] = res
                 return
 
@@ -78,9 +78,18 @@ def _worker(rank, world, port, out):
         xs, hist = DI.gmres_solve(opn, bn, 1e-10, 500, restart=30)
         res["gmres_x"], res["gmres_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
         res["err2"] = int(opn.peer.error.item())
+        # SELL-P local blocks: BiCGSTAB's dots summed inside the SpMVs
+        # (wk_bicg_spmv_dots fused path), GMRES on the same operator
+        ops_ = DI.stencil_slab_operator(10, 10, None, corpus.points_7pt(6.0, corpus.CONV_DIFF_BETA), dist,
+                                        fmt="sellp", weak=False, nz=10).enable_peer()
+        xs, hist = DI.bicgstab_solve(ops_, bn, 1e-10, 500)
+        res["bicg_sellp_x"], res["bicg_sellp_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        xs, hist = DI.gmres_solve(ops_, bn, 1e-10, 500, restart=30)
+        res["gmres_sellp_x"], res["gmres_sellp_hist"] = xs.cpu().numpy(), hist.cpu().numpy()
+        res["err3"] = int(ops_.peer.error.item())
         torch.cuda.synchronize()
         dist.barrier()
-        for o in (op, opg, opn):
+        for o in (op, opg, opn, ops_):
             o.peer.close()
         out[rank] = res
     finally:
@@ -101,7 +110,7 @@ def parts():
 
 def test_peer_no_timeouts(parts):
     for p in parts:
-        assert (p["err0"], p["err1"], p["err2"]) == (0, 0, 0)
+        assert (p["err0"], p["err1"], p["err2"], p["err3"]) == (0, 0, 0, 0)
 
 
 def test_peer_spmv_bitwise(parts):
@@ -146,12 +155,12 @@ def test_peer_cg_graph(parts):
         assert np.array_equal(p["cg_x_unfused"], p["cg_x_True"])
 
 
-@pytest.mark.parametrize("solver", ["bicg", "gmres"])
+@pytest.mark.parametrize("solver", ["bicg", "gmres", "bicg_sellp", "gmres_sellp"])
 def test_peer_nonsymmetric(parts, solver):
     m = corpus_ref.stencil(10, 10, 10, corpus_ref.points_7pt(beta=(1.0, 0.5, 0.25)))
     b = np.ones(m.nrows)
     f = lambda v: sparse_ref.spmv(m, v)  # noqa: E731
-    if solver == "bicg":
+    if solver.startswith("bicg"):
         xr, hr = krylov_ref.bicgstab_solve(f, b, 1e-10, 500)
     else:
         xr, hr = krylov_ref.gmres_solve(f, b, 1e-10, 500, restart=30)
