@@ -36,6 +36,8 @@ cap cg_update_xp_pair0 cg_update_xp_pair 4 1 python tools/profile_cg.py 256 60
 cap cg_update_xp_pair1 cg_update_xp_pair 5 1 python tools/profile_cg.py 256 60
 cap sort_downsweep rs_downsweep 2 1 python tools/quick_sort.py 22
 cap sort_upsweep rs_upsweep 2 1 python tools/quick_sort.py 22
+cap dedup_scatter dedup_scatter 1 1 python tools/quick_ingest.py
+cap coo_ptrs coo_ptrs 1 1 python tools/quick_ingest.py
 cap hybrid_coo_fill hybrid_coo 0 2 python tools/quick_hybrid.py 22
 if [ -z "$ONLY" ]; then
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
