@@ -99,7 +99,12 @@ constexpr int kMgColSlots = kMgTile + 4;
 constexpr int kMgEndSlots = kMgTile + 1 + 4;
 constexpr size_t kMgStageBytes =
     (size_t(kMgValSlots) * 8 + size_t(kMgColSlots) * 4 + size_t(kMgEndSlots) * 4 + 127) / 128 * 128;
-constexpr int kMgStages = 2;
+// One stage: 33 KB of shared memory per CTA, five CTAs per SM (registers);
+// two stages (double-buffered TMA) left three CTAs per SM and fewer tiles'
+// x gathers in flight: R-MAT 24 3.93 -> 2.34 ms, 27-point 200^3 1.09 -> 1.00
+// ms (tools/merge_probe.py; 1024-item tiles: 2.14 / 1.28 ms, 4096: 2.57 /
+// 1.61 ms).
+constexpr int kMgStages = 1;
 constexpr size_t kMgSmem = kMgStages * kMgStageBytes + kMgStages * 8 + 256;
 
 struct MgTile {
@@ -136,9 +141,10 @@ __device__ __forceinline__ void mg_issue(const MgTile& g, int64_t nrows, const i
     if (br) bulk_g2s(stage + size_t(kMgValSlots) * 8 + size_t(kMgColSlots) * 4, ptrs + ra, br, bar);
 }
 
-// Persistent merge-path kernel: CTA b takes tiles b, b + grid, ...; the next
-// tile's operands stream in (cp.async.bulk, mbarrier complete_tx) while the
-// current one is folded.
+// Persistent merge-path kernel: CTA b takes tiles b, b + grid, ...; a tile's
+// operands stream in with cp.async.bulk (mbarrier complete_tx) as soon as the
+// previous tile's stage is free; the five CTAs of an SM overlap each other's
+// loads, gathers and folds.
 __global__ void __launch_bounds__(kMgThreads)
 csr_merge_kernel(int64_t nrows, int64_t nnz, int64_t ntiles, const int* __restrict__ ptrs,
                  const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,

@@ -24,9 +24,9 @@ namespace wk {
 constexpr int kCsrChunk = 256;
 constexpr int kCsrCap = 2 * kCsrChunk;
 
-template <int W, int S>
+template <int W, int S, int B = 1>
 struct CsrTmaCfg {
-    static constexpr int kW = W, kS = S;
+    static constexpr int kW = W, kS = S, kMinBlocks = B;
     static constexpr int kValSlots = kCsrCap + 2;   // 16-byte alignment slack
     static constexpr int kColSlots = kCsrCap + 4;
     static constexpr size_t kStageBytes = size_t(kValSlots) * 8 + size_t(kColSlots) * 4;
@@ -132,7 +132,7 @@ __device__ __forceinline__ void csr_long_part(int64_t L, int64_t lo, int64_t hi,
 }
 
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::kW * 32, 1)
+__global__ void __launch_bounds__(Cfg::kW * 32, Cfg::kMinBlocks)
 csr_tma_kernel(int64_t nrows, int64_t nnz, int64_t nchunks, const int* __restrict__ ptrs,
                const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ x,
                double* __restrict__ y, const int* __restrict__ first, double* __restrict__ partials,
@@ -313,7 +313,9 @@ int launch_csr_tma(int64_t nrows, int64_t nnz, int64_t nchunks, const int* ptrs,
                                      int(Cfg::kSmem)));
         attr_set[dev & 63] = true;
     }
-    int64_t grid = sm_count();
+    int per_sm = 0;  // persistent grid: every CTA the SM can hold
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tma_kernel<Cfg>, Cfg::kW * 32, Cfg::kSmem));
+    int64_t grid = int64_t(sm_count()) * (per_sm > 0 ? per_sm : 1);
     const int64_t need = ceil_div(nchunks, Cfg::kW);
     if (grid > need) grid = need;
     csr_tma_kernel<Cfg><<<(unsigned)grid, Cfg::kW * 32, Cfg::kSmem, st>>>(nrows, nnz, nchunks, ptrs, col, val, x, y,

@@ -458,7 +458,11 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
         WK_REQUIRE(first != nullptr && partials != nullptr && tickets != nullptr, WK_ERR_INVALID,
                    "csr stream strategy needs a plan (wk_csr_plan_build)");
         const int64_t nchunks = csr_stream_chunks(nnz);
-        return launch_csr_tma<CsrTmaCfg<16, 2>>(nrows, nnz, nchunks, ptrs, col, val, x, y, first, partials, tickets,
+        // 8 warps, one stage each, <= 80 registers: three CTAs per SM (24
+        // warps); 16 warps x 2 stages left one CTA per SM (94 registers,
+        // 200 KB): R-MAT 24 4.82 -> 2.29 ms, 27-point 0.995 -> 0.784 ms
+        // (tools/merge_probe.py stream; 64-register caps spill)
+        return launch_csr_tma<CsrTmaCfg<8, 1, 3>>(nrows, nnz, nchunks, ptrs, col, val, x, y, first, partials, tickets,
                                                 skip, st);
     }
     WK_REQUIRE(strategy == WK_CSR_SUBWARP, WK_ERR_INVALID, "unknown CSR strategy %d", strategy);
