@@ -452,6 +452,11 @@ int launch_csr(int64_t nrows, int64_t ncols, int64_t nnz, const int* ptrs, const
         const double need = 32.0 * double(nnz) / double(nrows) * 1.25;
         if (need <= 640.0) return launch_csr_rowblock<CsrRbCfg<24, 1, 640>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
         if (need <= 768.0) return launch_csr_rowblock<CsrRbCfg<20, 1, 768>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
+        // rows of up to ~26.9 entries on average, 4% slack (27-point stencils:
+        // 855-entry mean blocks): 896-entry stages fit 20 warps per SM, not 16
+        // (27-point 200^3: 0.441 -> 0.411 ms, tools/merge_probe.py rowblock)
+        if (32.0 * double(nnz) / double(nrows) * 1.04 <= 896.0)
+            return launch_csr_rowblock<CsrRbCfg<20, 1, 896>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
         return launch_csr_rowblock<CsrRbCfg<16, 1, 1024>>(nrows, nnz, ptrs, col, val, x, y, skip, st);
     }
     if (strategy == WK_CSR_STREAM) {
