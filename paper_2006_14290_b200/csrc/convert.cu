@@ -142,10 +142,14 @@ sellp_fill_kernel(int64_t nrows, int log2ss, const int* __restrict__ ptrs, const
 // range passes nnz, read global memory directly. 27-point 200^3: SELL-P fill
 // 1.015 -> 0.876 ms, ELL fill 1.149 -> 0.838 ms (wider ELL tiles: 1 KB
 // contiguous stores per column instead of 512 B). (sparse.py:219-242.)
-constexpr int kFillCap = 4096;  // entries per stage (48 KB; 2 stages, 2 CTAs per SM)
+// entries per stage (48 KB). SELL-P fill: one stage, three CTAs per SM
+// (0.99 -> 0.90 ms for the 27-point 200^3 conversion: more CTAs beat the
+// in-CTA prefetch); ELL fill: two stages, two CTAs (one stage: 0.89 -> 0.95
+// ms). Grids are sized by the occupancy calculator.
+constexpr int kFillCap = 4096;
 
 template <int NS, bool kEll, int C = kFillCap>
-__global__ void __launch_bounds__(kConvThreads, 2)
+__global__ void __launch_bounds__(kConvThreads, NS == 1 ? 3 : 2)
 fill_tma_kernel(int64_t nrows, int log2r, int64_t ntiles, const int* __restrict__ ptrs, const int* __restrict__ col,
                 const double* __restrict__ val, const int64_t* __restrict__ sets, int64_t width, int64_t stride,
                 int* __restrict__ dcol, double* __restrict__ dval, int* __restrict__ dlen) {
@@ -265,7 +269,9 @@ int launch_fill_tma(int64_t nrows, int log2r, int64_t ntiles, const int* ptrs, c
                                      int(smem)));
         attr_set[dev & 63] = true;
     }
-    int64_t grid = int64_t(sm_count()) * 2;
+    int per_sm = 0;  // persistent grid: every CTA the SM can hold
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fill_tma_kernel<NS, kEll, C>, kConvThreads, smem));
+    int64_t grid = int64_t(sm_count()) * (per_sm > 0 ? per_sm : 1);
     if (grid > ntiles) grid = ntiles;
     fill_tma_kernel<NS, kEll, C><<<(unsigned)grid, kConvThreads, smem, st>>>(nrows, log2r, ntiles, ptrs, col, val, sets,
                                                                         width, stride, dcol, dval, dlen);
@@ -650,7 +656,7 @@ int wk_csr_to_sellp_fill(int64_t nrows, int64_t slice_size, const int32_t* row_p
     int l2 = 0;
     while ((int64_t(1) << l2) < slice_size) ++l2;
     if (slice_size >= 4 && slice_size <= 256 && al16(col_idx) && al16(values))
-        return launch_fill_tma<2, false>(nrows, l2, nslices, row_ptrs, col_idx, values, slice_sets, 0, 0, s_col,
+        return launch_fill_tma<1, false>(nrows, l2, nslices, row_ptrs, col_idx, values, slice_sets, 0, 0, s_col,
                                                s_val, nullptr, as_stream(stream));
     sellp_fill_kernel<<<(unsigned)nslices, kConvThreads, 0, as_stream(stream)>>>(nrows, l2, row_ptrs, col_idx, values,
                                                                                slice_sets, s_col, s_val);
